@@ -1,0 +1,237 @@
+/*
+ * probestream.h -- C ABI of the B200-native probe-streaming hot path.
+ *
+ * Drop-in boundary for the reference's Python entry points
+ * (/root/reference/pkg/src/probestream/).  Every entry point takes plain
+ * device pointers, sizes and a cudaStream_t passed as `void *`; none
+ * allocates (scratch comes from the caller, sized by the *_workspace_bytes
+ * queries) and none synchronises the stream.  All work is stream-ordered.
+ *
+ * Status codes map 1:1 onto the reference's exception classes; the Python
+ * shim (paper_2103_05875_b200/_native.py) re-raises the same classes.
+ * Validation the reference performs before mutating state happens here
+ * before any launch.
+ *
+ * Texel formats (volume.py:147-154): colour = uint32 (H, W) with R/G/B in
+ * bits 0-9/10-19/20-29; visibility = uint16 (H, W, 2) raw half bits.
+ * Probe p's block sits at block row p / probes_per_row, block column
+ * p % probes_per_row (volume.py:198-203).
+ */
+#ifndef PROBESTREAM_H
+#define PROBESTREAM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PS_ABI_VERSION 1
+
+/* status codes */
+#define PS_OK 0
+#define PS_ERR_VALUE (-1)         /* ValueError (packing.py:80, :120, :140)            */
+#define PS_ERR_LAYOUT (-2)        /* LayoutMismatchError(ValueError) (selection.py:25)  */
+#define PS_ERR_SLOT_OVERFLOW (-3) /* SlotOverflowError(RuntimeError) (packing.py:227)   */
+#define PS_ERR_INDEX (-4)         /* IndexError (volume.py:199, packing.py:273)         */
+#define PS_ERR_CUDA (-5)          /* RuntimeError: CUDA launch / runtime failure        */
+#define PS_ERR_WORKSPACE (-6)     /* ValueError: caller workspace too small             */
+
+#define PS_KIND_COLOR 0
+#define PS_KIND_VISIBILITY 1
+
+/* device-side status word bits (written by kernels, read by the shim) */
+#define PS_DEV_SLOT_OVERFLOW 1u   /* selection larger than slot_count, nothing mutated */
+#define PS_DEV_INDEX 2u           /* id outside [0, probe_count)                       */
+
+/* thread-local message for the last non-zero status */
+const char *ps_last_error(void);
+int ps_abi_version(void);
+/* number of SMs of the current device (grid sizing helper for the shim) */
+int ps_device_sm_count(void);
+
+/* ---------------------------------------------------------------------------
+ * Stage (4): plane packing.
+ * ------------------------------------------------------------------------- */
+
+/* pack_color (packing.py:73-89): texels uint32 (h, w) with row stride
+ * `row_stride` elements -> planes uint16 (3, h, w) contiguous. */
+int ps_pack_color(const uint32_t *texels, int64_t h, int64_t w, int64_t row_stride,
+                  uint16_t *planes, void *stream);
+
+/* widened_width (packing.py:105-109) = ceil(4w/3); -1 if w < 0 */
+int64_t ps_widened_width(int64_t w);
+
+/* pack_visibility (packing.py:112-133): texels uint16 (h, w, 2) with row
+ * stride `row_stride` texels -> planes uint8 (3, h, ceil(4w/3)) contiguous. */
+int ps_pack_visibility(const uint16_t *texels, int64_t h, int64_t w, int64_t row_stride,
+                       uint8_t *planes, void *stream);
+
+/* unpack_* (packing.py:92-99, :136-151): client-side inverses, used as
+ * round-trip verifiers. */
+int ps_unpack_color(const uint16_t *planes, int64_t h, int64_t w, uint32_t *texels,
+                    void *stream);
+int ps_unpack_visibility(const uint8_t *planes, int64_t h, int64_t w, uint16_t *texels,
+                         void *stream);
+
+/* Temporal delta (codec.py:207-215 residual, :250-272 SKIP rule) over plane
+ * sets of `elem_bytes` (2 = colour uint16, 1 = visibility uint8) elements,
+ * shape (3, h, w).  residual = (cur - prev) mod 2^bits; skip is uint8
+ * (3, ceil(h/16), ceil(w/16)), 1 where the clipped 16x16 block is
+ * bit-identical.  prev == NULL is a key frame: residual untouched, skip 0. */
+int ps_temporal_delta(int elem_bytes, const void *cur, const void *prev, int64_t h,
+                      int64_t w, void *residual, uint8_t *skip, void *stream);
+
+/* Fused pack + temporal delta over a whole update atlas: writes planes_cur,
+ * residual (vs planes_prev) and skip in one pass.  planes_prev == NULL is a
+ * key frame (residual untouched, skip 0). */
+int ps_pack_delta(int kind, const void *texels, int64_t h, int64_t w, int64_t row_stride,
+                  void *planes_cur, const void *planes_prev, void *residual,
+                  uint8_t *skip, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Stage (3): change detection and compaction (selection.py:284-323).
+ * ------------------------------------------------------------------------- */
+
+/* threshold handling mirrors the reference's numpy promotion:
+ *   threshold <= 0                  -> exact bit compare of the full block;
+ *   colour, threshold > 0 (or NaN)  -> max channel |delta| > threshold;
+ *   visibility, threshold > 0/NaN   -> |f32(a)-f32(b)| > thr OR (NaN delta and
+ *                                      bits differ); thr is compared as float32
+ *                                      unless threshold_is_f64 (a numpy float64
+ *                                      scalar in the caller). */
+size_t ps_detect_workspace_bytes(int64_t probe_count);
+int ps_detect_changed(int kind, const void *rendered, const void *last_sent,
+                      int64_t probe_count, int64_t probes_per_row, int64_t block_rows,
+                      const uint8_t *active, double threshold, int threshold_is_f64,
+                      uint32_t *changed_bits, int64_t *out_ids, int64_t *out_count,
+                      void *workspace, size_t workspace_bytes, void *stream);
+
+/* Bitmap <-> id list helpers.  ids_to_bits ORs ids[0..n) (n read from
+ * n_dev when non-NULL, else n_host) into bits (caller zeroes) and sets
+ * PS_DEV_INDEX in *status_dev for ids outside [0, probe_count).
+ * bits_to_ids writes ascending ids (flatnonzero) and the count. */
+int ps_ids_to_bits(const int64_t *ids, const int64_t *n_dev, int64_t n_host,
+                   int64_t probe_count, uint32_t *bits, uint32_t *status_dev, void *stream);
+size_t ps_compact_workspace_bytes(int64_t probe_count);
+int ps_bits_to_ids(const uint32_t *bits, int64_t probe_count, int64_t *out_ids,
+                   int64_t *out_count, void *workspace, size_t workspace_bytes, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Stage (3) tail: budgeted selection (selection.py:413-437).
+ * candidates = changed & pvs & active (bitmaps; pvs_bits NULL = all), ordered
+ * by staleness (current_seq - last_sent_seq[p]) descending then id
+ * ascending, truncated with python slice semantics when has_budget.
+ * ------------------------------------------------------------------------- */
+size_t ps_select_workspace_bytes(int64_t probe_count);
+int ps_select(const uint32_t *changed_bits, const uint32_t *pvs_bits, const uint8_t *active,
+              const int64_t *last_sent_seq, int64_t current_seq, int64_t probe_count,
+              int has_budget, int64_t budget, int64_t *out_ids, int64_t *out_count,
+              void *workspace, size_t workspace_bytes, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Stage (4): update-atlas slot cache (packing.py:243-317) and build
+ * (packing.py:320-338).  Slot state lives in device memory:
+ *   probe_slot int32[probe_count] (-1 = none), slot_probe int32[slot_count],
+ *   last_selected int64[probe_count], meta int64[4] = {tick, used, -, -}.
+ * ------------------------------------------------------------------------- */
+size_t ps_assign_workspace_bytes(int64_t probe_count, int64_t slot_count);
+/* selected ids (any order, duplicates allowed): n from n_dev if non-NULL. On
+ * overflow nothing is mutated, *status_dev |= PS_DEV_SLOT_OVERFLOW and
+ * entry_count = 0.  entries = (slot, probe) int64 pairs sorted by slot. */
+int ps_assign_slots(const int64_t *selected, const int64_t *n_dev, int64_t n_host,
+                    int64_t probe_count, int64_t slot_count, int32_t *probe_slot,
+                    int32_t *slot_probe, int64_t *last_selected, int64_t *meta,
+                    int64_t *entries, int64_t *entry_count, uint32_t *status_dev,
+                    void *workspace, size_t workspace_bytes, void *stream);
+
+/* Copy each entry's stripped core (block[1:-1,1:-1]) into its slot region of
+ * update_texels (packing.py:335-337).  Optional commit: when
+ * last_sent != NULL also copies the full block into last_sent and stamps
+ * last_sent_seq[p] = current_seq.  Work is bounded by *entry_count (device). */
+int ps_build_update(int kind, const void *source, int64_t probe_count,
+                    int64_t probes_per_row, const int64_t *entries,
+                    const int64_t *entry_count, int64_t max_entries, int64_t slots_per_row,
+                    void *update_texels, int64_t update_row_stride, void *last_sent,
+                    int64_t *last_sent_seq, int64_t current_seq, void *stream);
+
+/* Guard-band reconstruct over a whole atlas (packing.py:180-196 applied to
+ * every probe block): rewrites each block's border from its core. */
+int ps_reconstruct_guard_bands(int kind, void *atlas, int64_t probe_count,
+                               int64_t probes_per_row, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Stages (1)+(2): probe ray tracing and DDGI blend (new API, no reference
+ * implementation).
+ * ------------------------------------------------------------------------- */
+
+/* BVH: built on the host (binned SAH), uploaded by the shim. */
+typedef struct ps_bvh_sizes {
+    int64_t node_count;  /* 64-byte nodes          */
+    int64_t tri_count;   /* triangles after build  */
+    int64_t tri_slots;   /* 48-byte triangle records incl. leaf terminators */
+} ps_bvh_sizes;
+
+/* Build a BVH2 over `tri_count` triangles given as float64 vertices
+ * (tri_count, 3, 3).  Writes host arrays: nodes (node_count * 16 floats),
+ * tris (tri_slots * 12 floats).  Two-call protocol: pass NULL outputs to
+ * query sizes. */
+int ps_bvh_build(const double *vertices, int64_t tri_count, int leaf_size,
+                 ps_bvh_sizes *sizes, float *nodes_out, float *tris_out);
+
+/* Trace parameters (device pointers inside). */
+typedef struct ps_trace_params {
+    /* probe grid (volume.py:68-144) */
+    int32_t nx, ny, nz;
+    int32_t probe_begin;     /* first probe id handled (slab sharding)   */
+    int32_t probe_end;       /* one past the last probe id handled       */
+    double origin[3];
+    double spacing[3];
+    /* rays: directions for this frame (rays_per_probe, 4) float, shared by
+     * every probe (one random rotation per frame) */
+    const float *ray_dirs;
+    int32_t rays_per_probe;
+    /* scene */
+    const float *nodes;      /* BVH2 nodes */
+    const float *tris;       /* triangle records */
+    const float *materials;  /* per original triangle: albedo rgb, emission rgb (6 floats) */
+    int32_t light_count;
+    const float *lights;     /* per light: position xyz, intensity rgb (6 floats) */
+    float sky[3];
+    float max_distance;
+    float normal_bias;
+    int32_t shadows;         /* trace a shadow ray per light at each hit */
+    /* blend */
+    const float *w_color;    /* (rays, 64) cosine weights, transposed       */
+    const float *w_depth;    /* (rays, 256) cosine^sharpness weights        */
+    const float *inv_wsum;   /* (64 + 256) reciprocal weight sums            */
+    float hysteresis;        /* 0 on the first frame                        */
+    float irradiance_scale;  /* colour unorm = irradiance / scale            */
+    /* state (float, persistent across frames) */
+    float *irradiance;       /* (probe_count, 64, 3)  */
+    float *moments;          /* (probe_count, 256, 2) */
+    /* outputs: atlases with guard bands (volume.py:147) */
+    uint32_t *color_atlas;
+    uint16_t *vis_atlas;
+    int32_t probes_per_row_color;
+    int32_t probes_per_row_vis;
+    /* optional per-ray debug record (probe_count_local * rays, 8 floats:
+     * radiance rgb, depth, hit t, prim id bits, pad, pad); NULL = off */
+    float *ray_records;
+} ps_trace_params;
+
+/* Per-frame weights: from ray_dirs and the texel directions
+ * (texdir: 64*4 colour then 256*4 depth floats), writes w_color, w_depth,
+ * inv_wsum. */
+int ps_blend_weights(const float *ray_dirs, int32_t rays_per_probe, const float *texdir,
+                     float sharpness, float *w_color, float *w_depth, float *inv_wsum,
+                     void *stream);
+
+int ps_trace_blend(const ps_trace_params *params, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PROBESTREAM_H */

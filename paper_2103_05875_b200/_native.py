@@ -1,0 +1,147 @@
+"""ctypes binding of ``libprobestream.so`` (the C ABI in include/probestream.h).
+
+There is no fallback: importing the package on a machine where the library
+is missing raises ``NativeLibraryError`` the first time a native entry point
+is needed, and every status code is converted into the reference's exception
+class.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+from pathlib import Path
+
+from .errors import LayoutMismatchError, NativeLibraryError, SlotOverflowError
+
+LIB_PATH = Path(os.environ.get("PROBESTREAM_LIB", Path(__file__).resolve().parent / "libprobestream.so"))
+ABI_VERSION = 1
+
+PS_OK = 0
+PS_ERR_VALUE = -1
+PS_ERR_LAYOUT = -2
+PS_ERR_SLOT_OVERFLOW = -3
+PS_ERR_INDEX = -4
+PS_ERR_CUDA = -5
+PS_ERR_WORKSPACE = -6
+
+PS_KIND_COLOR = 0
+PS_KIND_VISIBILITY = 1
+
+PS_DEV_SLOT_OVERFLOW = 1
+PS_DEV_INDEX = 2
+
+_vp, _i64, _i32, _f32, _f64, _sz = C.c_void_p, C.c_int64, C.c_int32, C.c_float, C.c_double, C.c_size_t
+_int = C.c_int
+
+
+class BvhSizes(C.Structure):
+    _fields_ = [("node_count", _i64), ("tri_count", _i64), ("tri_slots", _i64)]
+
+
+class TraceParams(C.Structure):
+    _fields_ = [
+        ("nx", _i32), ("ny", _i32), ("nz", _i32),
+        ("probe_begin", _i32), ("probe_end", _i32),
+        ("origin", _f64 * 3), ("spacing", _f64 * 3),
+        ("ray_dirs", _vp), ("rays_per_probe", _i32),
+        ("nodes", _vp), ("tris", _vp), ("materials", _vp),
+        ("light_count", _i32), ("lights", _vp),
+        ("sky", _f32 * 3), ("max_distance", _f32), ("normal_bias", _f32),
+        ("shadows", _i32),
+        ("w_color", _vp), ("w_depth", _vp), ("inv_wsum", _vp),
+        ("hysteresis", _f32), ("irradiance_scale", _f32),
+        ("irradiance", _vp), ("moments", _vp),
+        ("color_atlas", _vp), ("vis_atlas", _vp),
+        ("probes_per_row_color", _i32), ("probes_per_row_vis", _i32),
+        ("ray_records", _vp),
+    ]
+
+
+_SIGNATURES = {
+    "ps_last_error": (C.c_char_p, []),
+    "ps_abi_version": (_int, []),
+    "ps_device_sm_count": (_int, []),
+    "ps_pack_color": (_int, [_vp, _i64, _i64, _i64, _vp, _vp]),
+    "ps_widened_width": (_i64, [_i64]),
+    "ps_pack_visibility": (_int, [_vp, _i64, _i64, _i64, _vp, _vp]),
+    "ps_unpack_color": (_int, [_vp, _i64, _i64, _vp, _vp]),
+    "ps_unpack_visibility": (_int, [_vp, _i64, _i64, _vp, _vp]),
+    "ps_temporal_delta": (_int, [_int, _vp, _vp, _i64, _i64, _vp, _vp, _vp]),
+    "ps_pack_delta": (_int, [_int, _vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp]),
+    "ps_detect_workspace_bytes": (_sz, [_i64]),
+    "ps_detect_changed": (_int, [_int, _vp, _vp, _i64, _i64, _i64, _vp, _f64, _int,
+                                 _vp, _vp, _vp, _vp, _sz, _vp]),
+    "ps_ids_to_bits": (_int, [_vp, _vp, _i64, _i64, _vp, _vp, _vp]),
+    "ps_compact_workspace_bytes": (_sz, [_i64]),
+    "ps_bits_to_ids": (_int, [_vp, _i64, _vp, _vp, _vp, _sz, _vp]),
+    "ps_select_workspace_bytes": (_sz, [_i64]),
+    "ps_select": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _int, _i64, _vp, _vp, _vp, _sz, _vp]),
+    "ps_assign_workspace_bytes": (_sz, [_i64, _i64]),
+    "ps_assign_slots": (_int, [_vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp,
+                               _vp, _vp, _sz, _vp]),
+    "ps_build_update": (_int, [_int, _vp, _i64, _i64, _vp, _vp, _i64, _i64, _vp, _i64, _vp,
+                               _vp, _i64, _vp]),
+    "ps_reconstruct_guard_bands": (_int, [_int, _vp, _i64, _i64, _vp]),
+    "ps_bvh_build": (_int, [_vp, _i64, _int, C.POINTER(BvhSizes), _vp, _vp]),
+    "ps_blend_weights": (_int, [_vp, _i32, _vp, _f32, _vp, _vp, _vp, _vp]),
+    "ps_trace_blend": (_int, [C.POINTER(TraceParams), _vp]),
+}
+
+# entry points of stages (1)+(2) still being brought up; remove once exported
+_PENDING = {"ps_bvh_build", "ps_blend_weights", "ps_trace_blend"}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def lib():
+    """The loaded library (loads on first use; raises if it is missing)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not LIB_PATH.exists():
+            raise NativeLibraryError(
+                f"{LIB_PATH} not found: build it with "
+                "`python -m paper_2103_05875_b200.build_native` (no CPU fallback exists)")
+        handle = C.CDLL(str(LIB_PATH))
+        for name, (res, args) in _SIGNATURES.items():
+            fn = getattr(handle, name, None)
+            if fn is None:
+                if name in _PENDING:
+                    continue
+                raise NativeLibraryError(f"{LIB_PATH} does not export {name}")
+            fn.restype = res
+            fn.argtypes = args
+        if handle.ps_abi_version() != ABI_VERSION:
+            raise NativeLibraryError("libprobestream ABI version mismatch; rebuild")
+        _lib = handle
+        return _lib
+
+
+def exported_symbols():
+    return list(_SIGNATURES)
+
+
+def check(status: int, what: str = "") -> None:
+    if status == PS_OK:
+        return
+    msg = lib().ps_last_error().decode(errors="replace")
+    text = f"{what}: {msg}" if what else msg
+    if status == PS_ERR_LAYOUT:
+        raise LayoutMismatchError(text)
+    if status == PS_ERR_SLOT_OVERFLOW:
+        raise SlotOverflowError(text)
+    if status == PS_ERR_INDEX:
+        raise IndexError(text)
+    if status in (PS_ERR_VALUE, PS_ERR_WORKSPACE):
+        raise ValueError(text)
+    raise RuntimeError(text)
+
+
+def call(name: str, *args) -> None:
+    check(getattr(lib(), name)(*args), name)

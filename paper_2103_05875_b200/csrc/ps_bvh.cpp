@@ -1,0 +1,288 @@
+// Host BVH2 builder (binned SAH) for the probe ray tracer.
+//
+// The reference has no acceleration structure: SceneGeometry.raycast
+// (selection.py:66-149) tests every ray against every primitive.  B200 has no
+// RT cores, so stage (1) traverses a BVH in SIMT code (csrc/ps_trace.cu);
+// this file builds it once per scene on the host.
+//
+// GPU layout (all little-endian float words):
+//   node  = 16 floats: [c0.lo.x c0.hi.x c0.lo.y c0.hi.y]
+//                      [c1.lo.x c1.hi.x c1.lo.y c1.hi.y]
+//                      [c0.lo.z c0.hi.z c1.lo.z c1.hi.z]
+//                      [child0  child1  0       0      ]  (int bits)
+//           child >= 0: inner node index; child < 0: leaf at tri record ~child
+//   tri   = 12 floats: [v0.xyz prim] [e1.xyz 0] [e2.xyz 0]; a record whose
+//           prim word is -1 terminates a leaf.
+// Edges are formed in double (v1 - v0, v2 - v0) and rounded once to float,
+// the same construction the Moller-Trumbore test of the reference uses
+// (selection.py:124-126).
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <limits>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "probestream.h"
+
+namespace ps {
+void set_last_error(const std::string &msg);
+}
+
+namespace {
+
+struct Aabb {
+    double lo[3] = {std::numeric_limits<double>::infinity(), std::numeric_limits<double>::infinity(),
+                    std::numeric_limits<double>::infinity()};
+    double hi[3] = {-std::numeric_limits<double>::infinity(), -std::numeric_limits<double>::infinity(),
+                    -std::numeric_limits<double>::infinity()};
+    void grow(const Aabb &b) {
+        for (int k = 0; k < 3; ++k) {
+            lo[k] = std::min(lo[k], b.lo[k]);
+            hi[k] = std::max(hi[k], b.hi[k]);
+        }
+    }
+    void grow(const double *p) {
+        for (int k = 0; k < 3; ++k) {
+            lo[k] = std::min(lo[k], p[k]);
+            hi[k] = std::max(hi[k], p[k]);
+        }
+    }
+    double area() const {
+        double d[3];
+        for (int k = 0; k < 3; ++k) d[k] = std::max(0.0, hi[k] - lo[k]);
+        return 2.0 * (d[0] * d[1] + d[1] * d[2] + d[2] * d[0]);
+    }
+};
+
+struct BuildNode {
+    Aabb box;
+    int left = -1, right = -1;  // children (inner)
+    int first = 0, count = 0;   // primitive range (leaf)
+};
+
+struct Builder {
+    const double *v;
+    std::vector<Aabb> tri_box;
+    std::vector<double> centroid;
+    std::vector<int> order;
+    std::vector<BuildNode> nodes;
+    int leaf_size;
+    static constexpr int BINS = 32;
+
+    int build(int first, int count) {
+        BuildNode node;
+        for (int i = first; i < first + count; ++i) node.box.grow(tri_box[order[i]]);
+        node.first = first;
+        node.count = count;
+        const int id = int(nodes.size());
+        nodes.push_back(node);
+        if (count <= 1) return id;
+        // centroid bounds
+        Aabb cb;
+        for (int i = first; i < first + count; ++i) cb.grow(&centroid[3 * order[i]]);
+        double best_cost = std::numeric_limits<double>::infinity();
+        int best_axis = -1, best_split = -1;
+        for (int axis = 0; axis < 3; ++axis) {
+            const double lo = cb.lo[axis], ext = cb.hi[axis] - cb.lo[axis];
+            if (!(ext > 0.0)) continue;
+            Aabb bin_box[BINS];
+            int bin_cnt[BINS] = {0};
+            const double scale = BINS / ext;
+            for (int i = first; i < first + count; ++i) {
+                int b = int((centroid[3 * order[i] + axis] - lo) * scale);
+                b = std::min(std::max(b, 0), BINS - 1);
+                bin_cnt[b]++;
+                bin_box[b].grow(tri_box[order[i]]);
+            }
+            double left_area[BINS];
+            int left_cnt[BINS];
+            Aabb acc;
+            int cnt = 0;
+            for (int b = 0; b < BINS - 1; ++b) {
+                acc.grow(bin_box[b]);
+                cnt += bin_cnt[b];
+                left_area[b] = cnt ? acc.area() : 0.0;
+                left_cnt[b] = cnt;
+            }
+            Aabb racc;
+            int rcnt = 0;
+            for (int b = BINS - 1; b > 0; --b) {
+                racc.grow(bin_box[b]);
+                rcnt += bin_cnt[b];
+                const int lc = left_cnt[b - 1];
+                if (lc == 0 || rcnt == 0) continue;
+                const double cost = left_area[b - 1] * lc + racc.area() * rcnt;
+                if (cost < best_cost) {
+                    best_cost = cost;
+                    best_axis = axis;
+                    best_split = b;
+                }
+            }
+        }
+        const double parent_area = nodes[id].box.area();
+        const double leaf_cost = parent_area * count;
+        // traversal cost ~ 1 box pair per node vs 1 triangle per primitive
+        const double split_cost = 1.2 * parent_area + best_cost;
+        if (best_axis < 0) {
+            if (count <= leaf_size) return id;
+            // coincident centroids: split the range in half by index
+            const int half = count / 2;
+            const int l = build(first, half);
+            const int r = build(first + half, count - half);
+            nodes[id].left = l;
+            nodes[id].right = r;
+            return id;
+        }
+        if (count <= leaf_size && leaf_cost <= split_cost) return id;
+        const double lo = cb.lo[best_axis];
+        const double scale = BINS / (cb.hi[best_axis] - cb.lo[best_axis]);
+        auto mid_it = std::partition(order.begin() + first, order.begin() + first + count, [&](int t) {
+            int b = int((centroid[3 * t + best_axis] - lo) * scale);
+            b = std::min(std::max(b, 0), BINS - 1);
+            return b < best_split;
+        });
+        int mid = int(mid_it - order.begin());
+        if (mid == first || mid == first + count) mid = first + count / 2;
+        int l = build(first, mid - first);
+        int r = build(mid, first + count - mid);
+        nodes[id].left = l;
+        nodes[id].right = r;
+        return id;
+    }
+};
+
+}  // namespace
+
+extern "C" int ps_bvh_build(const double *vertices, int64_t tri_count, int leaf_size,
+                            ps_bvh_sizes *sizes, float *nodes_out, float *tris_out) {
+    try {
+        if (!sizes) throw std::invalid_argument("sizes must not be NULL");
+        if (tri_count < 1) throw std::invalid_argument("scene needs at least one triangle");
+        if (tri_count > (int64_t(1) << 30)) throw std::invalid_argument("too many triangles");
+        if (leaf_size < 1 || leaf_size > 16) throw std::invalid_argument("leaf_size in [1, 16]");
+        Builder b;
+        b.v = vertices;
+        b.leaf_size = leaf_size;
+        const int n = int(tri_count);
+        b.tri_box.resize(n);
+        b.centroid.resize(3 * size_t(n));
+        b.order.resize(n);
+        for (int t = 0; t < n; ++t) {
+            const double *p = vertices + 9 * size_t(t);
+            for (int k = 0; k < 3; ++k) b.tri_box[t].grow(p + 3 * k);
+            for (int a = 0; a < 3; ++a) b.centroid[3 * t + a] = (p[a] + p[3 + a] + p[6 + a]) / 3.0;
+            b.order[t] = t;
+        }
+        b.nodes.reserve(2 * size_t(n));
+        b.build(0, n);
+        // Flatten: inner nodes get GPU indices in DFS order (left child first);
+        // a scene that is a single leaf gets a root whose two children are
+        // that leaf and an empty box.
+        std::vector<int> gpu_index(b.nodes.size(), -1);
+        std::vector<int> inner;
+        std::vector<int> stack{0};
+        while (!stack.empty()) {
+            int id = stack.back();
+            stack.pop_back();
+            if (b.nodes[id].left < 0) continue;
+            gpu_index[id] = int(inner.size());
+            inner.push_back(id);
+            stack.push_back(b.nodes[id].right);
+            stack.push_back(b.nodes[id].left);
+        }
+        const bool single_leaf = inner.empty();
+        const int64_t node_count = single_leaf ? 1 : int64_t(inner.size());
+        // leaves in DFS order, each followed by a terminator record
+        std::vector<int> leaves;
+        std::vector<int> leaf_slot(b.nodes.size(), -1);
+        int64_t slots = 0;
+        {
+            std::vector<int> st{0};
+            while (!st.empty()) {
+                int id = st.back();
+                st.pop_back();
+                if (b.nodes[id].left < 0) {
+                    leaf_slot[id] = int(slots);
+                    leaves.push_back(id);
+                    slots += b.nodes[id].count + 1;
+                } else {
+                    st.push_back(b.nodes[id].right);
+                    st.push_back(b.nodes[id].left);
+                }
+            }
+        }
+        sizes->node_count = node_count;
+        sizes->tri_count = tri_count;
+        sizes->tri_slots = slots + (single_leaf ? 1 : 0);
+        if (!nodes_out || !tris_out) return PS_OK;
+
+        auto child_ref = [&](int id) -> int32_t {
+            if (b.nodes[id].left >= 0) return gpu_index[id];
+            return ~int32_t(leaf_slot[id]);
+        };
+        auto put_box = [](float *nd, int which, const Aabb &bx) {
+            // round outward so the float box contains the double box
+            auto dn = [](double x) { float f = float(x); return double(f) > x ? std::nextafter(f, -INFINITY) : f; };
+            auto up = [](double x) { float f = float(x); return double(f) < x ? std::nextafter(f, INFINITY) : f; };
+            nd[which * 4 + 0] = dn(bx.lo[0]);
+            nd[which * 4 + 1] = up(bx.hi[0]);
+            nd[which * 4 + 2] = dn(bx.lo[1]);
+            nd[which * 4 + 3] = up(bx.hi[1]);
+            nd[8 + which * 2 + 0] = dn(bx.lo[2]);
+            nd[8 + which * 2 + 1] = up(bx.hi[2]);
+        };
+        auto set_int = [](float *f, int32_t v) { std::memcpy(f, &v, 4); };
+        if (single_leaf) {
+            float *nd = nodes_out;
+            std::memset(nd, 0, 64);
+            put_box(nd, 0, b.nodes[0].box);
+            Aabb empty;  // inverted box never hits
+            nd[4] = 1.f; nd[5] = -1.f; nd[6] = 1.f; nd[7] = -1.f; nd[10] = 1.f; nd[11] = -1.f;
+            (void)empty;
+            set_int(nd + 12, ~int32_t(0));
+            set_int(nd + 13, ~int32_t(slots));  // points at a lone terminator
+        } else {
+            for (size_t g = 0; g < inner.size(); ++g) {
+                const BuildNode &bn = b.nodes[inner[g]];
+                float *nd = nodes_out + 16 * g;
+                std::memset(nd, 0, 64);
+                put_box(nd, 0, b.nodes[bn.left].box);
+                put_box(nd, 1, b.nodes[bn.right].box);
+                set_int(nd + 12, child_ref(bn.left));
+                set_int(nd + 13, child_ref(bn.right));
+            }
+        }
+        int64_t s = 0;
+        for (int id : leaves) {
+            const BuildNode &bn = b.nodes[id];
+            for (int i = bn.first; i < bn.first + bn.count; ++i) {
+                const int t = b.order[i];
+                const double *p = vertices + 9 * size_t(t);
+                float *r = tris_out + 12 * s;
+                r[0] = float(p[0]); r[1] = float(p[1]); r[2] = float(p[2]);
+                set_int(r + 3, t);
+                r[4] = float(p[3] - p[0]); r[5] = float(p[4] - p[1]); r[6] = float(p[5] - p[2]);
+                r[7] = 0.f;
+                r[8] = float(p[6] - p[0]); r[9] = float(p[7] - p[1]); r[10] = float(p[8] - p[2]);
+                r[11] = 0.f;
+                ++s;
+            }
+            float *term = tris_out + 12 * s;
+            std::memset(term, 0, 48);
+            set_int(term + 3, -1);
+            ++s;
+        }
+        if (single_leaf) {
+            float *term = tris_out + 12 * s;
+            std::memset(term, 0, 48);
+            set_int(term + 3, -1);
+        }
+        return PS_OK;
+    } catch (const std::exception &e) {
+        ps::set_last_error(e.what());
+        return PS_ERR_VALUE;
+    }
+}

@@ -1,0 +1,86 @@
+// Shared helpers for the probestream CUDA library (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+#include "probestream.h"
+
+#ifndef __CUDA_ARCH__
+#else
+#if __CUDA_ARCH__ < 1000
+#error "probestream kernels target sm_100a only"
+#endif
+#endif
+
+namespace ps {
+
+// error carrying a status code; converted to (status, thread-local message)
+// at the C boundary by PS_ABI_BEGIN/END.
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string &m) : std::runtime_error(m), code(c) {}
+};
+
+void set_last_error(const std::string &msg);
+
+[[noreturn]] inline void fail(int code, const std::string &msg) { throw Error(code, msg); }
+
+inline void check_cuda(cudaError_t e, const char *what) {
+    if (e != cudaSuccess) {
+        fail(PS_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    }
+}
+
+inline void check_launch(const char *what) { check_cuda(cudaGetLastError(), what); }
+
+inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline int sm_count() {
+    static int cached = 0;
+    if (!cached) {
+        int dev = 0;
+        check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+        check_cuda(cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev),
+                   "cudaDeviceGetAttribute");
+    }
+    return cached;
+}
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// carve aligned sub-buffers out of a caller workspace
+struct Carver {
+    char *base;
+    size_t cap, off = 0;
+    Carver(void *b, size_t c) : base(static_cast<char *>(b)), cap(c) {}
+    template <class T>
+    T *take(size_t n) {
+        off = (off + 255) & ~size_t(255);
+        T *p = reinterpret_cast<T *>(base ? base + off : nullptr);
+        off += n * sizeof(T);
+        return p;
+    }
+    void check() const {
+        if (off > cap) fail(PS_ERR_WORKSPACE, "workspace too small");
+    }
+};
+
+}  // namespace ps
+
+#define PS_ABI_BEGIN try {
+#define PS_ABI_END                                  \
+    return PS_OK;                                   \
+    }                                               \
+    catch (const ps::Error &e) {                    \
+        ps::set_last_error(e.what());               \
+        return e.code;                              \
+    }                                               \
+    catch (const std::exception &e) {               \
+        ps::set_last_error(e.what());               \
+        return PS_ERR_CUDA;                         \
+    }

@@ -1,0 +1,409 @@
+// Stage (4): lossless plane packing + temporal delta (+ SKIP map), sm_100a.
+//
+// One kernel family covers pack_color (packing.py:73-89), pack_visibility
+// (packing.py:112-133) and the codec's temporal residual / SKIP rule
+// (codec.py:207-215, :250-272).  The unit of work is a 16-element row
+// segment of a plane, which is exactly one row of one 16x16 codec block:
+//   colour     : 16 texels (64 B)      -> 16 uint16 per plane
+//   visibility : 12 texels (48 B)      -> 16 uint8 per plane  (48 stream bytes)
+// so the SKIP decision of a block is an OR over the 16 threads that own its
+// rows, and every byte is read once and written once (HBM-bound).
+#include <cuda_runtime.h>
+
+#include <mutex>
+#include <string>
+
+#include "ps_common.cuh"
+
+namespace ps {
+
+static thread_local std::string g_last_error;
+void set_last_error(const std::string &msg) { g_last_error = msg; }
+
+namespace {
+
+constexpr int SEG = 16;     // elements per plane per thread == codec block side
+constexpr int TILE_X = 16;  // segments (codec blocks) per CTA in x
+constexpr int TILE_Y = 16;  // rows per CTA == codec block side
+
+__device__ __forceinline__ uint32_t bfe10(uint32_t t, int e) { return (t >> (10 * e)) & 0x3FFu; }
+
+// Visibility: 3 texel words (R | G << 16, little endian) -> 4 plane bytes per
+// plane.  Stream per texel is [R.hi, R.lo, G.hi, G.lo]; byte k of the 12-byte
+// stream goes to plane k % 3, element k / 3.
+__device__ __forceinline__ void vis_group(uint32_t t0, uint32_t t1, uint32_t t2, uint32_t &y,
+                                          uint32_t &u, uint32_t &v) {
+    // stream bytes: s0=t0.b1 s1=t0.b0 s2=t0.b3 s3=t0.b2 s4=t1.b1 s5=t1.b0
+    //               s6=t1.b3 s7=t1.b2 s8=t2.b1 s9=t2.b0 s10=t2.b3 s11=t2.b2
+    // Y = s0 s3 s6 s9 ; U = s1 s4 s7 s10 ; V = s2 s5 s8 s11
+    // __byte_perm(x, y, sel): result byte i = byte sel_i of {y:x} (x: 0..3, y: 4..7)
+    y = __byte_perm(__byte_perm(t0, t1, 0x0721), t2, 0x4210);  // t0.b1 t0.b2 t1.b3 t2.b0
+    u = __byte_perm(__byte_perm(t0, t1, 0x0650), t2, 0x7210);  // t0.b0 t1.b1 t1.b2 t2.b3
+    v = __byte_perm(__byte_perm(t0, t1, 0x0043), t2, 0x6510);  // t0.b3 t1.b0 t2.b1 t2.b2
+}
+
+struct PackArgs {
+    const uint8_t *texels;  // colour u32 / visibility u16x2 texel rows
+    int64_t h, w;           // texel rows / texels per row
+    int64_t row_stride_b;   // texel row stride in bytes
+    int64_t pw;             // plane width in elements
+    int64_t nseg;           // segments (16-element blocks) per row
+    uint8_t *cur;           // planes (3, h, pw)
+    const uint8_t *prev;    // previous planes or nullptr
+    uint8_t *residual;      // may be nullptr
+    uint8_t *skip;          // (3, ceil(h/16), nseg) or nullptr
+    int vec_in;             // texel rows 16-byte aligned
+    int vec_out;            // plane rows 16-byte aligned
+};
+
+// Loads the 16-element segment `seg` of row `r` for all three planes into
+// `out` as 32-bit words (colour: 8 words of 2 x u16; visibility: 4 words of
+// 4 x u8).  Elements beyond the plane width are zero.
+template <int KIND>
+__device__ __forceinline__ void load_segment(const PackArgs &a, int64_t r, int64_t seg,
+                                             uint32_t out[3][8]) {
+    const uint8_t *row = a.texels + r * a.row_stride_b;
+    if (KIND == PS_KIND_COLOR) {
+        const int64_t x0 = seg * SEG;
+        uint32_t t[16];
+        if (a.vec_in && x0 + 16 <= a.w) {
+            const uint4 *p = reinterpret_cast<const uint4 *>(row + x0 * 4);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                uint4 q = __ldg(p + i);
+                t[4 * i] = q.x;
+                t[4 * i + 1] = q.y;
+                t[4 * i + 2] = q.z;
+                t[4 * i + 3] = q.w;
+            }
+        } else {
+            const uint32_t *p = reinterpret_cast<const uint32_t *>(row);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) t[i] = (x0 + i < a.w) ? __ldg(p + x0 + i) : 0u;
+        }
+#pragma unroll
+        for (int e = 0; e < 3; ++e)
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                out[e][i] = bfe10(t[2 * i], e) | (bfe10(t[2 * i + 1], e) << 16);
+    } else {
+        const int64_t t0 = seg * 12;  // first texel of the 48-byte stream window
+        uint32_t t[12];
+        if (a.vec_in && t0 + 12 <= a.w) {
+            const uint4 *p = reinterpret_cast<const uint4 *>(row + t0 * 4);
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                uint4 q = __ldg(p + i);
+                t[4 * i] = q.x;
+                t[4 * i + 1] = q.y;
+                t[4 * i + 2] = q.z;
+                t[4 * i + 3] = q.w;
+            }
+        } else {
+            const uint32_t *p = reinterpret_cast<const uint32_t *>(row);
+#pragma unroll
+            for (int i = 0; i < 12; ++i) t[i] = (t0 + i < a.w) ? __ldg(p + t0 + i) : 0u;
+        }
+#pragma unroll
+        for (int g = 0; g < 4; ++g) vis_group(t[3 * g], t[3 * g + 1], t[3 * g + 2], out[0][g],
+                                              out[1][g], out[2][g]);
+#pragma unroll
+        for (int e = 0; e < 3; ++e)
+#pragma unroll
+            for (int i = 4; i < 8; ++i) out[e][i] = 0u;
+    }
+}
+
+template <int KIND>
+__device__ __forceinline__ void load_plane_words(const uint8_t *base, int64_t x0_b,
+                                                 int64_t valid_b, bool vec, uint32_t w[8]) {
+    constexpr int NB = (KIND == PS_KIND_COLOR) ? 32 : 16;  // bytes per segment
+    const uint8_t *p = base + x0_b;
+    if (vec && valid_b >= NB) {
+        const uint4 *q = reinterpret_cast<const uint4 *>(p);
+#pragma unroll
+        for (int i = 0; i < NB / 16; ++i) {
+            uint4 v = __ldg(q + i);
+            w[4 * i] = v.x;
+            w[4 * i + 1] = v.y;
+            w[4 * i + 2] = v.z;
+            w[4 * i + 3] = v.w;
+        }
+#pragma unroll
+        for (int i = NB / 4; i < 8; ++i) w[i] = 0u;
+    } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            uint32_t v = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                int64_t b = 4 * i + k;
+                if (b < NB && b < valid_b) v |= uint32_t(p[b]) << (8 * k);
+            }
+            w[i] = v;
+        }
+    }
+}
+
+template <int KIND>
+__device__ __forceinline__ void store_plane_words(uint8_t *base, int64_t x0_b, int64_t valid_b,
+                                                  bool vec, const uint32_t w[8]) {
+    constexpr int NB = (KIND == PS_KIND_COLOR) ? 32 : 16;
+    uint8_t *p = base + x0_b;
+    if (vec && valid_b >= NB) {
+        uint4 *q = reinterpret_cast<uint4 *>(p);
+#pragma unroll
+        for (int i = 0; i < NB / 16; ++i)
+            q[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+    } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                int64_t b = 4 * i + k;
+                if (b < NB && b < valid_b) p[b] = uint8_t(w[i] >> (8 * k));
+            }
+    }
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(TILE_X *TILE_Y)
+    pack_delta_kernel(PackArgs a) {
+    constexpr int EB = (KIND == PS_KIND_COLOR) ? 2 : 1;  // element bytes
+    constexpr int NB = SEG * EB;                         // bytes per plane segment
+    __shared__ uint32_t dirty[3][TILE_X];
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int64_t seg = int64_t(blockIdx.x) * TILE_X + tx;
+    const int64_t by = blockIdx.y;
+    const int64_t r = by * TILE_Y + ty;
+    if (ty == 0)
+        for (int e = 0; e < 3; ++e) dirty[e][tx] = 0u;
+    __syncthreads();
+    if (seg < a.nseg && r < a.h) {
+        uint32_t cur[3][8];
+        load_segment<KIND>(a, r, seg, cur);
+        const int64_t x0_b = seg * NB;
+        const int64_t valid_b = (a.pw - seg * SEG) * EB;
+        const int64_t plane_b = a.h * a.pw * EB;
+        const int64_t row_b = r * a.pw * EB;
+#pragma unroll
+        for (int e = 0; e < 3; ++e) {
+            uint8_t *dst = a.cur + e * plane_b + row_b;
+            if (a.prev) {
+                uint32_t pv[8];
+                load_plane_words<KIND>(a.prev + e * plane_b + row_b, x0_b, valid_b, a.vec_out,
+                                       pv);
+                uint32_t any = 0, res[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    any |= cur[e][i] ^ pv[i];
+                    res[i] = (KIND == PS_KIND_COLOR) ? __vsub2(cur[e][i], pv[i])
+                                                     : __vsub4(cur[e][i], pv[i]);
+                }
+                if (a.residual)
+                    store_plane_words<KIND>(a.residual + e * plane_b + row_b, x0_b, valid_b,
+                                            a.vec_out, res);
+                if (any) atomicOr(&dirty[e][tx], 1u);
+            }
+            store_plane_words<KIND>(dst, x0_b, valid_b, a.vec_out, cur[e]);
+        }
+    }
+    __syncthreads();
+    if (a.skip && ty < 3 && seg < a.nseg) {
+        const int64_t nby = (a.h + TILE_Y - 1) / TILE_Y;
+        uint8_t s = a.prev ? uint8_t(dirty[ty][tx] == 0u) : uint8_t(0);
+        a.skip[(int64_t(ty) * nby + by) * a.nseg + seg] = s;
+    }
+}
+
+// Generic temporal delta over already-packed planes (elements of 1 or 2 B).
+template <int EB>
+__global__ void __launch_bounds__(TILE_X *TILE_Y)
+    delta_kernel(const uint8_t *cur, const uint8_t *prev, int64_t h, int64_t w, int64_t nseg,
+                 uint8_t *residual, uint8_t *skip) {
+    __shared__ uint32_t dirty[TILE_X];
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int64_t seg = int64_t(blockIdx.x) * TILE_X + tx;
+    const int64_t by = blockIdx.y;
+    const int e = blockIdx.z;
+    const int64_t r = by * TILE_Y + ty;
+    if (ty == 0) dirty[tx] = 0u;
+    __syncthreads();
+    if (seg < nseg && r < h && prev) {
+        const int64_t base = (int64_t(e) * h + r) * w;
+        uint32_t any = 0;
+        for (int i = 0; i < SEG; ++i) {
+            const int64_t x = seg * SEG + i;
+            if (x >= w) break;
+            if (EB == 2) {
+                uint16_t c = reinterpret_cast<const uint16_t *>(cur)[base + x];
+                uint16_t p = reinterpret_cast<const uint16_t *>(prev)[base + x];
+                any |= uint32_t(c ^ p);
+                if (residual) reinterpret_cast<uint16_t *>(residual)[base + x] = uint16_t(c - p);
+            } else {
+                uint8_t c = cur[base + x], p = prev[base + x];
+                any |= uint32_t(c ^ p);
+                if (residual) residual[base + x] = uint8_t(c - p);
+            }
+        }
+        if (any) atomicOr(&dirty[tx], 1u);
+    }
+    __syncthreads();
+    if (skip && ty == 0 && seg < nseg) {
+        const int64_t nby = (h + TILE_Y - 1) / TILE_Y;
+        skip[(int64_t(e) * nby + by) * nseg + seg] = prev ? uint8_t(dirty[tx] == 0u) : 0;
+    }
+}
+
+__global__ void unpack_color_kernel(const uint16_t *planes, int64_t n, uint32_t *texels) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        texels[i] = uint32_t(planes[i]) | (uint32_t(planes[n + i]) << 10) |
+                    (uint32_t(planes[2 * n + i]) << 20);
+    }
+}
+
+__global__ void unpack_vis_kernel(const uint8_t *planes, int64_t h, int64_t w, int64_t pw,
+                                  uint16_t *texels) {
+    const int64_t total = h * w;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t r = i / w, x = i % w;
+        uint8_t s[4];
+        for (int k = 0; k < 4; ++k) {
+            const int64_t b = 4 * x + k;
+            s[k] = planes[((b % 3) * h + r) * pw + b / 3];
+        }
+        texels[2 * i] = uint16_t((s[0] << 8) | s[1]);
+        texels[2 * i + 1] = uint16_t((s[2] << 8) | s[3]);
+    }
+}
+
+inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int launch_pack_delta(int kind, const void *texels, int64_t h, int64_t w, int64_t row_stride,
+                      void *planes_cur, const void *planes_prev, void *residual,
+                      uint8_t *skip, cudaStream_t stream) {
+    if (h < 0 || w < 0) fail(PS_ERR_VALUE, "negative texel region shape");
+    if (row_stride < w) fail(PS_ERR_VALUE, "row stride smaller than width");
+    if (kind != PS_KIND_COLOR && kind != PS_KIND_VISIBILITY) fail(PS_ERR_VALUE, "bad kind");
+    PackArgs a;
+    a.texels = static_cast<const uint8_t *>(texels);
+    a.h = h;
+    a.w = w;
+    a.row_stride_b = row_stride * 4;
+    a.pw = (kind == PS_KIND_COLOR) ? w : (4 * w + 2) / 3;
+    a.nseg = ceil_div(a.pw, SEG);
+    a.cur = static_cast<uint8_t *>(planes_cur);
+    a.prev = static_cast<const uint8_t *>(planes_prev);
+    a.residual = static_cast<uint8_t *>(residual);
+    a.skip = skip;
+    a.vec_in = aligned16(texels) && (a.row_stride_b % 16 == 0);
+    const int eb = (kind == PS_KIND_COLOR) ? 2 : 1;
+    a.vec_out = aligned16(planes_cur) && (!planes_prev || aligned16(planes_prev)) &&
+                (!residual || aligned16(residual)) && ((a.pw * eb) % 16 == 0);
+    if (h == 0 || a.pw == 0) return PS_OK;
+    dim3 block(TILE_X, TILE_Y);
+    dim3 grid(unsigned(ceil_div(a.nseg, TILE_X)), unsigned(ceil_div(h, TILE_Y)));
+    if (grid.y > 65535u) fail(PS_ERR_VALUE, "plane too tall");
+    if (kind == PS_KIND_COLOR)
+        pack_delta_kernel<PS_KIND_COLOR><<<grid, block, 0, stream>>>(a);
+    else
+        pack_delta_kernel<PS_KIND_VISIBILITY><<<grid, block, 0, stream>>>(a);
+    check_launch("pack_delta_kernel");
+    return PS_OK;
+}
+
+}  // namespace
+}  // namespace ps
+
+using namespace ps;
+
+extern "C" {
+
+const char *ps_last_error(void) { return g_last_error.c_str(); }
+
+int ps_abi_version(void) { return PS_ABI_VERSION; }
+
+int ps_device_sm_count(void) {
+    try {
+        return sm_count();
+    } catch (...) {
+        return -1;
+    }
+}
+
+int64_t ps_widened_width(int64_t w) { return w < 0 ? -1 : (4 * w + 2) / 3; }
+
+int ps_pack_color(const uint32_t *texels, int64_t h, int64_t w, int64_t row_stride,
+                  uint16_t *planes, void *stream) {
+    PS_ABI_BEGIN
+    launch_pack_delta(PS_KIND_COLOR, texels, h, w, row_stride, planes, nullptr, nullptr,
+                      nullptr, as_stream(stream));
+    PS_ABI_END
+}
+
+int ps_pack_visibility(const uint16_t *texels, int64_t h, int64_t w, int64_t row_stride,
+                       uint8_t *planes, void *stream) {
+    PS_ABI_BEGIN
+    launch_pack_delta(PS_KIND_VISIBILITY, texels, h, w, row_stride, planes, nullptr, nullptr,
+                      nullptr, as_stream(stream));
+    PS_ABI_END
+}
+
+int ps_pack_delta(int kind, const void *texels, int64_t h, int64_t w, int64_t row_stride,
+                  void *planes_cur, const void *planes_prev, void *residual, uint8_t *skip,
+                  void *stream) {
+    PS_ABI_BEGIN
+    launch_pack_delta(kind, texels, h, w, row_stride, planes_cur, planes_prev, residual, skip,
+                      as_stream(stream));
+    PS_ABI_END
+}
+
+int ps_temporal_delta(int elem_bytes, const void *cur, const void *prev, int64_t h, int64_t w,
+                      void *residual, uint8_t *skip, void *stream) {
+    PS_ABI_BEGIN
+    if (h < 0 || w < 0) fail(PS_ERR_VALUE, "negative plane shape");
+    if (elem_bytes != 1 && elem_bytes != 2) fail(PS_ERR_VALUE, "element bytes must be 1 or 2");
+    if (h == 0 || w == 0) return PS_OK;
+    const int64_t nseg = ceil_div(w, SEG);
+    dim3 block(TILE_X, TILE_Y);
+    dim3 grid(unsigned(ceil_div(nseg, TILE_X)), unsigned(ceil_div(h, TILE_Y)), 3);
+    auto s = as_stream(stream);
+    if (elem_bytes == 2)
+        delta_kernel<2><<<grid, block, 0, s>>>(static_cast<const uint8_t *>(cur),
+                                                static_cast<const uint8_t *>(prev), h, w, nseg,
+                                                static_cast<uint8_t *>(residual), skip);
+    else
+        delta_kernel<1><<<grid, block, 0, s>>>(static_cast<const uint8_t *>(cur),
+                                                static_cast<const uint8_t *>(prev), h, w, nseg,
+                                                static_cast<uint8_t *>(residual), skip);
+    check_launch("delta_kernel");
+    PS_ABI_END
+}
+
+int ps_unpack_color(const uint16_t *planes, int64_t h, int64_t w, uint32_t *texels,
+                    void *stream) {
+    PS_ABI_BEGIN
+    if (h < 0 || w < 0) fail(PS_ERR_VALUE, "negative plane shape");
+    const int64_t n = h * w;
+    if (n == 0) return PS_OK;
+    unpack_color_kernel<<<unsigned(std::min<int64_t>(ceil_div(n, 256), 4096)), 256, 0,
+                          as_stream(stream)>>>(planes, n, texels);
+    check_launch("unpack_color_kernel");
+    PS_ABI_END
+}
+
+int ps_unpack_visibility(const uint8_t *planes, int64_t h, int64_t w, uint16_t *texels,
+                         void *stream) {
+    PS_ABI_BEGIN
+    if (h < 0 || w < 0) fail(PS_ERR_VALUE, "negative plane shape");
+    const int64_t n = h * w;
+    if (n == 0) return PS_OK;
+    unpack_vis_kernel<<<unsigned(std::min<int64_t>(ceil_div(n, 256), 4096)), 256, 0,
+                        as_stream(stream)>>>(planes, h, w, (4 * w + 2) / 3, texels);
+    check_launch("unpack_vis_kernel");
+    PS_ABI_END
+}
+
+}  // extern "C"
