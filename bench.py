@@ -1,0 +1,349 @@
+#!/usr/bin/env python
+"""Benchmark of the server-side probe hot path (BASELINE.json north_star).
+
+A step is one full-volume server frame at config 4 (64x32x64 probes, 256 rays
+per probe, the ~270k-triangle interior hall): trace + DDGI blend, then for
+colour and visibility: change detection, budgeted selection, slot
+assignment, update-atlas build + commit, plane packing + temporal delta.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 runs under torchrun: probes shard by z-slab, value is
+the whole-job probe updates/s, timed as the max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "probe updates/s & Grays/s at 1/2/4/8 B200; packed-atlas GB/s vs HBM roofline"
+CONFIGS = {
+    # name: (dims, rays, scene)
+    "c4": ((64, 32, 64), 256, "hall"),
+    "c2": ((32, 16, 32), 256, "hall"),
+    "c1": ((8, 8, 8), 64, "cornell"),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._proc = None
+        self._thread = None
+
+    def __enter__(self):
+        cmd = ["nvidia-smi", f"--id={self.index}",
+               "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+               "--format=csv,noheader,nounits", "-lms", "100"]
+        try:
+            self._proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                                          text=True)
+        except OSError:
+            self._proc = None
+            return self
+
+        def reader():
+            for line in self._proc.stdout:
+                self.samples.append([x.strip() for x in line.split(",")])
+
+        self._thread = threading.Thread(target=reader, daemon=True)
+        self._thread.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self._proc is not None:
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self._proc.kill()
+        if self._thread is not None:
+            self._thread.join(timeout=2)
+
+    def summary(self):
+        import statistics
+
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for name, v in zip(names, s[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def profile_traffic(kernel: str):
+    """dram bytes per launch of `kernel` from a committed ncu summary, if any."""
+    p = ROOT / "profiles" / "ncu_summary.json"
+    if not p.exists():
+        return None
+    try:
+        d = json.loads(p.read_text())
+        return d.get("kernels", {}).get(kernel, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# --------------------------------------------------------------------------------------------
+
+
+def build_scene(name):
+    from paper_2103_05875_b200 import scene as S
+
+    return S.interior_hall() if name == "hall" else S.cornell_box()
+
+
+def run_ours(args, rank, world, local):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2103_05875_b200 import scene as S
+    from paper_2103_05875_b200.sharding import SlabServer
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    dims, rays, scene_name = CONFIGS[args.config]
+    sc = build_scene(scene_name)
+    vol = S.volume_for(sc, dims)
+    n = vol.probe_count
+    server = SlabServer(vol, sc, rays_per_probe=rays, device=dev, rank=rank, world=world,
+                        irradiance_scale=4.0 if scene_name == "hall" else 2.0)
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def frame_lights(f):
+        return S.moving_light(sc, f).lights
+
+    for f in range(args.warmup):
+        server.tick(f, frame_lights(f))
+    barrier()
+    # ---- timed region: K full frames, inputs resident (scene, state), outputs on device
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        barrier()
+        start.record(stream)
+        for k in range(args.steps):
+            f = args.warmup + k
+            server.tick(f, frame_lights(f))
+        end.record(stream)
+        barrier()
+    ms = start.elapsed_time(end) / args.steps
+    ms_max = ms
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t.item())
+
+    # ---- end-to-end through the public API with host buffers -------------------------
+    e2e = server.run_e2e(args.steps, args.warmup + args.steps, frame_lights)
+    e2e_ms = e2e["ms_per_step"]
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    # ---- per-stage device times + launch count (untimed instrumented frames) ---------
+    base = args.warmup + 2 * args.steps + 1
+    stages = server.stage_times(3, base, frame_lights)
+    launches_per_step, kernel_names = server.count_launches(base + 3, frame_lights)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    rays_total = n * rays
+    value = n / (ms_max / 1e3)
+    peak, peak_kind = load_peaks()
+    # roofline of the HBM-bound pack kernel (pack + temporal delta over the update atlas)
+    pk = server.pack_delta_bytes()
+    pack_ms = stages.get("color.pack_delta", 0) + stages.get("visibility.pack_delta", 0)
+    achieved = pk["total"] / (pack_ms / 1e3) / 1e9 if pack_ms > 0 else None
+    traffic = profile_traffic("pack_delta_kernel")
+    trace_ms = stages.get("trace_blend", None)
+    out = {
+        "metric": METRIC,
+        "value": round(value, 1),
+        "unit": "probe updates/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_max, 4),
+        "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None,
+        "dtype": "f32+u32",
+        "data": "synthetic",
+        "config": {
+            "workload": f"config 4: {dims[0]}x{dims[1]}x{dims[2]} probe grid, {rays} rays/probe, "
+                        f"~{sc.triangle_count // 1000}k-triangle interior hall, full-volume update "
+                        "+ change detection + selection + slot assign + build + pack + temporal "
+                        "delta, colour + visibility",
+            "probes": n, "rays_per_probe": rays, "triangles": sc.triangle_count,
+            "lights": len(sc.lights), "shadow_rays": True,
+            "l2": "per-frame working set (atlases, float state, planes) > 126 MB L2; no flush",
+            "parallelism": f"z-slab x{world}",
+        },
+        "grays_per_s": round(rays_total / (ms_max / 1e3) / 1e9, 4),
+        "frame_hz": round(1e3 / ms_max, 2),
+        "stages_ms": {k: round(v, 4) for k, v in stages.items()},
+        "packed_atlas_gbs": round(achieved, 1) if achieved else None,
+        "roofline": {
+            "bound": "hbm",
+            "kernel": "pack_delta_kernel (colour + visibility)",
+            "achieved": round(achieved, 1) if achieved else None,
+            "peak": peak,
+            "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}, burst copy)",
+            "unit": "GB/s",
+            "frac": round(achieved / peak, 4) if achieved else None,
+            "traffic": traffic,
+            "algorithmic_bytes_per_launch": pk,
+        },
+        "roofline_trace": {
+            "kernel": "trace_blend_kernel",
+            "rays_per_s": round(rays_total / (trace_ms / 1e3), 1) if trace_ms else None,
+            "ms": trace_ms,
+            "note": "no dense roofline (BVH traversal, SIMT); see profiles/ for SM/L1 throughput",
+        },
+        "clocks": clocks.summary(),
+        "e2e": {"value": round(n / (e2e_ms / 1e3), 1), "unit": "probe updates/s",
+                "ms_per_step": round(e2e_ms, 4),
+                "h2d_bytes_per_step": e2e["h2d_bytes_per_step"],
+                "d2h_bytes_per_step": e2e["d2h_bytes_per_step"],
+                "path": "ProbeStreamServer.tick via the C ABI; per-frame ray table + lights "
+                        "H2D from pinned host memory, index entries + counts + SKIP maps D2H"},
+        "gpu_launches": launches_per_step * args.steps,
+        "gpu_launches_per_step": launches_per_step,
+        "kernels": kernel_names,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(sc, vol, rays, args.cpu_sample)
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def cpu_baseline(sc, vol, rays, sample):
+    from oracle import cpu_frame
+
+    r = cpu_frame.time_frame(sc, vol, rays, sample_probes=sample)
+    return {
+        "value": round(vol.probe_count / r["frame_s"], 3),
+        "unit": "probe updates/s",
+        "cores": r["threads"],
+        "kind": "port",
+        "sample": (f"{r['sample_probes']} probes x {rays} rays traced by the oracle's C restatement "
+                   f"of the reference brute-force raycast (float64, OpenMP on {r['threads']} "
+                   f"threads) + numpy blend, scaled to {vol.probe_count} probes; detect/select/"
+                   f"assign/build/pack/delta by the numpy restatement at full size (1 thread)"),
+        "frame_s": round(r["frame_s"], 3),
+        "detail": {k: (round(v, 6) if isinstance(v, float) else v) for k, v in r.items()},
+    }
+
+
+def run_reference(args, rank, world, local):
+    """The reference's CPU path (oracle port) on the host cores."""
+    if rank != 0:
+        return
+    from paper_2103_05875_b200 import scene as S
+    from oracle import cpu_frame
+
+    dims, rays, scene_name = CONFIGS[args.config]
+    sc = build_scene(scene_name)
+    vol = S.volume_for(sc, dims)
+    for w in range(min(args.warmup, 1)):
+        cpu_frame.time_frame(sc, vol, rays, sample_probes=1, stages_full=False, frame=w)
+    times = []
+    for k in range(args.steps):
+        r = cpu_frame.time_frame(sc, vol, rays, sample_probes=args.cpu_sample, frame=k,
+                                 stages_full=(k == 0), rng_seed=k)
+        times.append(r)
+    stages = times[0]["stages_s"]
+    per_probe = sum(t["trace_shade_s_per_probe"] + t["blend_s_per_probe"] for t in times) / len(times)
+    frame_s = per_probe * vol.probe_count + stages
+    value = vol.probe_count / frame_s
+    out = {
+        "metric": METRIC, "value": round(value, 3), "unit": "probe updates/s", "impl": "reference",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(frame_s * 1e3, 1), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64+u32", "data": "synthetic",
+        "config": {"workload": f"config 4 ({dims}, {rays} rays, interior hall) on the host CPU",
+                   "probes": vol.probe_count, "rays_per_probe": rays},
+        "grays_per_s": round(vol.probe_count * rays / frame_s / 1e9, 9),
+        "cpu_baseline": {"value": round(value, 3), "unit": "probe updates/s",
+                         "cores": os.cpu_count(), "kind": "port",
+                         "sample": f"{args.cpu_sample} probes/step traced+blended per step "
+                                   f"(scaled), stages 3-4 at full size once"},
+        "e2e": {"value": round(value, 3), "unit": "probe updates/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--cpu-sample", type=int, default=4)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("warmup raised to 3 (timing rules)")
+        args.warmup = 3
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world, local)
+    else:
+        run_ours(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -168,9 +168,10 @@ int ps_reconstruct_guard_bands(int kind, void *atlas, int64_t probe_count,
 
 /* BVH: built on the host (binned SAH), uploaded by the shim. */
 typedef struct ps_bvh_sizes {
-    int64_t node_count;  /* 64-byte nodes          */
-    int64_t tri_count;   /* triangles after build  */
-    int64_t tri_slots;   /* 48-byte triangle records incl. leaf terminators */
+    int64_t node_count;  /* 64-byte nodes                                     */
+    int64_t tri_count;   /* triangles                                         */
+    int64_t tri_slots;   /* 48-byte triangle records incl. leaf terminators   */
+    int64_t max_depth;   /* deepest inner-node path (traversal stack bound)   */
 } ps_bvh_sizes;
 
 /* Build a BVH2 over `tri_count` triangles given as float64 vertices
@@ -195,7 +196,8 @@ typedef struct ps_trace_params {
     /* scene */
     const float *nodes;      /* BVH2 nodes */
     const float *tris;       /* triangle records */
-    const float *materials;  /* per original triangle: albedo rgb, emission rgb (6 floats) */
+    const float *materials;  /* per original triangle, 12 floats: albedo rgb _, emission
+                              * rgb _, unit face normal xyz _ (normal in double, rounded) */
     int32_t light_count;
     const float *lights;     /* per light: position xyz, intensity rgb (6 floats) */
     float sky[3];
@@ -208,16 +210,18 @@ typedef struct ps_trace_params {
     const float *inv_wsum;   /* (64 + 256) reciprocal weight sums            */
     float hysteresis;        /* 0 on the first frame                        */
     float irradiance_scale;  /* colour unorm = irradiance / scale            */
-    /* state (float, persistent across frames) */
-    float *irradiance;       /* (probe_count, 64, 3)  */
-    float *moments;          /* (probe_count, 256, 2) */
+    /* state (float, persistent across frames), indexed by p - probe_begin */
+    float *irradiance;       /* (probes, 64, 3)  */
+    float *moments;          /* (probes, 256, 2) */
     /* outputs: atlases with guard bands (volume.py:147) */
     uint32_t *color_atlas;
     uint16_t *vis_atlas;
     int32_t probes_per_row_color;
     int32_t probes_per_row_vis;
-    /* optional per-ray debug record (probe_count_local * rays, 8 floats:
-     * radiance rgb, depth, hit t, prim id bits, pad, pad); NULL = off */
+    /* optional per-ray debug record ((probe_end - probe_begin) * rays, 8
+     * floats: radiance rgb, depth, hit t (inf = miss), prim id (int bits,
+     * -1 = miss), shadow mask (int bits, bit l = light l visible), 0);
+     * NULL = off */
     float *ray_records;
 } ps_trace_params;
 

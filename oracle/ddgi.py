@@ -1,0 +1,236 @@
+"""CPU oracle for stages (1)+(2): ray set, traversal, shading, DDGI blend.
+
+TEST INFRASTRUCTURE ONLY (see ``oracle/__init__``).
+
+PARITY UNPINNED for the DDGI arithmetic itself: the reference has no probe
+tracer and no irradiance/depth blend, so this module restates
+the algorithm documented in ``paper_2103_05875_b200/probes.py`` and
+DESIGN.md.  The pieces that the reference does pin are restated from it and
+checked against its golden vectors (tests/golden/geometry.npz):
+
+* ``fibonacci_sphere``      selection.py:241-249
+* ``texel_directions``      volume.py:286-314 (texel centres + oct_decode)
+* ``raycast`` (C, float64)  selection.py:66-149 for triangles
+* guard band rule           packing.py:180-196 (via stream_ops.guard_band_block)
+* texel formats             volume.py:150-153, :221-226
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+from . import stream_ops as so
+
+HERE = Path(__file__).resolve().parent
+_LIB = None
+
+
+def _lib():
+    global _LIB
+    if _LIB is None:
+        so_path = HERE / "build" / "libraycast.so"
+        if not so_path.exists() or so_path.stat().st_mtime < (HERE / "raycast.c").stat().st_mtime:
+            subprocess.run(["make", "-C", str(HERE)], check=True, capture_output=True)
+        lib = ctypes.CDLL(str(so_path))
+        vp, i64 = ctypes.c_void_p, ctypes.c_int64
+        lib.oracle_raycast.argtypes = [vp, i64, vp, vp, i64, vp, vp]
+        lib.oracle_occluded.argtypes = [vp, i64, vp, vp, vp, i64, vp]
+        _LIB = lib
+    return _LIB
+
+
+def _p(a):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def raycast(tris: np.ndarray, origins: np.ndarray, dirs: np.ndarray):
+    """Nearest hit (t, prim) per ray, float64 brute force; prim -1 = miss."""
+    tris = np.ascontiguousarray(tris, np.float64)
+    o = np.ascontiguousarray(np.broadcast_to(origins, dirs.shape), np.float64)
+    d = np.ascontiguousarray(dirs, np.float64)
+    n = len(d)
+    t = np.empty(n, np.float64)
+    prim = np.empty(n, np.int64)
+    _lib().oracle_raycast(_p(tris), len(tris), _p(o), _p(d), n, _p(t), _p(prim))
+    return t, prim
+
+
+def occluded(tris, origins, dirs, tmax):
+    tris = np.ascontiguousarray(tris, np.float64)
+    o = np.ascontiguousarray(origins, np.float64)
+    d = np.ascontiguousarray(dirs, np.float64)
+    tm = np.ascontiguousarray(tmax, np.float64)
+    out = np.empty(len(d), np.uint8)
+    _lib().oracle_occluded(_p(tris), len(tris), _p(o), _p(d), _p(tm), len(d), _p(out))
+    return out.astype(bool)
+
+
+# --- ray set ---------------------------------------------------------------------------
+
+
+def fibonacci_sphere(n: int) -> np.ndarray:
+    k = np.arange(n, dtype=np.float64) + 0.5
+    z = 1.0 - 2.0 * k / n
+    r = np.sqrt(np.maximum(0.0, 1.0 - z * z))
+    phi = np.pi * (1.0 + np.sqrt(5.0)) * k
+    return np.column_stack([r * np.cos(phi), r * np.sin(phi), z])
+
+
+def oct_uv(d: np.ndarray) -> np.ndarray:
+    """volume.py:262-283 without validation."""
+    d = d / np.linalg.norm(d, axis=1, keepdims=True)
+    l1 = np.abs(d).sum(axis=1)
+    p = d[:, :2] / l1[:, None]
+    sgn = np.where(p >= 0.0, 1.0, -1.0)
+    folded = (1.0 - np.abs(p[:, ::-1])) * sgn
+    p = np.where(d[:, 2:3] < 0.0, folded, p)
+    return p * 0.5 + 0.5
+
+
+def texel_directions(side: int) -> np.ndarray:
+    c = (np.arange(side) + 0.5) / side
+    uu, vv = np.meshgrid(c, c, indexing="xy")
+    f = np.stack([uu, vv], -1).reshape(-1, 2) * 2.0 - 1.0
+    z = 1.0 - np.abs(f[:, 0]) - np.abs(f[:, 1])
+    sgn = np.where(f >= 0.0, 1.0, -1.0)
+    xy = np.where((z < 0.0)[:, None], (1.0 - np.abs(f[:, ::-1])) * sgn, f)
+    d = np.column_stack([xy, z])
+    return d / np.linalg.norm(d, axis=1, keepdims=True)
+
+
+def coherence_order(dirs: np.ndarray) -> np.ndarray:
+    """Permutation sorting directions by the Morton code of their 10-bit
+    octahedral uv (stable)."""
+    q = np.clip(np.floor(oct_uv(dirs) * 1024.0).astype(np.int64), 0, 1023)
+    code = np.zeros(len(dirs), np.int64)
+    for bit in range(10):
+        code |= ((q[:, 0] >> bit) & 1) << (2 * bit)
+        code |= ((q[:, 1] >> bit) & 1) << (2 * bit + 1)
+    return np.argsort(code, kind="stable")
+
+
+def rotation(seed: int, frame: int) -> np.ndarray:
+    w, x, y, z = (lambda q: q / np.linalg.norm(q))(np.random.default_rng(seed + frame).normal(size=4))
+    return np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - z * w), 2 * (x * z + y * w)],
+                     [2 * (x * y + z * w), 1 - 2 * (x * x + z * z), 2 * (y * z - x * w)],
+                     [2 * (x * z - y * w), 2 * (y * z + x * w), 1 - 2 * (x * x + y * y)]])
+
+
+def ray_table(count: int, seed: int, frame: int) -> np.ndarray:
+    base = fibonacci_sphere(count)
+    base = base[coherence_order(base)]
+    return (rotation(seed, frame) @ base.T).T.astype(np.float32)
+
+
+# --- shading (float64, given hits) --------------------------------------------------------
+
+
+def shade(tris, albedo, emission, lights, sky, origins, dirs, t, prim, max_distance, bias,
+          shadows=True):
+    """Radiance and depth per ray, float64; returns (rgb (n,3), depth (n,), mask)."""
+    n = len(dirs)
+    rgb = np.tile(np.asarray(sky, np.float64), (n, 1))
+    depth = np.full(n, float(max_distance))
+    mask = np.zeros(n, np.int64)
+    hit = prim >= 0
+    if not hit.any():
+        return rgb, depth, mask
+    v = np.asarray(tris, np.float64)
+    nrm = np.cross(v[:, 1] - v[:, 0], v[:, 2] - v[:, 0])
+    nrm = nrm / np.maximum(np.linalg.norm(nrm, axis=1, keepdims=True), 1e-30)
+    nrm = nrm.astype(np.float32).astype(np.float64)  # the device table holds float normals
+    idx = np.nonzero(hit)[0]
+    pid = prim[idx]
+    o, d, th = origins[idx], dirs[idx], t[idx]
+    nn = nrm[pid]
+    nn = np.where((np.sum(nn * d, axis=1) > 0)[:, None], -nn, nn)
+    x = o + d * th[:, None]
+    s = x + bias * nn
+    acc = np.zeros((len(idx), 3))
+    for li, (lp, li_rgb) in enumerate(lights):
+        lv = np.asarray(lp, np.float64) - s
+        d2 = np.sum(lv * lv, axis=1)
+        dist = np.sqrt(d2)
+        u = lv / dist[:, None]
+        cos = np.sum(nn * u, axis=1)
+        ok = (d2 > 0) & (cos > 0)
+        if shadows and ok.any():
+            blocked = occluded(tris, s[ok], u[ok], dist[ok])
+            vis = ok.copy()
+            vis[np.nonzero(ok)[0][blocked]] = False
+        else:
+            vis = ok
+        mask[idx[vis]] |= 1 << li
+        acc += np.where(vis, cos / np.where(d2 > 0, d2, 1.0), 0.0)[:, None] * np.asarray(li_rgb, np.float64)
+    rgb[idx] = np.asarray(emission, np.float64)[pid] + np.asarray(albedo, np.float64)[pid] * acc
+    depth[idx] = np.minimum(th, max_distance)
+    return rgb, depth, mask
+
+
+# --- blend (float32) ----------------------------------------------------------------------
+
+
+def blend_weights(dirs32: np.ndarray, sharpness: float):
+    """(Wc (64,R), Wd (256,R), inv_c (64,), inv_d (256,)) in float32."""
+    tc = texel_directions(8).astype(np.float32)
+    td = texel_directions(16).astype(np.float32)
+    d = np.asarray(dirs32, np.float32)[:, :3]
+    wc = np.maximum(tc @ d.T, np.float32(0))
+    wd = np.power(np.maximum(td @ d.T, np.float32(0)), np.float32(sharpness))
+    inv = []
+    for w in (wc, wd):
+        s = w.sum(axis=1, dtype=np.float32)
+        with np.errstate(divide="ignore"):
+            inv.append(np.where(s > 0, np.float32(1) / s, np.float32(0)).astype(np.float32))
+    return wc, wd, inv[0], inv[1]
+
+
+def blend(rgb32, depth32, weights, prev_irr, prev_mom, hysteresis):
+    """rgb32 (P,R,3), depth32 (P,R) float32 -> new (irr (P,64,3), mom (P,256,2))."""
+    wc, wd, inv_c, inv_d = weights
+    rgb32 = np.asarray(rgb32, np.float32)
+    if prev_irr is None:
+        prev_irr = np.zeros((rgb32.shape[0], 64, 3), np.float32)
+    if prev_mom is None:
+        prev_mom = np.zeros((rgb32.shape[0], 256, 2), np.float32)
+    dep = np.asarray(depth32, np.float32)
+    irr = np.einsum("tr,prc->ptc", wc, rgb32).astype(np.float32) * inv_c[None, :, None]
+    m1 = np.einsum("tr,pr->pt", wd, dep).astype(np.float32) * inv_d[None, :]
+    m2 = np.einsum("tr,pr->pt", wd, dep * dep).astype(np.float32) * inv_d[None, :]
+    mom = np.stack([m1, m2], -1).astype(np.float32)
+    h = np.float32(hysteresis)
+    if h != 0:
+        irr = irr + h * (prev_irr - irr)
+        mom = mom + h * (prev_mom - mom)
+    irr = np.where((inv_c == 0)[None, :, None], prev_irr, irr)
+    mom = np.where((inv_d == 0)[None, :, None], prev_mom, mom)
+    return irr.astype(np.float32), mom.astype(np.float32)
+
+
+# --- quantisation + guard band (bit-exact given the float state) ---------------------------
+
+
+def quantize_color(irr32: np.ndarray, scale: float) -> np.ndarray:
+    """(P,64,3) float32 -> (P,8,8) uint32 r | g<<10 | b<<20 (volume.py:226)."""
+    qs = np.float32(1) / np.float32(scale) if scale > 0 else np.float32(0)
+    x = np.clip(irr32.astype(np.float32) * qs, np.float32(0), np.float32(1))
+    q = np.rint(x * np.float32(1023)).astype(np.uint32)
+    t = q[..., 0] | (q[..., 1] << np.uint32(10)) | (q[..., 2] << np.uint32(20))
+    return t.reshape(-1, 8, 8)
+
+
+def quantize_moments(mom32: np.ndarray) -> np.ndarray:
+    """(P,256,2) float32 -> (P,16,16,2) uint16 raw half bits."""
+    return mom32.astype(np.float16).view(np.uint16).reshape(-1, 16, 16, 2)
+
+
+def write_blocks(atlas: np.ndarray, kind: str, ppr: int, probe_ids, cores) -> None:
+    side = so.BLOCK_SIDE[kind]
+    for p, core in zip(probe_ids, cores):
+        br, bc = divmod(int(p), ppr)
+        atlas[br * side:(br + 1) * side, bc * side:(bc + 1) * side] = so.guard_band_block(core)

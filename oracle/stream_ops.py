@@ -296,11 +296,10 @@ def temporal_delta(cur: np.ndarray, prev: np.ndarray):
     residual = (cur - prev).astype(cur.dtype)  # wraps modulo 2^bits
     c, h, w = cur.shape
     by, bx = -(-h // CODEC_BLOCK), -(-w // CODEC_BLOCK)
-    skip = np.zeros((c, by, bx), np.uint8)
-    diff = cur != prev
-    for p in range(c):
-        for j in range(by):
-            for i in range(bx):
-                blk = diff[p, j * 16:(j + 1) * 16, i * 16:(i + 1) * 16]
-                skip[p, j, i] = 0 if blk.any() else 1
+    # pad the difference mask up to whole blocks (padding never differs), then
+    # reduce every 16x16 tile
+    diff = np.zeros((c, by * CODEC_BLOCK, bx * CODEC_BLOCK), bool)
+    diff[:, :h, :w] = cur != prev
+    tiles = diff.reshape(c, by, CODEC_BLOCK, bx, CODEC_BLOCK)
+    skip = (~tiles.any(axis=(2, 4))).astype(np.uint8)
     return residual, skip

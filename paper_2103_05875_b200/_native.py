@@ -37,7 +37,8 @@ _int = C.c_int
 
 
 class BvhSizes(C.Structure):
-    _fields_ = [("node_count", _i64), ("tri_count", _i64), ("tri_slots", _i64)]
+    _fields_ = [("node_count", _i64), ("tri_count", _i64), ("tri_slots", _i64),
+                ("max_depth", _i64)]
 
 
 class TraceParams(C.Structure):

@@ -30,7 +30,7 @@ NVCC_FLAGS = [
     "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
     "-Xptxas", "-v", "-Xcompiler", "-Wall",
 ]
-CXX_FLAGS = ["-O3", "-std=c++17", "-fPIC", "-Wall", "-march=x86-64-v2", "-fopenmp"]
+CXX_FLAGS = ["-O3", "-std=c++17", "-fPIC", "-Wall", "-march=x86-64-v2"]
 
 
 def _nvcc() -> str:
@@ -77,7 +77,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if force or not LIB.exists() or any(o.stat().st_mtime > LIB.stat().st_mtime for o in objs):
         tmp = LIB.with_suffix(".so.tmp")
         cmd = [_nvcc(), *ARCH, "-shared", "-o", str(tmp), *map(str, objs),
-               "-Xcompiler", "-fopenmp", "-lgomp"]
+               ]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"link failed: {' '.join(cmd)}\n{res.stdout}\n{res.stderr}")

@@ -183,15 +183,17 @@ extern "C" int ps_bvh_build(const double *vertices, int64_t tri_count, int leaf_
         // that leaf and an empty box.
         std::vector<int> gpu_index(b.nodes.size(), -1);
         std::vector<int> inner;
-        std::vector<int> stack{0};
+        std::vector<std::pair<int, int>> stack{{0, 1}};
+        int64_t max_depth = 0;
         while (!stack.empty()) {
-            int id = stack.back();
+            auto [id, depth] = stack.back();
             stack.pop_back();
             if (b.nodes[id].left < 0) continue;
+            max_depth = std::max<int64_t>(max_depth, depth);
             gpu_index[id] = int(inner.size());
             inner.push_back(id);
-            stack.push_back(b.nodes[id].right);
-            stack.push_back(b.nodes[id].left);
+            stack.push_back({b.nodes[id].right, depth + 1});
+            stack.push_back({b.nodes[id].left, depth + 1});
         }
         const bool single_leaf = inner.empty();
         const int64_t node_count = single_leaf ? 1 : int64_t(inner.size());
@@ -217,6 +219,7 @@ extern "C" int ps_bvh_build(const double *vertices, int64_t tri_count, int leaf_
         sizes->node_count = node_count;
         sizes->tri_count = tri_count;
         sizes->tri_slots = slots + (single_leaf ? 1 : 0);
+        sizes->max_depth = std::max<int64_t>(max_depth, 1);
         if (!nodes_out || !tris_out) return PS_OK;
 
         auto child_ref = [&](int id) -> int32_t {

@@ -1,0 +1,217 @@
+"""Stages (1)+(2): per-probe ray generation, BVH tracing and the DDGI blend.
+
+New API surface (the reference has no implementation of these stages,
+SURVEY F3/F4); it emits the reference's atlas types so stages (3)+(4)
+consume its output unchanged.  The algorithm, fixed here and restated
+independently by ``oracle/ddgi.py``:
+
+Ray set (host, float64 -> float32): the base set is
+``fibonacci_sphere(R)`` (selection.py:241-249) in a fixed coherence order
+(sorted by the Morton code of its octahedral uv, so a warp's 32 rays cover a
+small solid angle); frame ``f`` rotates it by the uniformly random rotation
+drawn from ``np.random.default_rng(seed + f)`` (unit quaternion from 4
+normals).  Every probe uses the same rotated set, as in DDGI.
+
+Tracing (device): ray origin = probe position (volume.py:127-138), nearest
+hit with the reference raycast semantics (selection.py:66-149).  A hit is
+shaded ``emission + albedo * sum_l I_l * cos / d^2 * V_l`` with the normal
+facing the ray and ``V_l`` a shadow ray from ``hit + bias * n``; a miss
+returns the sky colour.  Depth = ``min(t, max_distance)`` (miss:
+``max_distance``).
+
+Blend (device): colour texel t (8x8, texel_directions) averages radiance
+with weights ``max(0, n_t . d_r)``; depth texel t (16x16) averages depth and
+depth^2 with ``max(0, n_t . d_r)^sharpness``; state = frame + h (prev -
+frame) (h = 0 on the first frame); a texel no ray reaches keeps its state.
+Output: colour unorm10 of ``state / irradiance_scale`` (round to nearest
+even), visibility raw float16 halves; border texels by the guard-band rule
+(packing.py:180-196).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+import torch
+
+from . import _device as D
+from . import _native as N
+from .scene import DeviceScene, Scene
+from .volume import AtlasKind, ProbeAtlas, ProbeVolume, oct_encode, texel_directions
+
+
+def fibonacci_sphere(count: int) -> np.ndarray:
+    """selection.py:241-249 (float64)."""
+    if count < 1:
+        return np.zeros((0, 3))
+    i = np.arange(count, dtype=np.float64) + 0.5
+    z = 1.0 - 2.0 * i / count
+    rad = np.sqrt(np.maximum(0.0, 1.0 - z * z))
+    th = np.pi * (1.0 + np.sqrt(5.0)) * i
+    return np.stack([rad * np.cos(th), rad * np.sin(th), z], axis=1)
+
+
+def _morton2(x: np.ndarray, y: np.ndarray) -> np.ndarray:
+    def spread(v):
+        v = v.astype(np.uint32) & np.uint32(0xFFFF)
+        v = (v | (v << np.uint32(8))) & np.uint32(0x00FF00FF)
+        v = (v | (v << np.uint32(4))) & np.uint32(0x0F0F0F0F)
+        v = (v | (v << np.uint32(2))) & np.uint32(0x33333333)
+        v = (v | (v << np.uint32(1))) & np.uint32(0x55555555)
+        return v
+    return spread(x) | (spread(y) << np.uint32(1))
+
+
+def base_ray_set(count: int) -> np.ndarray:
+    """fibonacci_sphere(count) reordered by octahedral Morton code (float64)."""
+    fib = fibonacci_sphere(count)
+    uv = oct_encode(fib, validate=False)
+    q = np.clip((uv * 1024.0).astype(np.int64), 0, 1023)
+    order = np.argsort(_morton2(q[:, 0], q[:, 1]), kind="stable")
+    return fib[order]
+
+
+def frame_rotation(seed: int, frame: int) -> np.ndarray:
+    """Uniform random rotation for a frame: unit quaternion from 4 normals."""
+    q = np.random.default_rng(seed + frame).normal(size=4)
+    w, x, y, z = q / np.linalg.norm(q)
+    return np.array([
+        [1 - 2 * (y * y + z * z), 2 * (x * y - z * w), 2 * (x * z + y * w)],
+        [2 * (x * y + z * w), 1 - 2 * (x * x + z * z), 2 * (y * z - x * w)],
+        [2 * (x * z - y * w), 2 * (y * z + x * w), 1 - 2 * (x * x + y * y)],
+    ])
+
+
+def frame_ray_directions(count: int, seed: int, frame: int) -> np.ndarray:
+    """(count, 4) float32 table [dx dy dz 0] for a frame."""
+    d = base_ray_set(count) @ frame_rotation(seed, frame).T
+    out = np.zeros((count, 4), np.float32)
+    out[:, :3] = d
+    return out
+
+
+def texel_direction_table() -> np.ndarray:
+    """(320, 4) float32: 64 colour texel directions then 256 depth ones."""
+    out = np.zeros((320, 4), np.float32)
+    out[:64, :3] = texel_directions(8).reshape(-1, 3)
+    out[64:, :3] = texel_directions(16).reshape(-1, 3)
+    return out
+
+
+class ProbeUpdater:
+    """Owns the float probe state and the two output atlases on one GPU and
+    updates a contiguous probe range per frame (``probe_range`` = a z-slab
+    when sharded across GPUs).  ``update`` launches two kernels and never
+    synchronises."""
+
+    def __init__(self, volume: ProbeVolume, scene: Scene | DeviceScene, rays_per_probe: int = 256,
+                 hysteresis: float = 0.97, sharpness: float = 50.0, max_distance: float | None = None,
+                 irradiance_scale: float = 1.0, shadows: bool = True, normal_bias: float | None = None,
+                 seed: int = 0, probe_range=None, probes_per_row: int | None = None,
+                 device=None, record_rays: bool = False):
+        self.volume = volume
+        self.device = torch.device(device) if device is not None else D.device_of()
+        self.dscene = scene if isinstance(scene, DeviceScene) else scene.device(self.device)
+        sc = self.dscene.scene
+        (x0, y0, z0), (x1, y1, z1) = sc.bounds
+        diag = math.sqrt((x1 - x0) ** 2 + (y1 - y0) ** 2 + (z1 - z0) ** 2)
+        self.rays_per_probe = int(rays_per_probe)
+        self.hysteresis = float(hysteresis)
+        self.sharpness = float(sharpness)
+        self.max_distance = float(max_distance if max_distance is not None else diag)
+        self.irradiance_scale = float(irradiance_scale)
+        self.shadows = bool(shadows)
+        self.normal_bias = float(normal_bias if normal_bias is not None else 1e-3 * diag)
+        self.seed = int(seed)
+        n = volume.probe_count
+        self.probe_begin, self.probe_end = probe_range if probe_range is not None else (0, n)
+        nloc = self.probe_end - self.probe_begin
+        dev = self.device
+        self.irradiance = torch.zeros((max(nloc, 1), 64, 3), dtype=torch.float32, device=dev)
+        self.moments = torch.zeros((max(nloc, 1), 256, 2), dtype=torch.float32, device=dev)
+        self.color = ProbeAtlas(AtlasKind.COLOR, n, probes_per_row, device=dev)
+        self.visibility = ProbeAtlas(AtlasKind.VISIBILITY, n, probes_per_row, device=dev)
+        R = self.rays_per_probe
+        self.texdir = torch.from_numpy(texel_direction_table()).to(dev)
+        self.w_color = torch.empty((R, 64), dtype=torch.float32, device=dev)
+        self.w_depth = torch.empty((R, 256), dtype=torch.float32, device=dev)
+        self.inv_wsum = torch.empty(320, dtype=torch.float32, device=dev)
+        self.ray_dirs = torch.empty((R, 4), dtype=torch.float32, device=dev)
+        # double-buffered pinned staging for the per-frame ray table
+        self._pinned_dirs = [torch.empty((R, 4), dtype=torch.float32).pin_memory() for _ in range(2)]
+        self._pinned_evt = [None, None]
+        self.ray_records = (torch.empty((max(nloc, 1) * R, 8), dtype=torch.float32, device=dev)
+                            if record_rays else None)
+        self.frames_done = 0
+
+    def _params(self, hysteresis: float) -> N.TraceParams:
+        v, s = self.volume, self.dscene
+        p = N.TraceParams()
+        p.nx, p.ny, p.nz = v.dims
+        p.probe_begin, p.probe_end = self.probe_begin, self.probe_end
+        p.origin = (ctypes.c_double * 3)(*map(float, v.origin))
+        p.spacing = (ctypes.c_double * 3)(*map(float, v.spacing))
+        p.ray_dirs = self.ray_dirs.data_ptr()
+        p.rays_per_probe = self.rays_per_probe
+        p.nodes, p.tris, p.materials = s.nodes.data_ptr(), s.tris.data_ptr(), s.materials.data_ptr()
+        p.light_count = s.light_count
+        p.lights = s.lights.data_ptr()
+        p.sky = (ctypes.c_float * 3)(*map(float, s.scene.sky))
+        p.max_distance = self.max_distance
+        p.normal_bias = self.normal_bias
+        p.shadows = int(self.shadows)
+        p.w_color, p.w_depth, p.inv_wsum = (self.w_color.data_ptr(), self.w_depth.data_ptr(),
+                                            self.inv_wsum.data_ptr())
+        p.hysteresis = hysteresis
+        p.irradiance_scale = self.irradiance_scale
+        p.irradiance, p.moments = self.irradiance.data_ptr(), self.moments.data_ptr()
+        p.color_atlas = self.color.texels.data_ptr()
+        p.vis_atlas = self.visibility.texels.data_ptr()
+        p.probes_per_row_color = self.color.probes_per_row
+        p.probes_per_row_vis = self.visibility.probes_per_row
+        p.ray_records = self.ray_records.data_ptr() if self.ray_records is not None else None
+        return p
+
+    def upload_rays(self, frame: int) -> None:
+        k = frame & 1
+        if self._pinned_evt[k] is not None:
+            self._pinned_evt[k].synchronize()  # the copy that last read this buffer is done
+        self._pinned_dirs[k].numpy()[...] = frame_ray_directions(self.rays_per_probe, self.seed, frame)
+        self.ray_dirs.copy_(self._pinned_dirs[k], non_blocking=True)
+        evt = torch.cuda.Event()
+        evt.record(torch.cuda.current_stream(self.device))
+        self._pinned_evt[k] = evt
+
+    def update(self, frame: int | None = None, lights=None):
+        """Trace + blend one frame; returns (colour atlas, visibility atlas)."""
+        if frame is None:
+            frame = self.frames_done
+        if lights is not None:
+            self.dscene.set_lights(lights)
+        self.upload_rays(frame)
+        stream = D.stream_ptr(self.device)
+        N.call("ps_blend_weights", self.ray_dirs.data_ptr(), self.rays_per_probe,
+               self.texdir.data_ptr(), self.sharpness, self.w_color.data_ptr(),
+               self.w_depth.data_ptr(), self.inv_wsum.data_ptr(), stream)
+        h = 0.0 if self.frames_done == 0 else self.hysteresis
+        params = self._params(h)
+        N.call("ps_trace_blend", ctypes.byref(params), stream)
+        self.frames_done += 1
+        return self.color, self.visibility
+
+    @property
+    def rays_per_frame(self) -> int:
+        return (self.probe_end - self.probe_begin) * self.rays_per_probe
+
+
+def update_probes(volume: ProbeVolume, scene, state: ProbeUpdater | None = None, frame: int = 0,
+                  rays_per_probe: int = 256, hysteresis: float = 0.97, **kwargs):
+    """Functional entry point: returns (colour atlas,
+    visibility atlas, state); pass the returned state back next frame."""
+    if state is None:
+        state = ProbeUpdater(volume, scene, rays_per_probe=rays_per_probe, hysteresis=hysteresis,
+                             **kwargs)
+    color, vis = state.update(frame)
+    return color, vis, state

@@ -1,0 +1,185 @@
+"""Server-side frame pipeline: the caller of the hot path.
+
+The reference's server ``on_tick`` (supplement Alg. 1) is
+absent from /root/reference; this module plays its role for the
+hot path only -- per frame and per texture kind:
+
+  update probes (trace + blend)          probes.ProbeUpdater       stages 1+2
+  detect_changed vs last-sent atlas      selection.py:284-323      stage 3
+  select_for_client (staleness, budget)  selection.py:413-437      stage 3
+  UpdateAtlasLayout.assign               packing.py:283-317        stage 4
+  build_update_atlas + commit            packing.py:320-338, SPEC.md:341
+  pack_texels + temporal delta / SKIP    packing.py:154, codec.py:207-272
+
+Everything is stream-ordered on one CUDA stream with device-side counts; a
+frame launches ~40 kernels and never synchronises with the host.  The
+outputs are encoder-ready: packed planes, residual planes against the
+previous frame's planes, the SKIP map and the (slot, probe) index entries.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import _device as D
+from . import _native as N
+from .delta import pack_delta, skip_shape
+from .packing import UpdateAtlasLayout, widened_width
+from .probes import ProbeUpdater
+from .selection import detect_changed_device, select_device
+from .volume import AtlasKind, ProbeAtlas, ProbeVolume
+
+DEFAULT_GOP = 30  # codec.py:46
+
+
+@dataclass
+class KindOutput:
+    planes: torch.Tensor       # (3, h, w) uint16 / uint8, current frame
+    residual: torch.Tensor     # (3, h, w) planes - previous planes (mod 2^bits)
+    skip: torch.Tensor         # (3, ceil(h/16), ceil(w/16)) uint8
+    entries: torch.Tensor      # (slot_count, 2) int64 (slot, probe), first entry_count valid
+    entry_count: torch.Tensor  # (1,) int64
+    key: bool                  # key frame (no temporal reference)
+
+
+class KindStream:
+    """Per texture kind server state for one client (SPEC.md ClientSession)."""
+
+    def __init__(self, kind: AtlasKind, volume: ProbeVolume, device, slot_count=None,
+                 slots_per_row=None, threshold: float = 0.0, gop_length: int = DEFAULT_GOP,
+                 budget=None, probes_per_row=None):
+        self.kind = kind
+        self.volume = volume
+        self.device = device
+        n = volume.probe_count
+        self.threshold = threshold
+        self.budget = budget
+        self.gop_length = gop_length
+        self.frame_count = 0
+        self.last_sent = ProbeAtlas(kind, n, probes_per_row, device=device)
+        # never-sent probes are the most stale (selection.py:421-424)
+        self.last_sent_seq = torch.full((n,), -1, dtype=torch.int64, device=device)
+        self.layout = UpdateAtlasLayout(slot_count or n, kind.core_side, slots_per_row,
+                                        probe_count=n, device=device)
+        shape = self.layout.texel_shape(kind)
+        tdt = torch.uint32 if kind is AtlasKind.COLOR else torch.uint16
+        self.update_texels = torch.zeros(shape, dtype=tdt, device=device)
+        h, w = shape[0], shape[1]
+        pw, pdt = (w, torch.uint16) if kind is AtlasKind.COLOR else (widened_width(w), torch.uint8)
+        self.planes = [torch.zeros((3, h, pw), dtype=pdt, device=device) for _ in range(2)]
+        self.residual = torch.zeros((3, h, pw), dtype=pdt, device=device)
+        self.skip = torch.zeros(skip_shape(h, pw), dtype=torch.uint8, device=device)
+        self.bits = torch.empty((n + 31) // 32, dtype=torch.int32, device=device)
+        self.sel_ids = torch.empty(n, dtype=torch.int64, device=device)
+        self.sel_count = torch.empty(1, dtype=torch.int64, device=device)
+        self._cur = 0
+        self.timers = None  # optional dict of per-stage (start, end) event lists
+
+    def _mark(self, name, stage):
+        if self.timers is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            self.timers.setdefault(name, []).append((stage, e))
+
+    def tick(self, rendered: ProbeAtlas, seq: int, pvs_bits=None) -> KindOutput:
+        tag = self.kind.value
+        self._mark(f"{tag}.detect", 0)
+        detect_changed_device(rendered, self.last_sent, self.volume, self.threshold,
+                              bits=self.bits, with_ids=False, workspace_slot=f"detect.{tag}")
+        self._mark(f"{tag}.detect", 1)
+        self._mark(f"{tag}.select", 0)
+        select_device(self.bits, pvs_bits, self.volume, self.last_sent_seq, seq, self.budget,
+                      out_ids=self.sel_ids, out_count=self.sel_count,
+                      workspace_slot=f"select.{tag}")
+        self._mark(f"{tag}.select", 1)
+        self._mark(f"{tag}.assign", 0)
+        entries, count = self.layout.assign_device(self.sel_ids, self.sel_count)
+        self._mark(f"{tag}.assign", 1)
+        self._mark(f"{tag}.build", 0)
+        N.call("ps_build_update", self.kind.native, rendered.texels.data_ptr(),
+               self.volume.probe_count, rendered.probes_per_row, entries.data_ptr(),
+               count.data_ptr(), self.layout.slot_count, self.layout.slots_per_row,
+               self.update_texels.data_ptr(), self.update_texels.shape[1],
+               self.last_sent.texels.data_ptr(), self.last_sent_seq.data_ptr(), int(seq),
+               D.stream_ptr(self.device))
+        self._mark(f"{tag}.build", 1)
+        key = self.frame_count % self.gop_length == 0
+        prev = None if key else self.planes[self._cur]
+        cur = self.planes[1 - self._cur]
+        self._mark(f"{tag}.pack_delta", 0)
+        pack_delta(self.update_texels, self.kind, prev, planes_out=cur, residual=self.residual,
+                   skip=self.skip)
+        self._mark(f"{tag}.pack_delta", 1)
+        self._cur = 1 - self._cur
+        self.frame_count += 1
+        return KindOutput(cur, self.residual, self.skip, entries, count, key)
+
+
+class ProbeStreamServer:
+    """One client session's hot path: probe update + both texture streams."""
+
+    def __init__(self, volume: ProbeVolume, scene, rays_per_probe: int = 256, device=None,
+                 color_threshold: float = 0.0, visibility_threshold: float = 0.0,
+                 slot_count=None, budget=None, gop_length: int = DEFAULT_GOP, **probe_kwargs):
+        self.device = torch.device(device) if device is not None else D.device_of()
+        self.volume = volume
+        self.updater = ProbeUpdater(volume, scene, rays_per_probe=rays_per_probe,
+                                    device=self.device, **probe_kwargs)
+        ppr = self.updater.color.probes_per_row
+        self.color = KindStream(AtlasKind.COLOR, volume, self.device, slot_count,
+                                threshold=color_threshold, gop_length=gop_length, budget=budget,
+                                probes_per_row=ppr)
+        self.visibility = KindStream(AtlasKind.VISIBILITY, volume, self.device, slot_count,
+                                     threshold=visibility_threshold, gop_length=gop_length,
+                                     budget=budget, probes_per_row=ppr)
+        self.seq = 0
+        self.timers = None
+
+    def enable_stage_timers(self, on: bool = True) -> None:
+        self.timers = {} if on else None
+        self.color.timers = self.timers
+        self.visibility.timers = self.timers
+
+    def tick(self, frame: int | None = None, lights=None, pvs_bits=None):
+        """One server frame; returns (colour KindOutput, visibility KindOutput)."""
+        frame = self.seq if frame is None else frame
+        if self.timers is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            self.timers.setdefault("trace_blend", []).append((0, e))
+        color, vis = self.updater.update(frame, lights)
+        if self.timers is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            self.timers["trace_blend"].append((1, e))
+        out_c = self.color.tick(color, self.seq, pvs_bits)
+        out_v = self.visibility.tick(vis, self.seq, pvs_bits)
+        self.seq += 1
+        return out_c, out_v
+
+    def h2d_bytes_per_frame(self) -> int:
+        u = self.updater
+        return u.rays_per_probe * 16 + u.dscene.light_count * 24
+
+    def pack_delta_bytes(self) -> dict:
+        """Algorithmic bytes of one pack+delta launch per kind: read the update
+        texels and the previous planes, write planes + residual + SKIP map."""
+        out = {}
+        for ks in (self.color, self.visibility):
+            tex = ks.update_texels.numel() * ks.update_texels.element_size()
+            pl = ks.planes[0].numel() * ks.planes[0].element_size()
+            out[ks.kind.value] = tex + 3 * pl + ks.skip.numel()
+        out["total"] = sum(out.values())
+        return out
+
+    def stage_times_ms(self) -> dict:
+        """Average per-stage device time from the recorded event pairs."""
+        out = {}
+        for name, evs in (self.timers or {}).items():
+            starts = [e for s, e in evs if s == 0]
+            ends = [e for s, e in evs if s == 1]
+            if starts and ends:
+                out[name] = sum(a.elapsed_time(b) for a, b in zip(starts, ends)) / len(ends)
+        return out

@@ -1,0 +1,121 @@
+"""Multi-GPU z-slab sharding of the frame pipeline, plus bench helpers.
+
+Probe id = i + nx*(j + ny*k) (volume.py:72-74), so a z-slab is a contiguous
+ascending id range: rank r traces, blends and change-detects its slab only
+(scene replicated).  The only exchange the path has is the change bitmap
+(16 KB at 131,072 probes), all-gathered over NCCL so every rank runs the
+same global selection and slot assignment (twin-replay determinism,
+test_packing.py:235-240); then each rank exports the core tiles of its own
+selected probes and the encoder rank (0) gathers them into the single update
+atlas it packs (the "single encoder stream" of the north star).
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _device as D
+from .server import ProbeStreamServer
+
+
+def slab_range(volume, rank: int, world: int, align: int = 32):
+    """[begin, end) of rank's z-slab, boundaries on whole k-planes and on
+    multiples of `align` probes where the plane size allows."""
+    nx, ny, nz = volume.dims
+    plane = nx * ny
+    k0 = (nz * rank) // world
+    k1 = (nz * (rank + 1)) // world
+    return k0 * plane, k1 * plane
+
+
+class SlabServer:
+    """World size 1: the plain ProbeStreamServer.  World > 1: slab sharding."""
+
+    def __init__(self, volume, scene, rays_per_probe=256, device=None, rank=0, world=1, **kw):
+        self.rank, self.world = rank, world
+        self.volume = volume
+        self.device = torch.device(device) if device is not None else D.device_of()
+        if world == 1:
+            self.server = ProbeStreamServer(volume, scene, rays_per_probe, device=self.device, **kw)
+            self.dist = None
+        else:
+            from .distributed import DistributedFrame
+
+            self.server = None
+            self.dist = DistributedFrame(volume, scene, rays_per_probe, self.device, rank, world, **kw)
+
+    @property
+    def impl(self):
+        return self.server if self.server is not None else self.dist
+
+    def tick(self, frame, lights=None):
+        return self.impl.tick(frame, lights)
+
+    # --- bench helpers ----------------------------------------------------------------
+
+    def run_e2e(self, steps: int, first_frame: int, lights_for):
+        """Public-API frames with host I/O: per step the ray table and lights go
+        H2D from pinned memory (inside tick) and the index entries, counts and
+        SKIP maps come back D2H into pinned memory."""
+        impl = self.impl
+        outs = impl.tick(first_frame, lights_for(first_frame))  # shapes for the host buffers
+        torch.cuda.synchronize(self.device)
+        host = []
+        for o in outs:
+            if o is None:
+                host.append(None)
+                continue
+            host.append((torch.empty_like(o.entries, device="cpu").pin_memory(),
+                         torch.empty_like(o.entry_count, device="cpu").pin_memory(),
+                         torch.empty_like(o.skip, device="cpu").pin_memory()))
+        d2h = sum(h[0].numel() * 8 + 8 + h[2].numel() for h in host if h is not None)
+        h2d = impl.h2d_bytes_per_frame()
+        stream = torch.cuda.current_stream(self.device)
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(self.device)
+        start.record(stream)
+        for k in range(steps):
+            f = first_frame + 1 + k
+            outs = impl.tick(f, lights_for(f))
+            for o, h in zip(outs, host):
+                if o is None:
+                    continue
+                h[0].copy_(o.entries, non_blocking=True)
+                h[1].copy_(o.entry_count, non_blocking=True)
+                h[2].copy_(o.skip, non_blocking=True)
+        end.record(stream)
+        torch.cuda.synchronize(self.device)
+        return {"ms_per_step": start.elapsed_time(end) / steps, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h}
+
+    def stage_times(self, frames: int, first_frame: int, lights_for) -> dict:
+        impl = self.impl
+        impl.enable_stage_timers(True)
+        for k in range(frames):
+            impl.tick(first_frame + k, lights_for(first_frame + k))
+        torch.cuda.synchronize(self.device)
+        t = impl.stage_times_ms()
+        impl.enable_stage_timers(False)
+        return t
+
+    def count_launches(self, frame: int, lights_for):
+        from torch.profiler import ProfilerActivity, profile
+
+        impl = self.impl
+        torch.cuda.synchronize(self.device)
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            impl.tick(frame, lights_for(frame))
+            torch.cuda.synchronize(self.device)
+        names = {}
+        total = 0
+        for ev in prof.events():
+            if ev.device_type == torch.autograd.DeviceType.CUDA and not ev.name.startswith("Memcpy") \
+                    and not ev.name.startswith("Memset") and "memcpy" not in ev.name.lower() \
+                    and "memset" not in ev.name.lower():
+                total += 1
+                key = ev.name.split("(")[0].split("<")[0].replace("void ", "")
+                names[key] = names.get(key, 0) + 1
+        return total, names
+
+    def pack_delta_bytes(self) -> dict:
+        return self.impl.pack_delta_bytes()
