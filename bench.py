@@ -149,7 +149,8 @@ def run_ours(args, rank, world, local):
     vol = S.volume_for(sc, dims)
     n = vol.probe_count
     server = SlabServer(vol, sc, rays_per_probe=rays, device=dev, rank=rank, world=world,
-                        irradiance_scale=4.0 if scene_name == "hall" else 2.0)
+                        irradiance_scale=4.0 if scene_name == "hall" else 2.0,
+                        shadows=args.shadows)
     stream = torch.cuda.current_stream(dev)
 
     def barrier():
@@ -225,7 +226,8 @@ def run_ours(args, rank, world, local):
                         "+ change detection + selection + slot assign + build + pack + temporal "
                         "delta, colour + visibility",
             "probes": n, "rays_per_probe": rays, "triangles": sc.triangle_count,
-            "lights": len(sc.lights), "shadow_rays": True,
+            "lights": len(sc.lights), "shadows": server.impl.updater.shadows
+            if hasattr(server.impl, "updater") else "map",
             "l2": "per-frame working set (atlases, float state, planes) > 126 MB L2; no flush",
             "parallelism": f"z-slab x{world}",
         },
@@ -262,16 +264,16 @@ def run_ours(args, rank, world, local):
         "kernels": kernel_names,
     }
     if world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(sc, vol, rays, args.cpu_sample)
+        out["cpu_baseline"] = cpu_baseline(sc, vol, rays, args.cpu_sample, args.shadows)
     print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
-def cpu_baseline(sc, vol, rays, sample):
+def cpu_baseline(sc, vol, rays, sample, shadows="map"):
     from oracle import cpu_frame
 
-    r = cpu_frame.time_frame(sc, vol, rays, sample_probes=sample)
+    r = cpu_frame.time_frame(sc, vol, rays, sample_probes=sample, shadows=shadows)
     return {
         "value": round(vol.probe_count / r["frame_s"], 3),
         "unit": "probe updates/s",
@@ -301,11 +303,12 @@ def run_reference(args, rank, world, local):
     times = []
     for k in range(args.steps):
         r = cpu_frame.time_frame(sc, vol, rays, sample_probes=args.cpu_sample, frame=k,
-                                 stages_full=(k == 0), rng_seed=k)
+                                 stages_full=(k == 0), rng_seed=k, shadows=args.shadows)
         times.append(r)
     stages = times[0]["stages_s"]
     per_probe = sum(t["trace_shade_s_per_probe"] + t["blend_s_per_probe"] for t in times) / len(times)
-    frame_s = per_probe * vol.probe_count + stages
+    map_s = sum(t["shadow_map_s"] for t in times) / len(times)
+    frame_s = per_probe * vol.probe_count + map_s + stages
     value = vol.probe_count / frame_s
     out = {
         "metric": METRIC, "value": round(value, 3), "unit": "probe updates/s", "impl": "reference",
@@ -334,6 +337,7 @@ def main():
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--cpu-sample", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shadows", default="map", choices=["map", "rays", "none"])
     args = ap.parse_args()
     if args.warmup < 3:
         log("warmup raised to 3 (timing rules)")

@@ -41,6 +41,10 @@ extern "C" {
 #define PS_KIND_COLOR 0
 #define PS_KIND_VISIBILITY 1
 
+#define PS_SHADOW_NONE 0
+#define PS_SHADOW_RAYS 1
+#define PS_SHADOW_MAP 2
+
 /* device-side status word bits (written by kernels, read by the shim) */
 #define PS_DEV_SLOT_OVERFLOW 1u   /* selection larger than slot_count, nothing mutated */
 #define PS_DEV_INDEX 2u           /* id outside [0, probe_count)                       */
@@ -203,7 +207,16 @@ typedef struct ps_trace_params {
     float sky[3];
     float max_distance;
     float normal_bias;
-    int32_t shadows;         /* trace a shadow ray per light at each hit */
+    /* direct-light visibility at probe-ray hits:
+     *   PS_SHADOW_NONE  unshadowed
+     *   PS_SHADOW_RAYS  one any-hit shadow ray per light per hit
+     *   PS_SHADOW_MAP   per-light cube distance maps traced from the light
+     *                   each frame (the paper's server renders shadow maps,
+     *                   PAPER.md:370), one lookup per light per hit */
+    int32_t shadow_mode;
+    int32_t shadow_map_size; /* cube face side S (PS_SHADOW_MAP)              */
+    float *shadow_maps;      /* light_count * 6 * S * S distances (scratch)   */
+    float shadow_bias;       /* relative slack of the map depth compare       */
     /* blend */
     const float *w_color;    /* (rays, 64) cosine weights, transposed       */
     const float *w_depth;    /* (rays, 256) cosine^sharpness weights        */
@@ -218,6 +231,11 @@ typedef struct ps_trace_params {
     uint16_t *vis_atlas;
     int32_t probes_per_row_color;
     int32_t probes_per_row_vis;
+    /* per-ray records written by the trace pass and read by the blend pass:
+     * ((probe_end - probe_begin) * rays) float4 {radiance rgb, depth} */
+    float *records;
+    /* scratch: one uint32 work counter (dynamic ray-chunk scheduling) */
+    uint32_t *work_counter;
     /* optional per-ray debug record ((probe_end - probe_begin) * rays, 8
      * floats: radiance rgb, depth, hit t (inf = miss), prim id (int bits,
      * -1 = miss), shadow mask (int bits, bit l = light l visible), 0);

@@ -21,8 +21,9 @@ from . import stream_ops as so
 
 
 def time_frame(scene, volume, rays_per_probe: int, sample_probes: int = 4, seed: int = 0,
-               frame: int = 0, shadows: bool = True, max_distance=None, bias=None,
-               stages_full: bool = True, rng_seed: int = 0) -> dict:
+               frame: int = 0, shadows: str = "map", max_distance=None, bias=None,
+               stages_full: bool = True, rng_seed: int = 0, shadow_map_size: int = 256,
+               map_sample: int = 2048) -> dict:
     """Returns a dict of seconds per stage and the extrapolated frame time."""
     n = volume.probe_count
     (x0, y0, z0), (x1, y1, z1) = scene.bounds
@@ -34,13 +35,33 @@ def time_frame(scene, volume, rays_per_probe: int, sample_probes: int = 4, seed:
     dirs = ddgi.ray_table(rays_per_probe, seed, frame).astype(np.float64)
     lights = [(l.position, l.intensity) for l in scene.lights]
 
+    # load (and if needed build) the C oracle and spin up its thread pool
+    # outside the timed regions
+    ddgi.raycast(scene.vertices[:1], np.zeros((1, 3)), np.ones((64, 3)))
+    map_s = 0.0
+    maps = None
+    if shadows == "map" and lights:
+        # cube distance maps are a fixed per-frame cost: time a sample of map
+        # texels per light with the same brute-force query and scale it
+        S = shadow_map_size
+        dirs_map = ddgi.shadow_map_dirs(S).reshape(-1, 3).astype(np.float64)
+        pick = rng.choice(len(dirs_map), size=min(map_sample, len(dirs_map)), replace=False)
+        maps = np.full((len(lights), 6 * S * S), np.inf)
+        m0 = time.perf_counter()
+        for li, (lp, _) in enumerate(lights):
+            tm, _ = ddgi.raycast(scene.vertices, np.asarray(lp, np.float64)[None, :], dirs_map[pick])
+            maps[li, pick] = tm
+        map_s = (time.perf_counter() - m0) * (6 * S * S) / len(pick)
+        maps = maps.reshape(len(lights), 6, S, S)
+
     t0 = time.perf_counter()
     pos = volume.probe_positions(ids).astype(np.float32).astype(np.float64)
     O = np.repeat(pos, rays_per_probe, axis=0)
     D = np.tile(dirs, (len(ids), 1))
     t, prim = ddgi.raycast(scene.vertices, O, D)
     rgb, depth, _ = ddgi.shade(scene.vertices, scene.albedo, scene.emission, lights, scene.sky,
-                               O, D, t, prim, max_distance, bias, shadows)
+                               O, D, t, prim, max_distance, bias, shadows, shadow_map_size, 0.02,
+                               maps)
     t1 = time.perf_counter()
     w = ddgi.blend_weights(dirs.astype(np.float32), 50.0)
     irr, mom = ddgi.blend(rgb.reshape(len(ids), rays_per_probe, 3).astype(np.float32),
@@ -52,6 +73,7 @@ def time_frame(scene, volume, rays_per_probe: int, sample_probes: int = 4, seed:
     per_probe = (t2 - t0) / len(ids)
     out = {"trace_shade_s_per_probe": (t1 - t0) / len(ids),
            "blend_s_per_probe": (t2 - t1) / len(ids),
+           "shadow_map_s": map_s,
            "sample_probes": int(len(ids)),
            "sample_rays": int(len(ids) * rays_per_probe)}
     stages = 0.0
@@ -72,6 +94,6 @@ def time_frame(scene, volume, rays_per_probe: int, sample_probes: int = 4, seed:
             so.temporal_delta(planes, planes ^ planes.dtype.type(1))
             stages += time.perf_counter() - s0
     out["stages_s"] = stages
-    out["frame_s"] = per_probe * n + stages
+    out["frame_s"] = per_probe * n + map_s + stages
     out["threads"] = os.cpu_count()
     return out

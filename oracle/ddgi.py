@@ -130,9 +130,59 @@ def ray_table(count: int, seed: int, frame: int) -> np.ndarray:
 # --- shading (float64, given hits) --------------------------------------------------------
 
 
+def shadow_map_dirs(S: int) -> np.ndarray:
+    """(6, S, S, 3) texel directions of a cube distance map, float32 as the
+    device computes them: face f looks along axis f//2 (negative if f odd),
+    texel (j, i) adds u_i on axis (a+1)%3 and w_j on axis (a+2)%3."""
+    c = ((np.arange(S, dtype=np.float32) + np.float32(0.5)) / np.float32(S)) * np.float32(2) - np.float32(1)
+    out = np.zeros((6, S, S, 3), np.float32)
+    for f in range(6):
+        a = f // 2
+        out[f, :, :, a] = np.float32(-1.0 if f % 2 else 1.0)
+        out[f, :, :, (a + 1) % 3] = c[None, :]
+        out[f, :, :, (a + 2) % 3] = c[:, None]
+    norm = np.sqrt(np.sum(out.astype(np.float64) ** 2, axis=-1, keepdims=True))
+    return (out / norm).astype(np.float32)
+
+
+def shadow_maps(tris, lights, S: int) -> np.ndarray:
+    """(L, 6, S, S) nearest-hit distance from each light (inf on a miss)."""
+    d = shadow_map_dirs(S).reshape(-1, 3).astype(np.float64)
+    maps = []
+    for lp, _ in lights:
+        t, _prim = raycast(tris, np.asarray(lp, np.float64)[None, :], d)
+        maps.append(t.reshape(6, S, S))
+    return np.stack(maps) if maps else np.zeros((0, 6, S, S))
+
+
+def cube_lookup(maps_l, v, S):
+    """Map value for light-to-point vectors v (n, 3) of one light."""
+    av = np.abs(v)
+    a = np.where((av[:, 0] >= av[:, 1]) & (av[:, 0] >= av[:, 2]), 0,
+                 np.where(av[:, 1] >= av[:, 2], 1, 2))
+    rows = np.arange(len(v))
+    m = av[rows, a]
+    sgn = v[rows, a]
+    u = v[rows, (a + 1) % 3] / m
+    w = v[rows, (a + 2) % 3] / m
+    f = 2 * a + (sgn < 0)
+    i = np.clip(np.floor((u * 0.5 + 0.5) * S).astype(np.int64), 0, S - 1)
+    j = np.clip(np.floor((w * 0.5 + 0.5) * S).astype(np.int64), 0, S - 1)
+    return maps_l[f, j, i]
+
+
 def shade(tris, albedo, emission, lights, sky, origins, dirs, t, prim, max_distance, bias,
-          shadows=True):
-    """Radiance and depth per ray, float64; returns (rgb (n,3), depth (n,), mask)."""
+          shadows="rays", shadow_map_size=256, shadow_bias=0.02, maps=None):
+    """Radiance and depth per ray, float64; returns (rgb (n,3), depth (n,), mask).
+
+    shadows: "rays" (exact shadow ray), "map" (cube distance maps from the
+    lights, see shadow_map_dirs), "none"."""
+    if shadows is True:
+        shadows = "rays"
+    elif not shadows:
+        shadows = "none"
+    if shadows == "map" and maps is None:
+        maps = shadow_maps(tris, lights, shadow_map_size)
     n = len(dirs)
     rgb = np.tile(np.asarray(sky, np.float64), (n, 1))
     depth = np.full(n, float(max_distance))
@@ -159,10 +209,13 @@ def shade(tris, albedo, emission, lights, sky, origins, dirs, t, prim, max_dista
         u = lv / dist[:, None]
         cos = np.sum(nn * u, axis=1)
         ok = (d2 > 0) & (cos > 0)
-        if shadows and ok.any():
+        if shadows == "rays" and ok.any():
             blocked = occluded(tris, s[ok], u[ok], dist[ok])
             vis = ok.copy()
             vis[np.nonzero(ok)[0][blocked]] = False
+        elif shadows == "map" and ok.any():
+            dm = cube_lookup(maps[li], s - np.asarray(lp, np.float64), shadow_map_size)
+            vis = ok & (dist <= dm * (1.0 + shadow_bias))
         else:
             vis = ok
         mask[idx[vis]] |= 1 << li

@@ -29,6 +29,10 @@ PS_ERR_WORKSPACE = -6
 PS_KIND_COLOR = 0
 PS_KIND_VISIBILITY = 1
 
+PS_SHADOW_NONE = 0
+PS_SHADOW_RAYS = 1
+PS_SHADOW_MAP = 2
+
 PS_DEV_SLOT_OVERFLOW = 1
 PS_DEV_INDEX = 2
 
@@ -50,12 +54,14 @@ class TraceParams(C.Structure):
         ("nodes", _vp), ("tris", _vp), ("materials", _vp),
         ("light_count", _i32), ("lights", _vp),
         ("sky", _f32 * 3), ("max_distance", _f32), ("normal_bias", _f32),
-        ("shadows", _i32),
+        ("shadow_mode", _i32), ("shadow_map_size", _i32), ("shadow_maps", _vp),
+        ("shadow_bias", _f32),
         ("w_color", _vp), ("w_depth", _vp), ("inv_wsum", _vp),
         ("hysteresis", _f32), ("irradiance_scale", _f32),
         ("irradiance", _vp), ("moments", _vp),
         ("color_atlas", _vp), ("vis_atlas", _vp),
         ("probes_per_row_color", _i32), ("probes_per_row_vis", _i32),
+        ("records", _vp), ("work_counter", _vp),
         ("ray_records", _vp),
     ]
 

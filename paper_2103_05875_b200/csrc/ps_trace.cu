@@ -157,6 +157,28 @@ struct Shade {
     int shadow_mask;
 };
 
+// cube shadow map face / texel of a light-to-point vector (see shadow_map_kernel)
+__device__ __forceinline__ int cube_texel(float vx, float vy, float vz, int S) {
+    const float ax = fabsf(vx), ay = fabsf(vy), az = fabsf(vz);
+    int a;
+    float m, u, w, sgn;
+    if (ax >= ay && ax >= az) {
+        a = 0; m = ax; sgn = vx; u = vy; w = vz;
+    } else if (ay >= az) {
+        a = 1; m = ay; sgn = vy; u = vz; w = vx;
+    } else {
+        a = 2; m = az; sgn = vz; u = vx; w = vy;
+    }
+    const int f = 2 * a + (sgn < 0.0f ? 1 : 0);
+    const float inv = 1.0f / m;
+    int i = int(floorf(fmaf(u * inv, 0.5f, 0.5f) * float(S)));
+    int j = int(floorf(fmaf(w * inv, 0.5f, 0.5f) * float(S)));
+    i = min(max(i, 0), S - 1);
+    j = min(max(j, 0), S - 1);
+    return (f * S + j) * S + i;
+}
+
+template <int SHADOW>
 __device__ Shade shade_ray(const ps_trace_params &p, const float4 *nodes, const float4 *tris,
                            const Ray &ray) {
     Shade s;
@@ -187,9 +209,10 @@ __device__ Shade shade_ray(const ps_trace_params &p, const float4 *nodes, const 
                 sz = fmaf(nz, p.normal_bias, hz);
     float lr = 0.f, lg = 0.f, lb = 0.f;
     const float *L = p.lights;
+    const int S = p.shadow_map_size;
     for (int l = 0; l < p.light_count; ++l) {
-        const float lx = __ldg(L + 6 * l) - sx, ly = __ldg(L + 6 * l + 1) - sy,
-                    lz = __ldg(L + 6 * l + 2) - sz;
+        const float px = __ldg(L + 6 * l), py = __ldg(L + 6 * l + 1), pz = __ldg(L + 6 * l + 2);
+        const float lx = px - sx, ly = py - sy, lz = pz - sz;
         const float d2 = dot3(lx, ly, lz, lx, ly, lz);
         if (!(d2 > 0.0f)) continue;
         const float dist = sqrtf(d2);
@@ -197,10 +220,14 @@ __device__ Shade shade_ray(const ps_trace_params &p, const float4 *nodes, const 
         const float ux = lx * inv, uy = ly * inv, uz = lz * inv;
         const float cosv = dot3(nx, ny, nz, ux, uy, uz);
         if (!(cosv > 0.0f)) continue;
-        if (p.shadows) {
+        if (SHADOW == PS_SHADOW_RAYS) {
             Ray sh{sx, sy, sz, ux, uy, uz};
             float ts;
             if (traverse<true>(nodes, tris, sh, dist, ts) >= 0) continue;
+        } else if (SHADOW == PS_SHADOW_MAP) {
+            const float dm = __ldg(p.shadow_maps + int64_t(l) * 6 * S * S +
+                                   cube_texel(-lx, -ly, -lz, S));
+            if (dist > dm * (1.0f + p.shadow_bias)) continue;
         }
         s.shadow_mask |= 1 << l;
         const float k = cosv / d2;
@@ -235,59 +262,114 @@ __device__ __forceinline__ int guard_source(int r, int c, int side) {
     return (rr - 1) * n + (cc - 1);
 }
 
+// ---- pass 0: cube distance maps traced from each light ------------------------------
+// face f: axis a = f / 2, sign = f % 2 ? -1 : +1, (b, c) = ((a+1)%3, (a+2)%3);
+// texel (i, j): direction e_a*sign + e_b*u + e_c*w with u = (i+.5)/S*2-1,
+// w = (j+.5)/S*2-1, normalised; value = nearest hit distance (inf on a miss).
+__global__ void __launch_bounds__(256) shadow_map_kernel(ps_trace_params prm) {
+    const int S = prm.shadow_map_size;
+    const int64_t per_light = int64_t(6) * S * S;
+    const int64_t total = per_light * prm.light_count;
+    const float4 *nodes = reinterpret_cast<const float4 *>(prm.nodes);
+    const float4 *tris = reinterpret_cast<const float4 *>(prm.tris);
+    for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
+         idx += int64_t(gridDim.x) * blockDim.x) {
+        const int l = int(idx / per_light);
+        const int rem = int(idx - int64_t(l) * per_light);
+        const int f = rem / (S * S);
+        const int j = (rem / S) % S, i = rem % S;
+        const int a = f >> 1;
+        const float sgn = (f & 1) ? -1.0f : 1.0f;
+        const float u = (float(i) + 0.5f) / float(S) * 2.0f - 1.0f;
+        const float w = (float(j) + 0.5f) / float(S) * 2.0f - 1.0f;
+        float d[3];
+        d[a] = sgn;
+        d[(a + 1) % 3] = u;
+        d[(a + 2) % 3] = w;
+        const float inv = 1.0f / sqrtf(dot3(d[0], d[1], d[2], d[0], d[1], d[2]));
+        Ray ray{__ldg(prm.lights + 6 * l), __ldg(prm.lights + 6 * l + 1),
+                __ldg(prm.lights + 6 * l + 2), d[0] * inv, d[1] * inv, d[2] * inv};
+        float t;
+        const int slot = traverse<false>(nodes, tris, ray, INFINITY, t);
+        prm.shadow_maps[idx] = slot < 0 ? INFINITY : t;
+    }
+}
+
+// ---- pass 1: probe rays -> per-ray records (persistent, dynamic chunks) -----------------
+// A warp claims 32 consecutive rays of one probe (neighbouring directions in
+// the coherence-ordered set) from a global counter, traces + shades them and
+// writes {rgb, depth}.  Dynamic claiming keeps every SM busy regardless of the
+// large per-direction cost differences.
+template <int SHADOW>
+__global__ void __launch_bounds__(THREADS) trace_kernel(ps_trace_params prm) {
+    const float4 *nodes = reinterpret_cast<const float4 *>(prm.nodes);
+    const float4 *tris = reinterpret_cast<const float4 *>(prm.tris);
+    const float4 *dirs = reinterpret_cast<const float4 *>(prm.ray_dirs);
+    const int R = prm.rays_per_probe;
+    const int64_t nloc = int64_t(prm.probe_end) - prm.probe_begin;
+    const int64_t total_rays = nloc * R;
+    const int64_t chunks_per_probe = (R + 31) / 32;
+    const int64_t total_chunks = nloc * chunks_per_probe;
+    const int lane = threadIdx.x & 31;
+    float4 *records = reinterpret_cast<float4 *>(prm.records);
+    while (true) {
+        uint32_t task = 0;
+        if (lane == 0) task = atomicAdd(prm.work_counter, 1u);
+        task = __shfl_sync(0xffffffffu, task, 0);
+        if (int64_t(task) >= total_chunks) break;
+        const int64_t q = int64_t(task) / chunks_per_probe;
+        const int r = int(int64_t(task) - q * chunks_per_probe) * 32 + lane;
+        if (r >= R) continue;
+        const int64_t p = prm.probe_begin + q;
+        const int64_t i = p % prm.nx, j = (p / prm.nx) % prm.ny, k = p / (int64_t(prm.nx) * prm.ny);
+        Ray ray;
+        // origin + spacing * (i, j, k) in double, rounded once (no FMA
+        // contraction, as numpy evaluates volume.py:138)
+        ray.ox = float(__dadd_rn(prm.origin[0], __dmul_rn(prm.spacing[0], double(i))));
+        ray.oy = float(__dadd_rn(prm.origin[1], __dmul_rn(prm.spacing[1], double(j))));
+        ray.oz = float(__dadd_rn(prm.origin[2], __dmul_rn(prm.spacing[2], double(k))));
+        const float4 d = __ldg(dirs + r);
+        ray.dx = d.x;
+        ray.dy = d.y;
+        ray.dz = d.z;
+        const Shade s = shade_ray<SHADOW>(prm, nodes, tris, ray);
+        const int64_t ray_id = q * R + r;
+        records[ray_id] = make_float4(s.r, s.g, s.b, s.depth);
+        if (prm.ray_records) {
+            float4 *rec = reinterpret_cast<float4 *>(prm.ray_records) + 2 * ray_id;
+            rec[0] = make_float4(s.r, s.g, s.b, s.depth);
+            rec[1] = make_float4(s.t, __int_as_float(s.prim), __int_as_float(s.shadow_mask), 0.f);
+        }
+        (void)total_rays;
+    }
+}
+
+// ---- pass 2: DDGI blend of P probes per CTA ---------------------------------------------
 template <int P>
-__global__ void __launch_bounds__(THREADS) trace_blend_kernel(ps_trace_params prm) {
+__global__ void __launch_bounds__(THREADS) blend_kernel(ps_trace_params prm) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int R = prm.rays_per_probe;
-    float4 *s_dir = reinterpret_cast<float4 *>(smem_raw);          // R
-    float4 *s_rgb = s_dir + R;                                       // R * P   [r][q]
-    float2 *s_dep = reinterpret_cast<float2 *>(s_rgb + R * P);      // R * P   [r][q] (d, d^2)
+    float4 *s_rgb = reinterpret_cast<float4 *>(smem_raw);            // R * P   [r][q]
+    float2 *s_dep = reinterpret_cast<float2 *>(s_rgb + R * P);       // R * P   [r][q] (d, d^2)
     uint32_t *s_ccore = reinterpret_cast<uint32_t *>(s_dep + R * P); // P * 64
     uint32_t *s_vcore = s_ccore + P * 64;                            // P * 256
 
-    const float4 *nodes = reinterpret_cast<const float4 *>(prm.nodes);
-    const float4 *tris = reinterpret_cast<const float4 *>(prm.tris);
     const int tid = threadIdx.x;
     const int64_t p0 = int64_t(prm.probe_begin) + int64_t(blockIdx.x) * P;
     const int64_t left = int64_t(prm.probe_end) - p0;
     const int nq = int(left < P ? left : P);
-
-    for (int r = tid; r < R; r += THREADS) s_dir[r] = __ldg(reinterpret_cast<const float4 *>(prm.ray_dirs) + r);
-    __syncthreads();
-
-    // ---- phase 1: trace ---------------------------------------------------------
+    const float4 *records = reinterpret_cast<const float4 *>(prm.records) +
+                            (p0 - prm.probe_begin) * R;
     for (int g = tid; g < P * R; g += THREADS) {
         const int q = g / R, r = g - q * R;
-        Shade s;
-        if (q < nq) {
-            const int64_t p = p0 + q;
-            const int64_t i = p % prm.nx, j = (p / prm.nx) % prm.ny, k = p / (int64_t(prm.nx) * prm.ny);
-            Ray ray;
-            // origin + spacing * (i, j, k) in double, rounded once (no FMA
-            // contraction, as numpy evaluates volume.py:138)
-            ray.ox = float(__dadd_rn(prm.origin[0], __dmul_rn(prm.spacing[0], double(i))));
-            ray.oy = float(__dadd_rn(prm.origin[1], __dmul_rn(prm.spacing[1], double(j))));
-            ray.oz = float(__dadd_rn(prm.origin[2], __dmul_rn(prm.spacing[2], double(k))));
-            const float4 d = s_dir[r];
-            ray.dx = d.x;
-            ray.dy = d.y;
-            ray.dz = d.z;
-            s = shade_ray(prm, nodes, tris, ray);
-            if (prm.ray_records) {
-                float4 *rec = reinterpret_cast<float4 *>(prm.ray_records) +
-                              2 * ((p - prm.probe_begin) * R + r);
-                rec[0] = make_float4(s.r, s.g, s.b, s.depth);
-                rec[1] = make_float4(s.t, __int_as_float(s.prim), __int_as_float(s.shadow_mask), 0.f);
-            }
-        } else {
-            s.r = s.g = s.b = s.depth = 0.f;
-        }
-        s_rgb[r * P + q] = make_float4(s.r, s.g, s.b, 0.f);
-        s_dep[r * P + q] = make_float2(s.depth, s.depth * s.depth);
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (q < nq) v = __ldcs(records + g);  // streamed once
+        s_rgb[r * P + q] = make_float4(v.x, v.y, v.z, 0.f);
+        s_dep[r * P + q] = make_float2(v.w, v.w * v.w);
     }
     __syncthreads();
 
-    // ---- phase 2a: irradiance (64 texels x P probes) ------------------------------
+    // ---- irradiance (64 texels x P probes) --------------------------------------------
     {
         constexpr int QPT = (P + 3) / 4;  // probes per thread
         const int t = tid & 63, qg = tid >> 6;
@@ -329,7 +411,7 @@ __global__ void __launch_bounds__(THREADS) trace_blend_kernel(ps_trace_params pr
             s_ccore[q * 64 + t] = texel;
         }
     }
-    // ---- phase 2b: depth moments (256 texels x P probes) -----------------------------
+    // ---- depth moments (256 texels x P probes) ------------------------------------------
     {
         const int t = tid;
         float m1[P], m2[P];
@@ -369,7 +451,7 @@ __global__ void __launch_bounds__(THREADS) trace_blend_kernel(ps_trace_params pr
     }
     __syncthreads();
 
-    // ---- phase 3: atlas blocks with guard bands ------------------------------------------
+    // ---- atlas blocks with guard bands ----------------------------------------------------
     {
         const int ppr = prm.probes_per_row_color;
         const int64_t W = int64_t(ppr) * 10;
@@ -424,8 +506,16 @@ __global__ void wsum_kernel(int R, const float *w_color, const float *w_depth, f
 
 constexpr int PROBES_PER_CTA = 8;
 
-size_t trace_smem_bytes(int R, int P) {
-    return size_t(R) * 16 + size_t(R) * P * 16 + size_t(R) * P * 8 + size_t(P) * (64 + 256) * 4;
+size_t blend_smem_bytes(int R, int P) {
+    return size_t(R) * P * 16 + size_t(R) * P * 8 + size_t(P) * (64 + 256) * 4;
+}
+
+template <class K>
+int resident_blocks(K kernel, int threads, size_t smem) {
+    int n = 0;
+    check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, smem),
+               "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+    return n > 0 ? n : 1;
 }
 
 }  // namespace
@@ -459,23 +549,57 @@ int ps_trace_blend(const ps_trace_params *params, void *stream) {
     const int64_t n = int64_t(p.nx) * p.ny * p.nz;
     if (p.probe_begin < 0 || p.probe_end > n || p.probe_begin > p.probe_end)
         fail(PS_ERR_INDEX, "probe range outside the volume");
-    if (p.rays_per_probe < 1 || p.rays_per_probe > 4096) fail(PS_ERR_VALUE, "rays_per_probe in [1, 4096]");
+    if (p.rays_per_probe < 1 || p.rays_per_probe > 2048) fail(PS_ERR_VALUE, "rays_per_probe in [1, 2048]");
     if (p.light_count < 0 || p.light_count > 30) fail(PS_ERR_VALUE, "light_count in [0, 30]");
     if (p.probes_per_row_color < 1 || p.probes_per_row_vis < 1) fail(PS_ERR_LAYOUT, "bad atlas layout");
+    if (p.shadow_mode < PS_SHADOW_NONE || p.shadow_mode > PS_SHADOW_MAP) fail(PS_ERR_VALUE, "bad shadow_mode");
+    if (p.shadow_mode == PS_SHADOW_MAP && p.light_count > 0 &&
+        (p.shadow_map_size < 1 || p.shadow_map_size > 4096 || !p.shadow_maps))
+        fail(PS_ERR_VALUE, "shadow map size / buffer missing");
+    if (!p.records || !p.work_counter) fail(PS_ERR_VALUE, "records / work_counter scratch missing");
     const int64_t nloc = p.probe_end - p.probe_begin;
     if (nloc == 0) return PS_OK;
-    const size_t smem = trace_smem_bytes(p.rays_per_probe, PROBES_PER_CTA);
+    auto s = as_stream(stream);
+    const int sms = sm_count();
+    // pass 0: shadow maps
+    if (p.shadow_mode == PS_SHADOW_MAP && p.light_count > 0) {
+        const int64_t texels = int64_t(p.light_count) * 6 * p.shadow_map_size * p.shadow_map_size;
+        const unsigned blocks = unsigned(std::min<int64_t>(ceil_div(texels, 256), int64_t(sms) * 32));
+        shadow_map_kernel<<<blocks, 256, 0, s>>>(p);
+        check_launch("shadow_map_kernel");
+    }
+    // pass 1: persistent trace with dynamic chunk claiming
+    check_cuda(cudaMemsetAsync(p.work_counter, 0, sizeof(uint32_t), s), "memset counter");
+    {
+        int per_sm;
+        switch (p.shadow_mode) {
+            case PS_SHADOW_NONE:
+                per_sm = resident_blocks(trace_kernel<PS_SHADOW_NONE>, THREADS, 0);
+                trace_kernel<PS_SHADOW_NONE><<<sms * per_sm, THREADS, 0, s>>>(p);
+                break;
+            case PS_SHADOW_RAYS:
+                per_sm = resident_blocks(trace_kernel<PS_SHADOW_RAYS>, THREADS, 0);
+                trace_kernel<PS_SHADOW_RAYS><<<sms * per_sm, THREADS, 0, s>>>(p);
+                break;
+            default:
+                per_sm = resident_blocks(trace_kernel<PS_SHADOW_MAP>, THREADS, 0);
+                trace_kernel<PS_SHADOW_MAP><<<sms * per_sm, THREADS, 0, s>>>(p);
+                break;
+        }
+        check_launch("trace_kernel");
+    }
+    // pass 2: blend
+    const size_t smem = blend_smem_bytes(p.rays_per_probe, PROBES_PER_CTA);
     static bool attr_set = false;
     if (!attr_set) {
-        check_cuda(cudaFuncSetAttribute(trace_blend_kernel<PROBES_PER_CTA>,
+        check_cuda(cudaFuncSetAttribute(blend_kernel<PROBES_PER_CTA>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
                    "cudaFuncSetAttribute");
         attr_set = true;
     }
     if (smem > 200 * 1024) fail(PS_ERR_VALUE, "too many rays per probe for shared memory");
-    const unsigned blocks = unsigned(ceil_div(nloc, PROBES_PER_CTA));
-    trace_blend_kernel<PROBES_PER_CTA><<<blocks, THREADS, smem, as_stream(stream)>>>(p);
-    check_launch("trace_blend_kernel");
+    blend_kernel<PROBES_PER_CTA><<<unsigned(ceil_div(nloc, PROBES_PER_CTA)), THREADS, smem, s>>>(p);
+    check_launch("blend_kernel");
     PS_ABI_END
 }
 

@@ -15,9 +15,17 @@ normals).  Every probe uses the same rotated set, as in DDGI.
 Tracing (device): ray origin = probe position (volume.py:127-138), nearest
 hit with the reference raycast semantics (selection.py:66-149).  A hit is
 shaded ``emission + albedo * sum_l I_l * cos / d^2 * V_l`` with the normal
-facing the ray and ``V_l`` a shadow ray from ``hit + bias * n``; a miss
+facing the ray and the light seen from ``s = hit + bias * n``; a miss
 returns the sky colour.  Depth = ``min(t, max_distance)`` (miss:
-``max_distance``).
+``max_distance``).  ``V_l`` (``shadows``):
+  "map"  -- default, as the paper's server (shadow-mapped direct light,
+            PAPER.md:370): each frame a cube distance map of side S is traced
+            from every light (face f: axis f//2, sign -1 if f odd; texel
+            (i, j) looks along e_a*sign + e_b*u + e_c*w, u = (i+.5)/S*2-1,
+            w = (j+.5)/S*2-1, b, c = a+1, a+2 mod 3); V = |light - s| <=
+            map[face, texel of (s - light)] * (1 + shadow_bias);
+  "rays" -- an exact any-hit shadow ray s -> light;
+  "none" -- V = 1.
 
 Blend (device): colour texel t (8x8, texel_directions) averages radiance
 with weights ``max(0, n_t . d_r)``; depth texel t (16x16) averages depth and
@@ -108,9 +116,10 @@ class ProbeUpdater:
 
     def __init__(self, volume: ProbeVolume, scene: Scene | DeviceScene, rays_per_probe: int = 256,
                  hysteresis: float = 0.97, sharpness: float = 50.0, max_distance: float | None = None,
-                 irradiance_scale: float = 1.0, shadows: bool = True, normal_bias: float | None = None,
+                 irradiance_scale: float = 1.0, shadows="map", normal_bias: float | None = None,
                  seed: int = 0, probe_range=None, probes_per_row: int | None = None,
-                 device=None, record_rays: bool = False):
+                 device=None, record_rays: bool = False, shadow_map_size: int = 256,
+                 shadow_bias: float = 0.02):
         self.volume = volume
         self.device = torch.device(device) if device is not None else D.device_of()
         self.dscene = scene if isinstance(scene, DeviceScene) else scene.device(self.device)
@@ -122,7 +131,18 @@ class ProbeUpdater:
         self.sharpness = float(sharpness)
         self.max_distance = float(max_distance if max_distance is not None else diag)
         self.irradiance_scale = float(irradiance_scale)
-        self.shadows = bool(shadows)
+        # shadows: "map" (cube distance maps traced from each light, the
+        # paper's shadow-mapped server), "rays" (exact shadow rays), "none";
+        # booleans map True -> "rays", False -> "none"
+        if shadows is True:
+            shadows = "rays"
+        elif shadows is False or shadows is None:
+            shadows = "none"
+        self.shadow_mode = {"none": N.PS_SHADOW_NONE, "rays": N.PS_SHADOW_RAYS,
+                            "map": N.PS_SHADOW_MAP}[shadows]
+        self.shadows = shadows
+        self.shadow_map_size = int(shadow_map_size)
+        self.shadow_bias = float(shadow_bias)
         self.normal_bias = float(normal_bias if normal_bias is not None else 1e-3 * diag)
         self.seed = int(seed)
         n = volume.probe_count
@@ -144,6 +164,11 @@ class ProbeUpdater:
         self._pinned_evt = [None, None]
         self.ray_records = (torch.empty((max(nloc, 1) * R, 8), dtype=torch.float32, device=dev)
                             if record_rays else None)
+        self.records = torch.empty((max(nloc, 1) * R, 4), dtype=torch.float32, device=dev)
+        self.work_counter = torch.zeros(1, dtype=torch.int32, device=dev)
+        S = self.shadow_map_size
+        self.shadow_maps = (torch.empty((self.dscene.MAX_LIGHTS, 6, S, S), dtype=torch.float32,
+                                        device=dev) if self.shadow_mode == N.PS_SHADOW_MAP else None)
         self.frames_done = 0
 
     def _params(self, hysteresis: float) -> N.TraceParams:
@@ -161,7 +186,12 @@ class ProbeUpdater:
         p.sky = (ctypes.c_float * 3)(*map(float, s.scene.sky))
         p.max_distance = self.max_distance
         p.normal_bias = self.normal_bias
-        p.shadows = int(self.shadows)
+        p.shadow_mode = self.shadow_mode
+        p.shadow_map_size = self.shadow_map_size
+        p.shadow_maps = self.shadow_maps.data_ptr() if self.shadow_maps is not None else None
+        p.shadow_bias = self.shadow_bias
+        p.records = self.records.data_ptr()
+        p.work_counter = self.work_counter.data_ptr()
         p.w_color, p.w_depth, p.inv_wsum = (self.w_color.data_ptr(), self.w_depth.data_ptr(),
                                             self.inv_wsum.data_ptr())
         p.hysteresis = hysteresis

@@ -62,9 +62,25 @@ def _check_trace(upd, sc, frame, max_mismatch=2e-3):
     assert np.all(rel[prim_ok] < 1e-4), rel.max()
     # shading with the oracle's own shadow rays, on rays whose hit agrees
     lights = [(l.position, l.intensity) for l in upd.dscene.scene.lights]
+    maps = None
+    if upd.shadows == "map":
+        # the device's maps, checked against the oracle's own on a sample
+        S = upd.shadow_map_size
+        g_maps = upd.shadow_maps[: len(lights)].cpu().numpy().astype(np.float64)
+        dirs_map = ddgi.shadow_map_dirs(S).reshape(-1, 3).astype(np.float64)
+        rng = np.random.default_rng(frame)
+        for li, (lp, _) in enumerate(lights):
+            pick = rng.choice(len(dirs_map), size=min(2000, len(dirs_map)), replace=False)
+            t_map, _ = ddgi.raycast(sc.vertices, np.asarray(lp, np.float64)[None, :], dirs_map[pick])
+            g = g_maps[li].reshape(-1)[pick]
+            assert (np.isfinite(t_map) != np.isfinite(g)).mean() < 2e-3
+            fin = np.isfinite(t_map) & np.isfinite(g)
+            close = np.abs(g[fin] - t_map[fin]) <= 1e-4 * t_map[fin] + 1e-6
+            assert close.mean() > 0.995, close.mean()
+        maps = g_maps  # lookups are then compared on identical map values
     rgb_ref, dep_ref, mask_ref = ddgi.shade(sc.vertices, sc.albedo, sc.emission, lights, sc.sky, O,
                                             Dd, t_ref, prim_ref, upd.max_distance, upd.normal_bias,
-                                            upd.shadows)
+                                            upd.shadows, upd.shadow_map_size, upd.shadow_bias, maps)
     agree = same_hit.copy()
     agree[np.nonzero(both)[0][~prim_ok]] = False
     agree &= prim_g == np.where(hit_ref, prim_ref, -1)
@@ -109,13 +125,14 @@ def _check_atlas(upd):
         assert np.array_equal(vis, want_v)
 
 
-def test_cornell_box_config1(pkg):
+@pytest.mark.parametrize("shadows", ["map", "rays"])
+def test_cornell_box_config1(pkg, shadows):
     """Config 1: analytic Cornell box, 8x8x8 probes, 64 rays, three frames."""
     p, probes, scene = pkg
     sc = scene.cornell_box()
     vol = scene.volume_for(sc, (8, 8, 8))
     upd = probes.ProbeUpdater(vol, sc, rays_per_probe=64, hysteresis=0.9, record_rays=True,
-                              irradiance_scale=2.0)
+                              irradiance_scale=2.0, shadows=shadows, shadow_map_size=128)
     irr = np.zeros((512, 64, 3), np.float32)
     mom = np.zeros((512, 256, 2), np.float32)
     for f in range(3):
@@ -135,7 +152,7 @@ def test_cornell_box_config1(pkg):
     assert upd.irradiance.max().item() > 0.01
 
 
-@pytest.mark.parametrize("shadows", [True, False])
+@pytest.mark.parametrize("shadows", ["map", "rays", "none"])
 def test_interior_hall_sampled_probes(pkg, shadows):
     """Config 2 scene (~270k triangles), 256 rays; a sampled probe range is
     checked against the float64 brute-force oracle."""
