@@ -17,7 +17,6 @@ from __future__ import annotations
 import argparse
 import json
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -47,42 +46,57 @@ def dist_env():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons during the timed region."""
+    """SM clock + clock-event (throttle) reasons sampled through NVML every
+    ~5 ms while the timed region runs (falls back to nvidia-smi)."""
 
-    def __init__(self, index: int):
+    REASONS = {
+        "hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
+        "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
+        "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
+        "sw_power_cap": "nvmlClocksEventReasonSwPowerCap",
+        "hw_power_brake": "nvmlClocksEventReasonHwPowerBrakeSlowdown",
+    }
+
+    def __init__(self, index: int, period_s: float = 0.005):
         self.index = index
+        self.period = period_s
         self.samples = []
-        self._proc = None
+        self.max_mhz = None
+        self._stop = threading.Event()
         self._thread = None
+        self._nvml = None
 
     def __enter__(self):
-        cmd = ["nvidia-smi", f"--id={self.index}",
-               "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-               "--format=csv,noheader,nounits", "-lms", "100"]
         try:
-            self._proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
-                                          text=True)
-        except OSError:
-            self._proc = None
+            import pynvml
+
+            pynvml.nvmlInit()
+            visible = os.environ.get("CUDA_VISIBLE_DEVICES")
+            phys = int(visible.split(",")[self.index]) if visible else self.index
+            h = pynvml.nvmlDeviceGetHandleByIndex(phys)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self._nvml = (pynvml, h)
+        except Exception:
+            self._nvml = None
             return self
 
-        def reader():
-            for line in self._proc.stdout:
-                self.samples.append([x.strip() for x in line.split(",")])
+        def loop():
+            pynvml, h = self._nvml
+            while not self._stop.is_set():
+                try:
+                    mhz = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    reasons = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.samples.append((mhz, reasons))
+                except Exception:
+                    pass
+                time.sleep(self.period)
 
-        self._thread = threading.Thread(target=reader, daemon=True)
+        self._thread = threading.Thread(target=loop, daemon=True)
         self._thread.start()
         return self
 
     def __exit__(self, *exc):
-        if self._proc is not None:
-            self._proc.terminate()
-            try:
-                self._proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self._proc.kill()
+        self._stop.set()
         if self._thread is not None:
             self._thread.join(timeout=2)
 
@@ -90,18 +104,16 @@ class ClockSampler:
         import statistics
 
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["no NVML samples"]}
+        pynvml = self._nvml[0]
         reasons = set()
-        for s in self.samples:
-            for name, v in zip(names, s[3:7]):
-                if v.lower().startswith("active"):
+        for _, bits in self.samples:
+            for name, attr in self.REASONS.items():
+                if bits & getattr(pynvml, attr, 0):
                     reasons.add(name)
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.samples)}
+        return {"sm_mhz": statistics.median(m for m, _ in self.samples),
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(reasons),
+                "samples": len(self.samples), "source": "NVML"}
 
 
 def load_peaks():
@@ -329,6 +341,10 @@ def run_reference(args, rank, world, local):
 
 
 def main():
+    # keep rank 0's stdout to the single JSON line (NCCL prints its version
+    # banner to stdout at init when NCCL_DEBUG asks for it)
+    if os.environ.get("NCCL_DEBUG", "").upper() in ("VERSION", "INFO", "TRACE"):
+        os.environ["NCCL_DEBUG"] = "WARN"
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)

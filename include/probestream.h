@@ -112,6 +112,16 @@ int ps_detect_changed(int kind, const void *rendered, const void *last_sent,
                       uint32_t *changed_bits, int64_t *out_ids, int64_t *out_count,
                       void *workspace, size_t workspace_bytes, void *stream);
 
+/* Same, restricted to probes [probe_begin, probe_end) (a z-slab of a sharded
+ * volume): only those bits can be set; only the block rows covering the range
+ * are read. */
+int ps_detect_changed_range(int kind, const void *rendered, const void *last_sent,
+                            int64_t probe_count, int64_t probes_per_row, int64_t block_rows,
+                            int64_t probe_begin, int64_t probe_end, const uint8_t *active,
+                            double threshold, int threshold_is_f64, uint32_t *changed_bits,
+                            int64_t *out_ids, int64_t *out_count, void *workspace,
+                            size_t workspace_bytes, void *stream);
+
 /* Bitmap <-> id list helpers.  ids_to_bits ORs ids[0..n) (n read from
  * n_dev when non-NULL, else n_host) into bits (caller zeroes) and sets
  * PS_DEV_INDEX in *status_dev for ids outside [0, probe_count).
@@ -159,6 +169,25 @@ int ps_build_update(int kind, const void *source, int64_t probe_count,
                     const int64_t *entry_count, int64_t max_entries, int64_t slots_per_row,
                     void *update_texels, int64_t update_row_stride, void *last_sent,
                     int64_t *last_sent_seq, int64_t current_seq, void *stream);
+
+/* Slab-sharded build (multi-GPU, single encoder stream).  Every rank runs
+ * the same selection + slot assignment; a rank then
+ *   - copies the core of each entry whose probe lies in [probe_begin,
+ *     probe_end) into `payload` at index (probe - probe_begin) (core_side^2
+ *     texels per probe), commits the full block into last_sent (if non-NULL),
+ *   - stamps last_sent_seq[p] = current_seq for EVERY entry (replicated state).
+ * The encoder rank gathers the payloads of all ranks and imports them:
+ *   update_texels[slot] = payload_r[(probe - rank_begin[r])] with r the rank
+ *   whose [rank_begin[r], rank_begin[r+1]) holds the probe; payload_r sits at
+ *   payloads + r * payload_stride probes. */
+int ps_export_tiles(int kind, const void *source, int64_t probe_count, int64_t probes_per_row,
+                    const int64_t *entries, const int64_t *entry_count, int64_t max_entries,
+                    int64_t probe_begin, int64_t probe_end, void *payload, void *last_sent,
+                    int64_t *last_sent_seq, int64_t current_seq, void *stream);
+int ps_import_tiles(int kind, const void *payloads, int64_t payload_stride,
+                    const int64_t *rank_begin, int32_t world, const int64_t *entries,
+                    const int64_t *entry_count, int64_t max_entries, int64_t slots_per_row,
+                    void *update_texels, int64_t update_row_stride, void *stream);
 
 /* Guard-band reconstruct over a whole atlas (packing.py:180-196 applied to
  * every probe block): rewrites each block's border from its core. */

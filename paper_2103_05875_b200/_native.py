@@ -80,6 +80,8 @@ _SIGNATURES = {
     "ps_detect_workspace_bytes": (_sz, [_i64]),
     "ps_detect_changed": (_int, [_int, _vp, _vp, _i64, _i64, _i64, _vp, _f64, _int,
                                  _vp, _vp, _vp, _vp, _sz, _vp]),
+    "ps_detect_changed_range": (_int, [_int, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _f64,
+                                       _int, _vp, _vp, _vp, _vp, _sz, _vp]),
     "ps_ids_to_bits": (_int, [_vp, _vp, _i64, _i64, _vp, _vp, _vp]),
     "ps_compact_workspace_bytes": (_sz, [_i64]),
     "ps_bits_to_ids": (_int, [_vp, _i64, _vp, _vp, _vp, _sz, _vp]),
@@ -91,13 +93,15 @@ _SIGNATURES = {
     "ps_build_update": (_int, [_int, _vp, _i64, _i64, _vp, _vp, _i64, _i64, _vp, _i64, _vp,
                                _vp, _i64, _vp]),
     "ps_reconstruct_guard_bands": (_int, [_int, _vp, _i64, _i64, _vp]),
+    "ps_export_tiles": (_int, [_int, _vp, _i64, _i64, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp,
+                               _i64, _vp]),
+    "ps_import_tiles": (_int, [_int, _vp, _i64, _vp, _i32, _vp, _vp, _i64, _i64, _vp, _i64, _vp]),
     "ps_bvh_build": (_int, [_vp, _i64, _int, C.POINTER(BvhSizes), _vp, _vp]),
     "ps_blend_weights": (_int, [_vp, _i32, _vp, _f32, _vp, _vp, _vp, _vp]),
     "ps_trace_blend": (_int, [C.POINTER(TraceParams), _vp]),
 }
 
-# entry points of stages (1)+(2) still being brought up; remove once exported
-_PENDING = {"ps_bvh_build", "ps_blend_weights", "ps_trace_blend"}
+_PENDING: set = set()
 
 _lib = None
 _lock = threading.Lock()

@@ -31,6 +31,9 @@ struct DetectArgs {
     int side;                // block side (10 or 18)
     int64_t ppr;             // probes per row
     int64_t probe_count;
+    int64_t probe_begin;     // only probes in [probe_begin, probe_end) are tested
+    int64_t probe_end;
+    int64_t band0;           // first block row of the range
     const uint8_t *active;   // bool[probe_count] or nullptr (all active)
     uint32_t *bits;          // changed bitmap (zeroed by the launcher)
     int color_cut;           // COLOR_CUT: changed iff max channel delta >= cut
@@ -74,7 +77,7 @@ __device__ __forceinline__ uint2 ldg_stream(const uint2 *p) {
 template <int MODE, int SIDE>
 __global__ void __launch_bounds__(DET_THREADS) detect_kernel(DetectArgs a) {
     __shared__ uint32_t probe_hit[DET_PAIRS * 2 / SIDE + 2];
-    const int64_t band = blockIdx.y;
+    const int64_t band = a.band0 + blockIdx.y;
     const int64_t pair0 = int64_t(blockIdx.x) * DET_PAIRS;
     const int64_t col0 = pair0 * 2;               // first texel column of the CTA
     const int64_t bc0 = col0 / SIDE;              // first block column touched
@@ -105,7 +108,7 @@ __global__ void __launch_bounds__(DET_THREADS) detect_kernel(DetectArgs a) {
         const int64_t bc = bc0 + i;
         if (bc >= a.ppr) continue;
         const int64_t p = band * a.ppr + bc;
-        if (p >= a.probe_count || !probe_hit[i]) continue;
+        if (p < a.probe_begin || p >= a.probe_end || !probe_hit[i]) continue;
         if (a.active && !a.active[p]) continue;
         atomicOr(&a.bits[p >> 5], 1u << (p & 31));
     }
@@ -242,12 +245,15 @@ size_t ps_compact_workspace_bytes(int64_t probe_count) {
     return compact_workspace_bytes(std::max<int64_t>(probe_count, 1));
 }
 
-int ps_detect_changed(int kind, const void *rendered, const void *last_sent,
-                      int64_t probe_count, int64_t probes_per_row, int64_t block_rows,
-                      const uint8_t *active, double threshold, int threshold_is_f64,
-                      uint32_t *changed_bits, int64_t *out_ids, int64_t *out_count,
-                      void *workspace, size_t workspace_bytes, void *stream) {
+int ps_detect_changed_range(int kind, const void *rendered, const void *last_sent,
+                            int64_t probe_count, int64_t probes_per_row, int64_t block_rows,
+                            int64_t probe_begin, int64_t probe_end, const uint8_t *active,
+                            double threshold, int threshold_is_f64, uint32_t *changed_bits,
+                            int64_t *out_ids, int64_t *out_count, void *workspace,
+                            size_t workspace_bytes, void *stream) {
     PS_ABI_BEGIN
+    if (probe_begin < 0 || probe_end > probe_count || probe_begin > probe_end)
+        fail(PS_ERR_INDEX, "probe range outside the volume");
     if (kind != PS_KIND_COLOR && kind != PS_KIND_VISIBILITY) fail(PS_ERR_VALUE, "bad kind");
     if (probe_count < 1) fail(PS_ERR_VALUE, "probe_count must be >= 1");
     if (probes_per_row < 1 || block_rows != ceil_div(probe_count, probes_per_row))
@@ -264,6 +270,9 @@ int ps_detect_changed(int kind, const void *rendered, const void *last_sent,
     a.side = side;
     a.ppr = probes_per_row;
     a.probe_count = probe_count;
+    a.probe_begin = probe_begin;
+    a.probe_end = probe_end;
+    a.band0 = probe_begin / probes_per_row;
     a.active = active;
     a.bits = changed_bits;
     a.color_cut = 1;
@@ -284,8 +293,10 @@ int ps_detect_changed(int kind, const void *rendered, const void *last_sent,
         a.thr32 = float(threshold);  // round-to-nearest, as numpy's weak-scalar cast
         a.thr64 = threshold;
     }
-    dim3 grid(unsigned(ceil_div(a.pairs_per_row, DET_PAIRS)), unsigned(block_rows));
-    if (grid.y > 65535u) fail(PS_ERR_VALUE, "too many block rows");
+    const int64_t bands = probe_end > probe_begin ? (probe_end - 1) / probes_per_row - a.band0 + 1 : 0;
+    if (bands > 65535) fail(PS_ERR_VALUE, "too many block rows");
+    dim3 grid(unsigned(ceil_div(a.pairs_per_row, DET_PAIRS)), unsigned(bands));
+    if (bands > 0) {
 #define PS_DET(M, S) detect_kernel<M, S><<<grid, DET_THREADS, 0, s>>>(a)
     if (side == 10) {
         switch (mode) {
@@ -301,10 +312,22 @@ int ps_detect_changed(int kind, const void *rendered, const void *last_sent,
     }
 #undef PS_DET
     check_launch("detect_kernel");
+    }
     if (out_ids || out_count)
         compact_bits(changed_bits, probe_count, out_ids, nullptr, out_count, workspace,
                      workspace_bytes, s);
     PS_ABI_END
+}
+
+int ps_detect_changed(int kind, const void *rendered, const void *last_sent,
+                      int64_t probe_count, int64_t probes_per_row, int64_t block_rows,
+                      const uint8_t *active, double threshold, int threshold_is_f64,
+                      uint32_t *changed_bits, int64_t *out_ids, int64_t *out_count,
+                      void *workspace, size_t workspace_bytes, void *stream) {
+    return ps_detect_changed_range(kind, rendered, last_sent, probe_count, probes_per_row,
+                                   block_rows, 0, probe_count, active, threshold,
+                                   threshold_is_f64, changed_bits, out_ids, out_count, workspace,
+                                   workspace_bytes, stream);
 }
 
 int ps_ids_to_bits(const int64_t *ids, const int64_t *n_dev, int64_t n_host,

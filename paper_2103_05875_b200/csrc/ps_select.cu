@@ -223,6 +223,62 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+// slab-sharded build: export own probes' cores into a per-rank payload
+template <int SIDE>
+__global__ void __launch_bounds__(256)
+    export_kernel(const uint32_t *src, int64_t src_w, int64_t ppr, const int64_t *entries,
+                  const int64_t *entry_count, int64_t probe_begin, int64_t probe_end,
+                  uint32_t *payload, uint32_t *last_sent, int64_t *last_sent_seq,
+                  int64_t current_seq) {
+    constexpr int CORE = SIDE - 2;
+    constexpr int WORDS = SIDE * SIDE;
+    const int64_t count = *entry_count;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t e = warp; e < count; e += nwarps) {
+        const int64_t p = entries[2 * e + 1];
+        if (lane == 0 && last_sent_seq) last_sent_seq[p] = current_seq;  // replicated stamp
+        if (p < probe_begin || p >= probe_end) continue;
+        const int64_t y0 = (p / ppr) * SIDE, x0 = (p % ppr) * SIDE;
+        uint32_t *dst = payload + (p - probe_begin) * (CORE * CORE);
+#pragma unroll 4
+        for (int k = lane; k < WORDS; k += 32) {
+            const int r = k / SIDE, c = k % SIDE;
+            const uint32_t v = src[(y0 + r) * src_w + x0 + c];
+            if (r >= 1 && r <= CORE && c >= 1 && c <= CORE) dst[(r - 1) * CORE + c - 1] = v;
+            if (last_sent) last_sent[(y0 + r) * src_w + x0 + c] = v;
+        }
+    }
+}
+
+// encoder rank: gathered payloads -> slot regions of the update atlas
+template <int CORE>
+__global__ void __launch_bounds__(256)
+    import_kernel(const uint32_t *payloads, int64_t payload_stride, const int64_t *rank_begin,
+                  int world, const int64_t *entries, const int64_t *entry_count,
+                  int64_t slots_per_row, uint32_t *dst, int64_t dst_w) {
+    __shared__ int64_t s_begin[65];
+    for (int i = threadIdx.x; i <= world; i += blockDim.x) s_begin[i] = rank_begin[i];
+    __syncthreads();
+    const int64_t count = *entry_count;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t e = warp; e < count; e += nwarps) {
+        const int64_t slot = entries[2 * e], p = entries[2 * e + 1];
+        int r = 0;
+        while (r + 1 < world && p >= s_begin[r + 1]) ++r;
+        const uint32_t *srcp = payloads + (int64_t(r) * payload_stride + (p - s_begin[r])) * (CORE * CORE);
+        const int64_t sy = (slot / slots_per_row) * CORE, sx = (slot % slots_per_row) * CORE;
+#pragma unroll 4
+        for (int k = lane; k < CORE * CORE; k += 32) {
+            const int rr = k / CORE, cc = k % CORE;
+            dst[(sy + rr) * dst_w + sx + cc] = srcp[k];
+        }
+    }
+}
+
 // guard band of every probe block from its core (packing.py:180-196)
 template <int SIDE>
 __global__ void guard_kernel(uint32_t *atlas, int64_t w, int64_t ppr, int64_t probe_count) {
@@ -449,6 +505,59 @@ int ps_build_update(int kind, const void *source, int64_t probe_count, int64_t p
             slots_per_row, static_cast<uint32_t *>(update_texels), update_row_stride,
             static_cast<uint32_t *>(last_sent), last_sent_seq, current_seq);
     check_launch("build_kernel");
+    PS_ABI_END
+}
+
+int ps_export_tiles(int kind, const void *source, int64_t probe_count, int64_t probes_per_row,
+                    const int64_t *entries, const int64_t *entry_count, int64_t max_entries,
+                    int64_t probe_begin, int64_t probe_end, void *payload, void *last_sent,
+                    int64_t *last_sent_seq, int64_t current_seq, void *stream) {
+    PS_ABI_BEGIN
+    if (kind != PS_KIND_COLOR && kind != PS_KIND_VISIBILITY) fail(PS_ERR_VALUE, "bad kind");
+    if (probe_begin < 0 || probe_end > probe_count || probe_begin > probe_end)
+        fail(PS_ERR_INDEX, "probe range outside the volume");
+    if (max_entries <= 0) return PS_OK;
+    auto s = as_stream(stream);
+    const unsigned blocks = unsigned(std::max<int64_t>(
+        1, std::min<int64_t>(ceil_div(max_entries, 8), int64_t(sm_count()) * 16)));
+    if (kind == PS_KIND_COLOR)
+        export_kernel<10><<<blocks, 256, 0, s>>>(
+            static_cast<const uint32_t *>(source), probes_per_row * 10, probes_per_row, entries,
+            entry_count, probe_begin, probe_end, static_cast<uint32_t *>(payload),
+            static_cast<uint32_t *>(last_sent), last_sent_seq, current_seq);
+    else
+        export_kernel<18><<<blocks, 256, 0, s>>>(
+            static_cast<const uint32_t *>(source), probes_per_row * 18, probes_per_row, entries,
+            entry_count, probe_begin, probe_end, static_cast<uint32_t *>(payload),
+            static_cast<uint32_t *>(last_sent), last_sent_seq, current_seq);
+    check_launch("export_kernel");
+    PS_ABI_END
+}
+
+int ps_import_tiles(int kind, const void *payloads, int64_t payload_stride,
+                    const int64_t *rank_begin, int32_t world, const int64_t *entries,
+                    const int64_t *entry_count, int64_t max_entries, int64_t slots_per_row,
+                    void *update_texels, int64_t update_row_stride, void *stream) {
+    PS_ABI_BEGIN
+    if (kind != PS_KIND_COLOR && kind != PS_KIND_VISIBILITY) fail(PS_ERR_VALUE, "bad kind");
+    if (world < 1 || world > 64) fail(PS_ERR_VALUE, "world size in [1, 64]");
+    if (max_entries <= 0) return PS_OK;
+    auto s = as_stream(stream);
+    const unsigned blocks = unsigned(std::max<int64_t>(
+        1, std::min<int64_t>(ceil_div(max_entries, 8), int64_t(sm_count()) * 16)));
+    if (kind == PS_KIND_COLOR)
+        import_kernel<8><<<blocks, 256, 0, s>>>(static_cast<const uint32_t *>(payloads),
+                                                payload_stride, rank_begin, world, entries,
+                                                entry_count, slots_per_row,
+                                                static_cast<uint32_t *>(update_texels),
+                                                update_row_stride);
+    else
+        import_kernel<16><<<blocks, 256, 0, s>>>(static_cast<const uint32_t *>(payloads),
+                                                 payload_stride, rank_begin, world, entries,
+                                                 entry_count, slots_per_row,
+                                                 static_cast<uint32_t *>(update_texels),
+                                                 update_row_stride);
+    check_launch("import_kernel");
     PS_ABI_END
 }
 

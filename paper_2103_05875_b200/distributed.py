@@ -1,0 +1,231 @@
+"""Slab-sharded frame over N GPUs of one node (one process per GPU, NCCL).
+
+Per frame, every rank r (z-slab [b_r, e_r), scene replicated):
+
+1. traces + blends its own probes (ProbeUpdater with probe_range);
+2. per texture kind, change-detects its slab only
+   (``ps_detect_changed_range``);
+3. EXCHANGE 1 -- the change bitmap: slabs are disjoint so the per-rank
+   bitmaps have disjoint bits, and an int32 all-reduce(SUM) of the 16 KB
+   bitmap (C4) equals their OR.  Every rank then holds the global bitmap,
+   identical to single-GPU ``flatnonzero`` order because slabs are ascending
+   id ranges;
+4. runs the same selection and slot assignment (replicated, deterministic:
+   twin layouts replay identically, test_packing.py:235-240);
+5. exports the cores of its own selected probes into a payload indexed by
+   local probe id, commits its own blocks into last_sent and stamps
+   last_sent_seq for every entry (replicated state);
+6. EXCHANGE 2 -- the packed tiles: payloads are gathered (NCCL send/recv) to
+   the encoder rank, which imports them into the single update atlas and
+   runs pack + temporal delta (the north star's "single encoder stream").
+
+The encoder rank's outputs are bit-identical to the single-GPU pipeline's
+(tests/test_gpu_dist.py).
+"""
+
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+from . import _device as D
+from . import _native as N
+from .delta import pack_delta, skip_shape
+from .packing import UpdateAtlasLayout, widened_width
+from .probes import ProbeUpdater
+from .selection import detect_changed_device, select_device
+from .server import DEFAULT_GOP, KindOutput
+from .volume import AtlasKind, ProbeAtlas
+
+
+def slab_range(volume, rank: int, world: int):
+    """[begin, end) of rank's z-slab: whole k-planes, balanced."""
+    nx, ny, nz = volume.dims
+    plane = nx * ny
+    return (nz * rank) // world * plane, (nz * (rank + 1)) // world * plane
+
+
+def exchange_bitmap(bits: torch.Tensor, group=None) -> None:
+    """In place: OR of the ranks' disjoint change bitmaps (all-reduce SUM of
+    int32 words; disjoint bits never carry)."""
+    dist.all_reduce(bits, op=dist.ReduceOp.SUM, group=group)
+
+
+def gather_payloads(payload: torch.Tensor, payloads: torch.Tensor | None, rank: int,
+                    world: int, encoder: int = 0, group=None) -> None:
+    """Send every rank's payload to the encoder rank's ``payloads[r]``.
+
+    The encoder's own payload is expected to already live in
+    ``payloads[encoder]`` (it exports in place)."""
+    ops = []
+    if rank == encoder:
+        for r in range(world):
+            if r != encoder:
+                ops.append(dist.P2POp(dist.irecv, payloads[r], r, group))
+    else:
+        ops.append(dist.P2POp(dist.isend, payload, encoder, group))
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+
+
+class DistKindStream:
+    def __init__(self, kind: AtlasKind, volume, device, rank, world, ranges, encoder=0,
+                 slot_count=None, threshold=0.0, gop_length=DEFAULT_GOP, budget=None,
+                 probes_per_row=None):
+        self.kind, self.volume, self.device = kind, volume, device
+        self.rank, self.world, self.encoder = rank, world, encoder
+        self.ranges = ranges
+        self.begin, self.end = ranges[rank]
+        n = volume.probe_count
+        self.threshold, self.budget, self.gop_length = threshold, budget, gop_length
+        self.frame_count = 0
+        self.last_sent = ProbeAtlas(kind, n, probes_per_row, device=device)
+        self.last_sent_seq = torch.full((n,), -1, dtype=torch.int64, device=device)
+        self.layout = UpdateAtlasLayout(slot_count or n, kind.core_side, probe_count=n,
+                                        device=device)
+        self.bits = torch.empty((n + 31) // 32, dtype=torch.int32, device=device)
+        self.sel_ids = torch.empty(n, dtype=torch.int64, device=device)
+        self.sel_count = torch.empty(1, dtype=torch.int64, device=device)
+        core = kind.core_side ** 2
+        self.slab_max = max(e - b for b, e in ranges)
+        self.is_encoder = rank == encoder
+        if self.is_encoder:
+            self.payloads = torch.zeros((world, self.slab_max * core), dtype=torch.int32,
+                                        device=device)
+            self.payload = self.payloads[rank]
+            self.rank_begin = torch.tensor([b for b, _ in ranges] + [ranges[-1][1]],
+                                           dtype=torch.int64, device=device)
+            shape = self.layout.texel_shape(kind)
+            tdt = torch.uint32 if kind is AtlasKind.COLOR else torch.uint16
+            self.update_texels = torch.zeros(shape, dtype=tdt, device=device)
+            h, w = shape[0], shape[1]
+            pw, pdt = (w, torch.uint16) if kind is AtlasKind.COLOR else (widened_width(w), torch.uint8)
+            self.planes = [torch.zeros((3, h, pw), dtype=pdt, device=device) for _ in range(2)]
+            self.residual = torch.zeros((3, h, pw), dtype=pdt, device=device)
+            self.skip = torch.zeros(skip_shape(h, pw), dtype=torch.uint8, device=device)
+            self._cur = 0
+        else:
+            self.payloads = None
+            self.payload = torch.zeros(self.slab_max * core, dtype=torch.int32, device=device)
+        self.timers = None
+
+    def _mark(self, name, stage):
+        if self.timers is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            self.timers.setdefault(name, []).append((stage, e))
+
+    def tick(self, rendered: ProbeAtlas, seq: int, pvs_bits=None):
+        tag = self.kind.value
+        dev = self.device
+        self._mark(f"{tag}.detect", 0)
+        detect_changed_device(rendered, self.last_sent, self.volume, self.threshold,
+                              bits=self.bits, with_ids=False, workspace_slot=f"detect.{tag}",
+                              probe_range=(self.begin, self.end))
+        self._mark(f"{tag}.detect", 1)
+        self._mark(f"{tag}.exchange_bits", 0)
+        exchange_bitmap(self.bits)
+        self._mark(f"{tag}.exchange_bits", 1)
+        self._mark(f"{tag}.select", 0)
+        select_device(self.bits, pvs_bits, self.volume, self.last_sent_seq, seq, self.budget,
+                      out_ids=self.sel_ids, out_count=self.sel_count,
+                      workspace_slot=f"select.{tag}")
+        self._mark(f"{tag}.select", 1)
+        self._mark(f"{tag}.assign", 0)
+        entries, count = self.layout.assign_device(self.sel_ids, self.sel_count)
+        self._mark(f"{tag}.assign", 1)
+        self._mark(f"{tag}.export", 0)
+        N.call("ps_export_tiles", self.kind.native, rendered.texels.data_ptr(),
+               self.volume.probe_count, rendered.probes_per_row, entries.data_ptr(),
+               count.data_ptr(), self.layout.slot_count, self.begin, self.end,
+               self.payload.data_ptr(), self.last_sent.texels.data_ptr(),
+               self.last_sent_seq.data_ptr(), int(seq), D.stream_ptr(dev))
+        self._mark(f"{tag}.export", 1)
+        self._mark(f"{tag}.gather", 0)
+        gather_payloads(self.payload, self.payloads, self.rank, self.world, self.encoder)
+        self._mark(f"{tag}.gather", 1)
+        key = self.frame_count % self.gop_length == 0
+        self.frame_count += 1
+        if not self.is_encoder:
+            return None
+        self._mark(f"{tag}.import", 0)
+        N.call("ps_import_tiles", self.kind.native, self.payloads.data_ptr(), self.slab_max,
+               self.rank_begin.data_ptr(), self.world, entries.data_ptr(), count.data_ptr(),
+               self.layout.slot_count, self.layout.slots_per_row, self.update_texels.data_ptr(),
+               self.update_texels.shape[1], D.stream_ptr(dev))
+        self._mark(f"{tag}.import", 1)
+        prev = None if key else self.planes[self._cur]
+        cur = self.planes[1 - self._cur]
+        self._mark(f"{tag}.pack_delta", 0)
+        pack_delta(self.update_texels, self.kind, prev, planes_out=cur, residual=self.residual,
+                   skip=self.skip)
+        self._mark(f"{tag}.pack_delta", 1)
+        self._cur = 1 - self._cur
+        return KindOutput(cur, self.residual, self.skip, entries, count, key)
+
+
+class DistributedFrame:
+    """One client session's hot path sharded over the process group."""
+
+    def __init__(self, volume, scene, rays_per_probe, device, rank, world, encoder=0,
+                 color_threshold=0.0, visibility_threshold=0.0, slot_count=None, budget=None,
+                 gop_length=DEFAULT_GOP, **probe_kwargs):
+        self.volume, self.device, self.rank, self.world = volume, device, rank, world
+        self.ranges = [slab_range(volume, r, world) for r in range(world)]
+        self.updater = ProbeUpdater(volume, scene, rays_per_probe=rays_per_probe, device=device,
+                                    probe_range=self.ranges[rank], **probe_kwargs)
+        ppr = self.updater.color.probes_per_row
+        kw = dict(encoder=encoder, slot_count=slot_count, gop_length=gop_length, budget=budget,
+                  probes_per_row=ppr)
+        self.color = DistKindStream(AtlasKind.COLOR, volume, device, rank, world, self.ranges,
+                                    threshold=color_threshold, **kw)
+        self.visibility = DistKindStream(AtlasKind.VISIBILITY, volume, device, rank, world,
+                                         self.ranges, threshold=visibility_threshold, **kw)
+        self.seq = 0
+        self.timers = None
+
+    def enable_stage_timers(self, on=True):
+        self.timers = {} if on else None
+        self.color.timers = self.timers
+        self.visibility.timers = self.timers
+
+    def tick(self, frame=None, lights=None, pvs_bits=None):
+        frame = self.seq if frame is None else frame
+        if self.timers is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            self.timers.setdefault("trace_blend", []).append((0, e))
+        color, vis = self.updater.update(frame, lights)
+        if self.timers is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            self.timers["trace_blend"].append((1, e))
+        out_c = self.color.tick(color, self.seq, pvs_bits)
+        out_v = self.visibility.tick(vis, self.seq, pvs_bits)
+        self.seq += 1
+        return out_c, out_v
+
+    def h2d_bytes_per_frame(self) -> int:
+        u = self.updater
+        return u.rays_per_probe * 16 + u.dscene.light_count * 24
+
+    def pack_delta_bytes(self) -> dict:
+        out = {}
+        for ks in (self.color, self.visibility):
+            if not ks.is_encoder:
+                continue
+            tex = ks.update_texels.numel() * ks.update_texels.element_size()
+            pl = ks.planes[0].numel() * ks.planes[0].element_size()
+            out[ks.kind.value] = tex + 3 * pl + ks.skip.numel()
+        out["total"] = sum(out.values())
+        return out
+
+    def stage_times_ms(self) -> dict:
+        out = {}
+        for name, evs in (self.timers or {}).items():
+            starts = [e for s, e in evs if s == 0]
+            ends = [e for s, e in evs if s == 1]
+            if starts and ends:
+                out[name] = sum(a.elapsed_time(b) for a, b in zip(starts, ends)) / len(ends)
+        return out

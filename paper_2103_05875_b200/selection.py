@@ -55,9 +55,11 @@ def _check_layout(rendered, last_sent, volume):
 
 
 def detect_changed_device(rendered, last_sent, volume, threshold=0.0, *, bits=None,
-                          ids=None, count=None, with_ids=True, workspace_slot="detect"):
+                          ids=None, count=None, with_ids=True, workspace_slot="detect",
+                          probe_range=None):
     """Stream-ordered detection.  Returns (changed_bits uint32[(N+31)/32],
-    ids int64[N] (first ``count`` valid) or None, count int64[1] or None)."""
+    ids int64[N] (first ``count`` valid) or None, count int64[1] or None).
+    ``probe_range`` restricts the test to a z-slab [begin, end)."""
     _check_layout(rendered, last_sent, volume)
     dev = D.device_of(rendered.texels, last_sent.texels)
     a, _ = _atlas_tensor(rendered, dev)
@@ -79,8 +81,9 @@ def detect_changed_device(rendered, last_sent, volume, threshold=0.0, *, bits=No
     ws = D.Workspace.get(N.lib().ps_detect_workspace_bytes(n), dev, workspace_slot)
     thr, is64 = _threshold_args(threshold)
     active = volume.active_device(dev)
-    N.call("ps_detect_changed", kind_of(rendered.kind).native, a.data_ptr(), b.data_ptr(), n,
-           ppr, block_rows, active.data_ptr(), thr, is64, bits.data_ptr(),
+    begin, end = probe_range if probe_range is not None else (0, n)
+    N.call("ps_detect_changed_range", kind_of(rendered.kind).native, a.data_ptr(), b.data_ptr(),
+           n, ppr, block_rows, begin, end, active.data_ptr(), thr, is64, bits.data_ptr(),
            D.ptr(ids) if with_ids else None, D.ptr(count) if with_ids else None,
            ws.data_ptr(), ws.numel(), D.stream_ptr(dev))
     return bits, (ids if with_ids else None), (count if with_ids else None)

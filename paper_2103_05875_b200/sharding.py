@@ -15,17 +15,8 @@ from __future__ import annotations
 import torch
 
 from . import _device as D
+from .distributed import slab_range  # noqa: F401  (re-exported)
 from .server import ProbeStreamServer
-
-
-def slab_range(volume, rank: int, world: int, align: int = 32):
-    """[begin, end) of rank's z-slab, boundaries on whole k-planes and on
-    multiples of `align` probes where the plane size allows."""
-    nx, ny, nz = volume.dims
-    plane = nx * ny
-    k0 = (nz * rank) // world
-    k1 = (nz * (rank + 1)) // world
-    return k0 * plane, k1 * plane
 
 
 class SlabServer:
@@ -106,15 +97,21 @@ class SlabServer:
         with profile(activities=[ProfilerActivity.CUDA]) as prof:
             impl.tick(frame, lights_for(frame))
             torch.cuda.synchronize(self.device)
+        import re
+
         names = {}
         total = 0
         for ev in prof.events():
-            if ev.device_type == torch.autograd.DeviceType.CUDA and not ev.name.startswith("Memcpy") \
-                    and not ev.name.startswith("Memset") and "memcpy" not in ev.name.lower() \
-                    and "memset" not in ev.name.lower():
+            if ev.device_type != torch.autograd.DeviceType.CUDA:
+                continue
+            low = ev.name.lower()
+            if "memcpy" in low or "memset" in low:
+                continue
+            key = ev.name.replace("(anonymous namespace)::", "").replace("void ", "")
+            key = re.sub(r"<.*", "", key.split("(")[0])
+            names[key] = names.get(key, 0) + 1
+            if not key.startswith("nccl"):  # NCCL's own kernels are listed, not counted
                 total += 1
-                key = ev.name.split("(")[0].split("<")[0].replace("void ", "")
-                names[key] = names.get(key, 0) + 1
         return total, names
 
     def pack_delta_bytes(self) -> dict:
