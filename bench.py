@@ -124,14 +124,18 @@ def load_peaks():
     return 6650.0, "fallback"
 
 
-def profile_traffic(kernel: str):
-    """dram bytes per launch of `kernel` from a committed ncu summary, if any."""
+def profile_traffic(prefix: str):
+    """DRAM bytes (read + write) per launch, summed over the kernels whose name
+    starts with `prefix` (one launch per texture kind), from the committed
+    ncu summary (profiles/ncu_summary.json); None if absent."""
     p = ROOT / "profiles" / "ncu_summary.json"
     if not p.exists():
         return None
     try:
-        d = json.loads(p.read_text())
-        return d.get("kernels", {}).get(kernel, {}).get("dram_bytes_per_launch")
+        d = json.loads(p.read_text()).get("kernels", {})
+        vals = [v["dram_bytes_per_launch"] for k, v in d.items()
+                if k.startswith(prefix) and "dram_bytes_per_launch" in v]
+        return round(sum(vals)) if vals else None
     except Exception:
         return None
 

@@ -10,9 +10,9 @@
 //                      [c1.lo.x c1.hi.x c1.lo.y c1.hi.y]
 //                      [c0.lo.z c0.hi.z c1.lo.z c1.hi.z]
 //                      [child0  child1  0       0      ]  (int bits)
-//           child >= 0: inner node index; child < 0: leaf at tri record ~child
-//   tri   = 12 floats: [v0.xyz prim] [e1.xyz 0] [e2.xyz 0]; a record whose
-//           prim word is -1 terminates a leaf.
+//           child >= 0: inner node index; child < 0: leaf with
+//           ~child = first_triangle_record << 3 | count (count <= 7)
+//   tri   = 12 floats: [v0.xyz prim] [e1.xyz 0] [e2.xyz 0], leaves contiguous
 // Edges are formed in double (v1 - v0, v2 - v0) and rounded once to float,
 // the same construction the Moller-Trumbore test of the reference uses
 // (selection.py:124-126).
@@ -162,7 +162,7 @@ extern "C" int ps_bvh_build(const double *vertices, int64_t tri_count, int leaf_
         if (!sizes) throw std::invalid_argument("sizes must not be NULL");
         if (tri_count < 1) throw std::invalid_argument("scene needs at least one triangle");
         if (tri_count > (int64_t(1) << 30)) throw std::invalid_argument("too many triangles");
-        if (leaf_size < 1 || leaf_size > 16) throw std::invalid_argument("leaf_size in [1, 16]");
+        if (leaf_size < 1 || leaf_size > 7) throw std::invalid_argument("leaf_size in [1, 7]");
         Builder b;
         b.v = vertices;
         b.leaf_size = leaf_size;
@@ -197,7 +197,7 @@ extern "C" int ps_bvh_build(const double *vertices, int64_t tri_count, int leaf_
         }
         const bool single_leaf = inner.empty();
         const int64_t node_count = single_leaf ? 1 : int64_t(inner.size());
-        // leaves in DFS order, each followed by a terminator record
+        // leaves in DFS order, triangles contiguous per leaf
         std::vector<int> leaves;
         std::vector<int> leaf_slot(b.nodes.size(), -1);
         int64_t slots = 0;
@@ -209,7 +209,7 @@ extern "C" int ps_bvh_build(const double *vertices, int64_t tri_count, int leaf_
                 if (b.nodes[id].left < 0) {
                     leaf_slot[id] = int(slots);
                     leaves.push_back(id);
-                    slots += b.nodes[id].count + 1;
+                    slots += b.nodes[id].count;
                 } else {
                     st.push_back(b.nodes[id].right);
                     st.push_back(b.nodes[id].left);
@@ -218,13 +218,13 @@ extern "C" int ps_bvh_build(const double *vertices, int64_t tri_count, int leaf_
         }
         sizes->node_count = node_count;
         sizes->tri_count = tri_count;
-        sizes->tri_slots = slots + (single_leaf ? 1 : 0);
+        sizes->tri_slots = slots;
         sizes->max_depth = std::max<int64_t>(max_depth, 1);
         if (!nodes_out || !tris_out) return PS_OK;
 
         auto child_ref = [&](int id) -> int32_t {
             if (b.nodes[id].left >= 0) return gpu_index[id];
-            return ~int32_t(leaf_slot[id]);
+            return ~int32_t((leaf_slot[id] << 3) | b.nodes[id].count);
         };
         auto put_box = [](float *nd, int which, const Aabb &bx) {
             // round outward so the float box contains the double box
@@ -245,8 +245,8 @@ extern "C" int ps_bvh_build(const double *vertices, int64_t tri_count, int leaf_
             Aabb empty;  // inverted box never hits
             nd[4] = 1.f; nd[5] = -1.f; nd[6] = 1.f; nd[7] = -1.f; nd[10] = 1.f; nd[11] = -1.f;
             (void)empty;
-            set_int(nd + 12, ~int32_t(0));
-            set_int(nd + 13, ~int32_t(slots));  // points at a lone terminator
+            set_int(nd + 12, ~int32_t(b.nodes[0].count));  // leaf at record 0
+            set_int(nd + 13, ~int32_t(0));                 // empty leaf
         } else {
             for (size_t g = 0; g < inner.size(); ++g) {
                 const BuildNode &bn = b.nodes[inner[g]];
@@ -273,15 +273,6 @@ extern "C" int ps_bvh_build(const double *vertices, int64_t tri_count, int leaf_
                 r[11] = 0.f;
                 ++s;
             }
-            float *term = tris_out + 12 * s;
-            std::memset(term, 0, 48);
-            set_int(term + 3, -1);
-            ++s;
-        }
-        if (single_leaf) {
-            float *term = tris_out + 12 * s;
-            std::memset(term, 0, 48);
-            set_int(term + 3, -1);
         }
         return PS_OK;
     } catch (const std::exception &e) {

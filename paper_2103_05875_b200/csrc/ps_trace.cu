@@ -29,6 +29,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 
 #include "ps_common.cuh"
 
@@ -101,8 +102,11 @@ __device__ __forceinline__ void node_hits(const float4 *nodes, int node, float i
 }
 
 // Nearest hit (ANY_HIT = false) or occlusion test (ANY_HIT = true) with a
-// per-thread stack.  Returns the hit record slot (or -1) and the distance.
-template <bool ANY_HIT>
+// per-thread stack of (node, entry distance) pairs: popped entries farther
+// than the current hit are skipped.  Leaves carry their triangle count
+// (~ref = first << 3 | count), so all of a leaf's triangle records are
+// fetched before the first test.  Returns the hit record index (or -1).
+template <bool ANY_HIT, int LEAFV = 0>
 __device__ int traverse(const float4 *__restrict__ nodes, const float4 *__restrict__ tris,
                         const Ray &r, float tmax, float &t_best) {
     // reciprocal direction; tiny components replaced so the slabs stay finite
@@ -111,7 +115,7 @@ __device__ int traverse(const float4 *__restrict__ nodes, const float4 *__restri
     const float sz = fabsf(r.dz) < 1e-12f ? copysignf(1e-12f, r.dz) : r.dz;
     const float ix = 1.0f / sx, iy = 1.0f / sy, iz = 1.0f / sz;
     const float oix = r.ox * ix, oiy = r.oy * iy, oiz = r.oz * iz;
-    int stack[STACK];
+    int2 stack[STACK];
     int sp = 0;
     int node = 0;
     int hit_slot = -1;
@@ -125,7 +129,7 @@ __device__ int traverse(const float4 *__restrict__ nodes, const float4 *__restri
             if (h0 && h1) {
                 const bool swap = t1 < t0;
                 node = swap ? c1 : c0;
-                stack[sp++] = swap ? c0 : c1;
+                stack[sp++] = make_int2(swap ? c0 : c1, __float_as_int(swap ? t0 : t1));
                 continue;
             }
             if (h0 || h1) {
@@ -133,20 +137,89 @@ __device__ int traverse(const float4 *__restrict__ nodes, const float4 *__restri
                 continue;
             }
         } else {
-            for (int s = ~node;; ++s) {
-                const float4 v0 = __ldg(tris + 3 * s);
-                const int prim = __float_as_int(v0.w);
-                if (prim < 0) break;
-                const float t = tri_hit(r, v0, __ldg(tris + 3 * s + 1), __ldg(tris + 3 * s + 2));
-                if (t < t_best) {
-                    t_best = t;
-                    hit_slot = s;
-                    if (ANY_HIT) return hit_slot;
+            const int ref = ~node;
+            const int first = ref >> 3, cnt = ref & 7;
+            if (LEAFV == 2) {  // fetch up to 4 triangles before testing
+                float4 v0[4], e1[4], e2[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (k < cnt) {
+                        v0[k] = __ldg(tris + 3 * (first + k));
+                        e1[k] = __ldg(tris + 3 * (first + k) + 1);
+                        e2[k] = __ldg(tris + 3 * (first + k) + 2);
+                    }
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (k < cnt) {
+                        const float t = tri_hit(r, v0[k], e1[k], e2[k]);
+                        if (t < t_best) {
+                            t_best = t;
+                            hit_slot = first + k;
+                            if (ANY_HIT) return hit_slot;
+                        }
+                    }
+            } else if (LEAFV == 1) {  // two triangles in flight
+                for (int k = 0; k < cnt; k += 2) {
+                    const float4 a0 = __ldg(tris + 3 * (first + k));
+                    const float4 a1 = __ldg(tris + 3 * (first + k) + 1);
+                    const float4 a2 = __ldg(tris + 3 * (first + k) + 2);
+                    float4 b0, b1, b2;
+                    const bool two = k + 1 < cnt;
+                    if (two) {
+                        b0 = __ldg(tris + 3 * (first + k + 1));
+                        b1 = __ldg(tris + 3 * (first + k + 1) + 1);
+                        b2 = __ldg(tris + 3 * (first + k + 1) + 2);
+                    }
+                    float t = tri_hit(r, a0, a1, a2);
+                    if (t < t_best) {
+                        t_best = t;
+                        hit_slot = first + k;
+                        if (ANY_HIT) return hit_slot;
+                    }
+                    if (two) {
+                        t = tri_hit(r, b0, b1, b2);
+                        if (t < t_best) {
+                            t_best = t;
+                            hit_slot = first + k + 1;
+                            if (ANY_HIT) return hit_slot;
+                        }
+                    }
+                }
+            } else {
+                for (int k = 0; k < cnt; ++k) {
+                    const float t = tri_hit(r, __ldg(tris + 3 * (first + k)),
+                                            __ldg(tris + 3 * (first + k) + 1),
+                                            __ldg(tris + 3 * (first + k) + 2));
+                    if (t < t_best) {
+                        t_best = t;
+                        hit_slot = first + k;
+                        if (ANY_HIT) return hit_slot;
+                    }
                 }
             }
+            if (LEAFV == 2)
+                for (int k = 4; k < cnt; ++k) {  // leaves larger than 4 (leaf_size > 4)
+                    const float t = tri_hit(r, __ldg(tris + 3 * (first + k)),
+                                            __ldg(tris + 3 * (first + k) + 1),
+                                            __ldg(tris + 3 * (first + k) + 2));
+                    if (t < t_best) {
+                        t_best = t;
+                        hit_slot = first + k;
+                        if (ANY_HIT) return hit_slot;
+                    }
+                }
         }
-        if (sp == 0) break;
-        node = stack[--sp];
+        // pop the nearest pending subtree that can still hold a closer hit
+        bool found = false;
+        while (sp > 0) {
+            const int2 e = stack[--sp];
+            if (__int_as_float(e.y) <= t_best) {
+                node = e.x;
+                found = true;
+                break;
+            }
+        }
+        if (!found) break;
     }
     return hit_slot;
 }
@@ -179,11 +252,22 @@ __device__ __forceinline__ int cube_texel(float vx, float vy, float vz, int S) {
 }
 
 template <int SHADOW>
+__device__ Shade shade_hit(const ps_trace_params &p, const float4 *nodes, const float4 *tris,
+                           const Ray &ray, int slot, float t);
+
+template <int SHADOW, int LEAFV>
 __device__ Shade shade_ray(const ps_trace_params &p, const float4 *nodes, const float4 *tris,
                            const Ray &ray) {
-    Shade s;
     float t;
-    const int slot = traverse<false>(nodes, tris, ray, INFINITY, t);
+    const int slot = traverse<false, LEAFV>(nodes, tris, ray, INFINITY, t);
+    return shade_hit<SHADOW>(p, nodes, tris, ray, slot, t);
+}
+
+// radiance + depth of a ray given its nearest hit (slot < 0: miss)
+template <int SHADOW>
+__device__ Shade shade_hit(const ps_trace_params &p, const float4 *nodes, const float4 *tris,
+                           const Ray &ray, int slot, float t) {
+    Shade s;
     s.shadow_mask = 0;
     if (slot < 0) {
         s.r = p.sky[0];
@@ -300,8 +384,8 @@ __global__ void __launch_bounds__(256) shadow_map_kernel(ps_trace_params prm) {
 // the coherence-ordered set) from a global counter, traces + shades them and
 // writes {rgb, depth}.  Dynamic claiming keeps every SM busy regardless of the
 // large per-direction cost differences.
-template <int SHADOW>
-__global__ void __launch_bounds__(THREADS) trace_kernel(ps_trace_params prm) {
+template <int SHADOW, int LEAFV, int MINB, int PROBE_PARALLEL = 0>
+__global__ void __launch_bounds__(THREADS, MINB) trace_kernel(ps_trace_params prm) {
     const float4 *nodes = reinterpret_cast<const float4 *>(prm.nodes);
     const float4 *tris = reinterpret_cast<const float4 *>(prm.tris);
     const float4 *dirs = reinterpret_cast<const float4 *>(prm.ray_dirs);
@@ -309,7 +393,11 @@ __global__ void __launch_bounds__(THREADS) trace_kernel(ps_trace_params prm) {
     const int64_t nloc = int64_t(prm.probe_end) - prm.probe_begin;
     const int64_t total_rays = nloc * R;
     const int64_t chunks_per_probe = (R + 31) / 32;
-    const int64_t total_chunks = nloc * chunks_per_probe;
+    // PROBE_PARALLEL: a chunk is one direction for 32 consecutive probes
+    // (parallel rays from neighbouring origins) instead of 32 directions of
+    // one probe
+    const int64_t probe_groups = (nloc + 31) / 32;
+    const int64_t total_chunks = PROBE_PARALLEL ? probe_groups * R : nloc * chunks_per_probe;
     const int lane = threadIdx.x & 31;
     float4 *records = reinterpret_cast<float4 *>(prm.records);
     while (true) {
@@ -317,9 +405,18 @@ __global__ void __launch_bounds__(THREADS) trace_kernel(ps_trace_params prm) {
         if (lane == 0) task = atomicAdd(prm.work_counter, 1u);
         task = __shfl_sync(0xffffffffu, task, 0);
         if (int64_t(task) >= total_chunks) break;
-        const int64_t q = int64_t(task) / chunks_per_probe;
-        const int r = int(int64_t(task) - q * chunks_per_probe) * 32 + lane;
-        if (r >= R) continue;
+        int64_t q;
+        int r;
+        if (PROBE_PARALLEL) {
+            const int64_t g = int64_t(task) / R;
+            r = int(int64_t(task) - g * R);
+            q = g * 32 + lane;
+            if (q >= nloc) continue;
+        } else {
+            q = int64_t(task) / chunks_per_probe;
+            r = int(int64_t(task) - q * chunks_per_probe) * 32 + lane;
+            if (r >= R) continue;
+        }
         const int64_t p = prm.probe_begin + q;
         const int64_t i = p % prm.nx, j = (p / prm.nx) % prm.ny, k = p / (int64_t(prm.nx) * prm.ny);
         Ray ray;
@@ -332,7 +429,7 @@ __global__ void __launch_bounds__(THREADS) trace_kernel(ps_trace_params prm) {
         ray.dx = d.x;
         ray.dy = d.y;
         ray.dz = d.z;
-        const Shade s = shade_ray<SHADOW>(prm, nodes, tris, ray);
+        const Shade s = shade_ray<SHADOW, LEAFV>(prm, nodes, tris, ray);
         const int64_t ray_id = q * R + r;
         records[ray_id] = make_float4(s.r, s.g, s.b, s.depth);
         if (prm.ray_records) {
@@ -344,109 +441,311 @@ __global__ void __launch_bounds__(THREADS) trace_kernel(ps_trace_params prm) {
     }
 }
 
-// ---- pass 2: DDGI blend of P probes per CTA ---------------------------------------------
-template <int P>
-__global__ void __launch_bounds__(THREADS) blend_kernel(ps_trace_params prm) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int R = prm.rays_per_probe;
-    float4 *s_rgb = reinterpret_cast<float4 *>(smem_raw);            // R * P   [r][q]
-    float2 *s_dep = reinterpret_cast<float2 *>(s_rgb + R * P);       // R * P   [r][q] (d, d^2)
-    uint32_t *s_ccore = reinterpret_cast<uint32_t *>(s_dep + R * P); // P * 64
-    uint32_t *s_vcore = s_ccore + P * 64;                            // P * 256
+// ---- pass 1 (alternative): persistent while-while traversal with per-lane refill -------
+// Aila & Laine style: every lane owns one ray; a lane that finds a leaf
+// postpones it and keeps walking inner nodes until all active lanes hold a
+// leaf (speculative traversal), then the warp tests leaves together.  When
+// fewer than DYN_FETCH lanes are still busy the warp shades the finished rays
+// and refills those lanes from the global ray counter (warp-aggregated
+// atomic), so SIMT lanes stay occupied despite the very uneven ray costs.
+constexpr int WW_SENTINEL = 0x7fffffff;
+constexpr int DYN_FETCH = 20;
 
-    const int tid = threadIdx.x;
-    const int64_t p0 = int64_t(prm.probe_begin) + int64_t(blockIdx.x) * P;
-    const int64_t left = int64_t(prm.probe_end) - p0;
-    const int nq = int(left < P ? left : P);
-    const float4 *records = reinterpret_cast<const float4 *>(prm.records) +
-                            (p0 - prm.probe_begin) * R;
-    for (int g = tid; g < P * R; g += THREADS) {
-        const int q = g / R, r = g - q * R;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (q < nq) v = __ldcs(records + g);  // streamed once
-        s_rgb[r * P + q] = make_float4(v.x, v.y, v.z, 0.f);
-        s_dep[r * P + q] = make_float2(v.w, v.w * v.w);
+__device__ __forceinline__ int ww_pop(const int2 *stack, int &sp, float tb) {
+    while (sp > 0) {
+        const int2 e = stack[--sp];
+        if (__int_as_float(e.y) <= tb) return e.x;
     }
-    __syncthreads();
+    return WW_SENTINEL;
+}
 
-    // ---- irradiance (64 texels x P probes) --------------------------------------------
-    {
-        constexpr int QPT = (P + 3) / 4;  // probes per thread
-        const int t = tid & 63, qg = tid >> 6;
-        float acc[QPT][3];
-#pragma unroll
-        for (int a = 0; a < QPT; ++a) acc[a][0] = acc[a][1] = acc[a][2] = 0.f;
-        const float *wc = prm.w_color + t;
-        for (int r = 0; r < R; ++r) {
-            const float w = __ldg(wc + r * 64);
-#pragma unroll
-            for (int a = 0; a < QPT; ++a) {
-                const int q = qg + 4 * a;
-                if (q < P) {
-                    const float4 L = s_rgb[r * P + q];
-                    acc[a][0] = fmaf(w, L.x, acc[a][0]);
-                    acc[a][1] = fmaf(w, L.y, acc[a][1]);
-                    acc[a][2] = fmaf(w, L.z, acc[a][2]);
+template <int SHADOW, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) trace_ww_kernel(ps_trace_params prm) {
+    const float4 *nodes = reinterpret_cast<const float4 *>(prm.nodes);
+    const float4 *tris = reinterpret_cast<const float4 *>(prm.tris);
+    const float4 *dirs = reinterpret_cast<const float4 *>(prm.ray_dirs);
+    const int R = prm.rays_per_probe;
+    const int64_t nloc = int64_t(prm.probe_end) - prm.probe_begin;
+    const uint32_t total = uint32_t(nloc * R);
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    float4 *records = reinterpret_cast<float4 *>(prm.records);
+
+    uint32_t ray_id = 0;
+    bool has_ray = false;
+    bool queue_done = false;
+    Ray ray{0.f, 0.f, 0.f, 0.f, 0.f, 1.f};
+    float ix = 0.f, iy = 0.f, iz = 0.f, oix = 0.f, oiy = 0.f, oiz = 0.f, tb = 0.f;
+    int hit = -1;
+    int node = WW_SENTINEL, leaf = 0, sp = 0;
+    int2 stack[STACK];
+
+    while (true) {
+        // ---- finished rays: shade + write; then refill from the queue ----------------
+        const bool idle = node == WW_SENTINEL;
+        if (idle && has_ray) {
+            const Shade sh = shade_hit<SHADOW>(prm, nodes, tris, ray, hit, tb);
+            records[ray_id] = make_float4(sh.r, sh.g, sh.b, sh.depth);
+            if (prm.ray_records) {
+                float4 *rec = reinterpret_cast<float4 *>(prm.ray_records) + 2 * int64_t(ray_id);
+                rec[0] = make_float4(sh.r, sh.g, sh.b, sh.depth);
+                rec[1] = make_float4(sh.t, __int_as_float(sh.prim), __int_as_float(sh.shadow_mask), 0.f);
+            }
+            has_ray = false;
+        }
+        const unsigned need = __ballot_sync(FULL, idle);
+        if (need && !queue_done) {
+            const int leader = __ffs(need) - 1;
+            uint32_t base = 0;
+            if (lane == leader) base = atomicAdd(prm.work_counter, uint32_t(__popc(need)));
+            base = __shfl_sync(FULL, base, leader);
+            if (base + uint32_t(__popc(need)) >= total) queue_done = true;  // warp-uniform
+            if (idle) {
+                const uint32_t id = base + uint32_t(__popc(need & lt_mask));
+                if (id < total) {
+                    ray_id = id;
+                    has_ray = true;
+                    const int64_t q = id / uint32_t(R);
+                    const int r = int(id - uint32_t(q) * uint32_t(R));
+                    const int64_t p = prm.probe_begin + q;
+                    const int64_t i = p % prm.nx, j = (p / prm.nx) % prm.ny,
+                                  k = p / (int64_t(prm.nx) * prm.ny);
+                    ray.ox = float(__dadd_rn(prm.origin[0], __dmul_rn(prm.spacing[0], double(i))));
+                    ray.oy = float(__dadd_rn(prm.origin[1], __dmul_rn(prm.spacing[1], double(j))));
+                    ray.oz = float(__dadd_rn(prm.origin[2], __dmul_rn(prm.spacing[2], double(k))));
+                    const float4 d = __ldg(dirs + r);
+                    ray.dx = d.x;
+                    ray.dy = d.y;
+                    ray.dz = d.z;
+                    const float sx = fabsf(d.x) < 1e-12f ? copysignf(1e-12f, d.x) : d.x;
+                    const float sy = fabsf(d.y) < 1e-12f ? copysignf(1e-12f, d.y) : d.y;
+                    const float sz = fabsf(d.z) < 1e-12f ? copysignf(1e-12f, d.z) : d.z;
+                    ix = 1.0f / sx;
+                    iy = 1.0f / sy;
+                    iz = 1.0f / sz;
+                    oix = ray.ox * ix;
+                    oiy = ray.oy * iy;
+                    oiz = ray.oz * iz;
+                    tb = INFINITY;
+                    hit = -1;
+                    node = 0;
+                    leaf = 0;
+                    sp = 0;
                 }
             }
         }
-        const float inv = __ldg(prm.inv_wsum + t);
-        const float h = prm.hysteresis;
-        const float qs = prm.irradiance_scale > 0.f ? 1.0f / prm.irradiance_scale : 0.f;
-#pragma unroll
-        for (int a = 0; a < QPT; ++a) {
-            const int q = qg + 4 * a;
-            if (q >= nq) continue;
-            float *st = prm.irradiance + ((p0 - prm.probe_begin + q) * 64 + t) * 3;
-            uint32_t texel = 0;
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                float v = acc[a][c] * inv;
-                if (inv == 0.f) v = st[c];  // no ray sees this texel: keep the state
-                else if (h != 0.f) v = fmaf(h, st[c] - v, v);
-                st[c] = v;
-                float x = fminf(fmaxf(v * qs, 0.0f), 1.0f);
-                texel |= __float2uint_rn(x * 1023.0f) << (10 * c);
+        if (__all_sync(FULL, node == WW_SENTINEL)) break;
+
+        // ---- while-while traversal -----------------------------------------------------
+        while (node != WW_SENTINEL) {
+            // inner nodes, postponing the first leaf found
+            while (node >= 0 && node != WW_SENTINEL) {
+                bool h0, h1;
+                float t0, t1;
+                int c0, c1;
+                node_hits(nodes, node, ix, iy, iz, oix, oiy, oiz, tb, h0, h1, t0, t1, c0, c1);
+                if (h0 && h1) {
+                    const bool swap = t1 < t0;
+                    node = swap ? c1 : c0;
+                    stack[sp++] = make_int2(swap ? c0 : c1, __float_as_int(swap ? t0 : t1));
+                } else if (h0 || h1) {
+                    node = h0 ? c0 : c1;
+                } else {
+                    node = ww_pop(stack, sp, tb);
+                }
+                if (node < 0 && leaf == 0) {  // postpone the leaf, keep walking
+                    leaf = node;
+                    node = ww_pop(stack, sp, tb);
+                }
+                if (!__any_sync(__activemask(), leaf == 0)) break;
             }
-            s_ccore[q * 64 + t] = texel;
+            // leaves
+            while (leaf < 0) {
+                const int ref = ~leaf;
+                const int first = ref >> 3, cnt = ref & 7;
+                for (int k = 0; k < cnt; k += 2) {
+                    const float4 a0 = __ldg(tris + 3 * (first + k));
+                    const float4 a1 = __ldg(tris + 3 * (first + k) + 1);
+                    const float4 a2 = __ldg(tris + 3 * (first + k) + 2);
+                    float4 b0, b1, b2;
+                    const bool two = k + 1 < cnt;
+                    if (two) {
+                        b0 = __ldg(tris + 3 * (first + k + 1));
+                        b1 = __ldg(tris + 3 * (first + k + 1) + 1);
+                        b2 = __ldg(tris + 3 * (first + k + 1) + 2);
+                    }
+                    float t = tri_hit(ray, a0, a1, a2);
+                    if (t < tb) {
+                        tb = t;
+                        hit = first + k;
+                    }
+                    if (two) {
+                        t = tri_hit(ray, b0, b1, b2);
+                        if (t < tb) {
+                            tb = t;
+                            hit = first + k + 1;
+                        }
+                    }
+                }
+                leaf = 0;
+                if (node < 0 && node != WW_SENTINEL) {  // another leaf popped: take it now
+                    leaf = node;
+                    node = ww_pop(stack, sp, tb);
+                }
+            }
+            if (__popc(__activemask()) < DYN_FETCH) break;  // refill idle lanes
         }
     }
-    // ---- depth moments (256 texels x P probes) ------------------------------------------
-    {
-        const int t = tid;
-        float m1[P], m2[P];
+}
+
+// ---- pass 2: DDGI blend, register-blocked over P = 16 probes per CTA ----------------------
+// Per probe the blend is two small dense products with per-frame weights
+// shared by every probe: irradiance (64 x R) . (R x 3) and depth moments
+// (256 x R) . (R x 2).  A CTA stages the ray records of 16 probes in shared
+// memory and streams the weight rows through it in chunks of RC rays; each
+// thread owns 4 depth texels x 4 probes (32 accumulators: one LDS.128 of
+// weights + two broadcast LDS.128 of (d, d^2) feed 32 FFMA) and 1 colour
+// texel x 4 probes (12 accumulators).
+constexpr int BP = 16;  // probes per CTA
+constexpr int RC = 16;  // rays per weight chunk
+
+__device__ __forceinline__ void finalize_color(const ps_trace_params &prm, int64_t p_local, int t,
+                                               const float acc[3], float inv, float h, float qs,
+                                               uint32_t *core) {
+    float *st = prm.irradiance + (p_local * 64 + t) * 3;
+    uint32_t texel = 0;
 #pragma unroll
-        for (int q = 0; q < P; ++q) m1[q] = m2[q] = 0.f;
-        const float *wd = prm.w_depth + t;
-        for (int r = 0; r < R; ++r) {
-            const float w = __ldg(wd + r * 256);
+    for (int c = 0; c < 3; ++c) {
+        float v = acc[c] * inv;
+        if (inv == 0.f) v = st[c];  // no ray sees this texel: keep the state
+        else if (h != 0.f) v = fmaf(h, st[c] - v, v);
+        st[c] = v;
+        const float x = fminf(fmaxf(v * qs, 0.0f), 1.0f);
+        texel |= __float2uint_rn(x * 1023.0f) << (10 * c);
+    }
+    *core = texel;
+}
+
+__global__ void __launch_bounds__(THREADS, 2) blend_kernel(ps_trace_params prm) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int R = prm.rays_per_probe;
+    float *s_rgb = reinterpret_cast<float *>(smem_raw);                 // [R][BP][3]
+    float2 *s_dep = reinterpret_cast<float2 *>(s_rgb + R * BP * 3);     // [R][BP]
+    float *s_wd = reinterpret_cast<float *>(s_dep + R * BP);            // [RC][256]
+    float *s_wc = s_wd + RC * 256;                                       // [RC][64]
+    uint32_t *s_ccore = reinterpret_cast<uint32_t *>(s_wd);             // [BP][64]  (aliases W after the loop)
+    uint32_t *s_vcore = s_ccore + BP * 64;                               // [BP][256]
+
+    const int tid = threadIdx.x;
+    const int64_t p0 = int64_t(prm.probe_begin) + int64_t(blockIdx.x) * BP;
+    const int64_t left = int64_t(prm.probe_end) - p0;
+    const int nq = int(left < BP ? left : BP);
+    const int64_t pl0 = p0 - prm.probe_begin;
+    const float4 *records = reinterpret_cast<const float4 *>(prm.records) + pl0 * R;
+    for (int g = tid; g < BP * R; g += THREADS) {
+        const int q = g / R, r = g - q * R;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (q < nq) v = __ldcs(records + g);  // streamed once
+        float *dst = s_rgb + (r * BP + q) * 3;
+        dst[0] = v.x;
+        dst[1] = v.y;
+        dst[2] = v.z;
+        s_dep[r * BP + q] = make_float2(v.w, v.w * v.w);
+    }
+
+    const int tg = tid & 63;       // colour texel / depth texel group
+    const int qg = tid >> 6;       // probe group (4 probes)
+    float cacc[4][3];
+    float dacc[4][4][2];           // [texel][probe][moment]
 #pragma unroll
-            for (int q = 0; q < P; ++q) {
-                const float2 d = s_dep[r * P + q];
-                m1[q] = fmaf(w, d.x, m1[q]);
-                m2[q] = fmaf(w, d.y, m2[q]);
-            }
+    for (int q = 0; q < 4; ++q) {
+        cacc[q][0] = cacc[q][1] = cacc[q][2] = 0.f;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) dacc[k][q][0] = dacc[k][q][1] = 0.f;
+    }
+    const float4 *wd_g = reinterpret_cast<const float4 *>(prm.w_depth);
+    const float4 *wc_g = reinterpret_cast<const float4 *>(prm.w_color);
+    for (int r0 = 0; r0 < R; r0 += RC) {
+        const int rc = min(RC, R - r0);
+        __syncthreads();  // previous chunk consumed (and records staged on the first pass)
+        for (int i = tid; i < rc * 64; i += THREADS)  // depth weights: rc x 256 floats
+            reinterpret_cast<float4 *>(s_wd)[i] = __ldg(wd_g + r0 * 64 + i);
+        for (int i = tid; i < rc * 16; i += THREADS)  // colour weights: rc x 64 floats
+            reinterpret_cast<float4 *>(s_wc)[i] = __ldg(wc_g + r0 * 16 + i);
+        __syncthreads();
+#pragma unroll 4
+        for (int rr = 0; rr < rc; ++rr) {
+            const int r = r0 + rr;
+            const float4 w4 = reinterpret_cast<const float4 *>(s_wd + rr * 256)[tg];
+            const float4 *dp = reinterpret_cast<const float4 *>(s_dep + r * BP + 4 * qg);
+            const float4 d01 = dp[0], d23 = dp[1];
+            const float dv[4][2] = {{d01.x, d01.y}, {d01.z, d01.w}, {d23.x, d23.y}, {d23.z, d23.w}};
+            const float wv[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    dacc[k][q][0] = fmaf(wv[k], dv[q][0], dacc[k][q][0]);
+                    dacc[k][q][1] = fmaf(wv[k], dv[q][1], dacc[k][q][1]);
+                }
+            const float wc = s_wc[rr * 64 + tg];
+            const float4 *cp = reinterpret_cast<const float4 *>(s_rgb + (r * BP + 4 * qg) * 3);
+            const float4 c0 = cp[0], c1 = cp[1], c2 = cp[2];
+            const float cv[12] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w, c2.x, c2.y, c2.z, c2.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) cacc[q][c] = fmaf(wc, cv[3 * q + c], cacc[q][c]);
         }
-        const float inv = __ldg(prm.inv_wsum + 64 + t);
-        const float h = prm.hysteresis;
+    }
+    __syncthreads();  // weights no longer read: their space holds the cores
+
+    const float h = prm.hysteresis;
+    const float qs = prm.irradiance_scale > 0.f ? 1.0f / prm.irradiance_scale : 0.f;
+    {
+        const float inv = __ldg(prm.inv_wsum + tg);
 #pragma unroll
-        for (int q = 0; q < P; ++q) {
-            if (q >= nq) continue;
-            float2 *st = reinterpret_cast<float2 *>(prm.moments) + (p0 - prm.probe_begin + q) * 256 + t;
-            float a = m1[q] * inv, b = m2[q] * inv;
-            if (inv == 0.f) {
-                const float2 o = *st;
-                a = o.x;
-                b = o.y;
-            } else if (h != 0.f) {
-                const float2 o = *st;
-                a = fmaf(h, o.x - a, a);
-                b = fmaf(h, o.y - b, b);
+        for (int q = 0; q < 4; ++q) {
+            const int qq = 4 * qg + q;
+            if (qq < nq) finalize_color(prm, pl0 + qq, tg, cacc[q], inv, h, qs, s_ccore + qq * 64 + tg);
+        }
+    }
+    {
+        const float4 inv4 = __ldg(reinterpret_cast<const float4 *>(prm.inv_wsum + 64) + tg);
+        const float inv[4] = {inv4.x, inv4.y, inv4.z, inv4.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int qq = 4 * qg + q;
+            if (qq >= nq) continue;
+            float4 *st = reinterpret_cast<float4 *>(prm.moments + ((pl0 + qq) * 256 + 4 * tg) * 2);
+            float4 o01 = make_float4(0.f, 0.f, 0.f, 0.f), o23 = o01;
+            if (h != 0.f || inv[0] == 0.f || inv[1] == 0.f || inv[2] == 0.f || inv[3] == 0.f) {
+                o01 = st[0];
+                o23 = st[1];
             }
-            *st = make_float2(a, b);
-            const uint32_t lo = __half_as_ushort(__float2half_rn(a));
-            const uint32_t hi = __half_as_ushort(__float2half_rn(b));
-            s_vcore[q * 256 + t] = lo | (hi << 16);
+            const float old[4][2] = {{o01.x, o01.y}, {o01.z, o01.w}, {o23.x, o23.y}, {o23.z, o23.w}};
+            float nv[4][2];
+            uint4 packed;
+            uint32_t *pk = reinterpret_cast<uint32_t *>(&packed);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                float a = dacc[k][q][0] * inv[k], b = dacc[k][q][1] * inv[k];
+                if (inv[k] == 0.f) {
+                    a = old[k][0];
+                    b = old[k][1];
+                } else if (h != 0.f) {
+                    a = fmaf(h, old[k][0] - a, a);
+                    b = fmaf(h, old[k][1] - b, b);
+                }
+                nv[k][0] = a;
+                nv[k][1] = b;
+                pk[k] = uint32_t(__half_as_ushort(__float2half_rn(a))) |
+                        (uint32_t(__half_as_ushort(__float2half_rn(b))) << 16);
+            }
+            st[0] = make_float4(nv[0][0], nv[0][1], nv[1][0], nv[1][1]);
+            st[1] = make_float4(nv[2][0], nv[2][1], nv[3][0], nv[3][1]);
+            reinterpret_cast<uint4 *>(s_vcore + qq * 256)[tg] = packed;
         }
     }
     __syncthreads();
@@ -504,10 +803,10 @@ __global__ void wsum_kernel(int R, const float *w_color, const float *w_depth, f
     inv_wsum[t] = s > 0.f ? 1.0f / s : 0.0f;
 }
 
-constexpr int PROBES_PER_CTA = 8;
-
-size_t blend_smem_bytes(int R, int P) {
-    return size_t(R) * P * 16 + size_t(R) * P * 8 + size_t(P) * (64 + 256) * 4;
+size_t blend_smem_bytes(int R) {
+    const size_t w = size_t(RC) * (256 + 64) * 4;
+    const size_t cores = size_t(BP) * (64 + 256) * 4;
+    return size_t(R) * BP * 12 + size_t(R) * BP * 8 + (w > cores ? w : cores);
 }
 
 template <class K>
@@ -516,6 +815,43 @@ int resident_blocks(K kernel, int threads, size_t smem) {
     check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, smem),
                "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
     return n > 0 ? n : 1;
+}
+
+template <int SHADOW, int LEAFV, int MINB, int PP = 0>
+void launch_trace_t(const ps_trace_params &p, int sms, cudaStream_t s) {
+    const int per_sm = resident_blocks(trace_kernel<SHADOW, LEAFV, MINB, PP>, THREADS, 0);
+    trace_kernel<SHADOW, LEAFV, MINB, PP><<<sms * per_sm, THREADS, 0, s>>>(p);
+}
+
+template <int SHADOW, int MINB>
+void launch_trace_ww(const ps_trace_params &p, int sms, cudaStream_t s) {
+    const int per_sm = resident_blocks(trace_ww_kernel<SHADOW, MINB>, THREADS, 0);
+    trace_ww_kernel<SHADOW, MINB><<<sms * per_sm, THREADS, 0, s>>>(p);
+}
+
+template <int SHADOW>
+void launch_trace_s(const ps_trace_params &p, int variant, int sms, cudaStream_t s) {
+    switch (variant) {
+        case 20: launch_trace_ww<SHADOW, 1>(p, sms, s); break;
+        case 30: launch_trace_t<SHADOW, 1, 1, 1>(p, sms, s); break;
+        case 31: launch_trace_t<SHADOW, 0, 4, 1>(p, sms, s); break;
+        case 21: launch_trace_ww<SHADOW, 3>(p, sms, s); break;
+        case 22: launch_trace_ww<SHADOW, 4>(p, sms, s); break;
+        case 0: launch_trace_t<SHADOW, 0, 1>(p, sms, s); break;
+        case 2: launch_trace_t<SHADOW, 2, 1>(p, sms, s); break;
+        case 10: launch_trace_t<SHADOW, 0, 4>(p, sms, s); break;
+        case 11: launch_trace_t<SHADOW, 1, 4>(p, sms, s); break;
+        default: launch_trace_t<SHADOW, 1, 1>(p, sms, s); break;
+    }
+}
+
+void launch_trace(const ps_trace_params &p, int variant, int sms, cudaStream_t s) {
+    switch (p.shadow_mode) {
+        case PS_SHADOW_NONE: launch_trace_s<PS_SHADOW_NONE>(p, variant, sms, s); break;
+        case PS_SHADOW_RAYS: launch_trace_s<PS_SHADOW_RAYS>(p, variant, sms, s); break;
+        default: launch_trace_s<PS_SHADOW_MAP>(p, variant, sms, s); break;
+    }
+    check_launch("trace_kernel");
 }
 
 }  // namespace
@@ -571,34 +907,25 @@ int ps_trace_blend(const ps_trace_params *params, void *stream) {
     // pass 1: persistent trace with dynamic chunk claiming
     check_cuda(cudaMemsetAsync(p.work_counter, 0, sizeof(uint32_t), s), "memset counter");
     {
-        int per_sm;
-        switch (p.shadow_mode) {
-            case PS_SHADOW_NONE:
-                per_sm = resident_blocks(trace_kernel<PS_SHADOW_NONE>, THREADS, 0);
-                trace_kernel<PS_SHADOW_NONE><<<sms * per_sm, THREADS, 0, s>>>(p);
-                break;
-            case PS_SHADOW_RAYS:
-                per_sm = resident_blocks(trace_kernel<PS_SHADOW_RAYS>, THREADS, 0);
-                trace_kernel<PS_SHADOW_RAYS><<<sms * per_sm, THREADS, 0, s>>>(p);
-                break;
-            default:
-                per_sm = resident_blocks(trace_kernel<PS_SHADOW_MAP>, THREADS, 0);
-                trace_kernel<PS_SHADOW_MAP><<<sms * per_sm, THREADS, 0, s>>>(p);
-                break;
-        }
-        check_launch("trace_kernel");
+        // PS_TRACE_VARIANT (tuning knob): leaf fetch 0 = sequential, 1 = pairs,
+        // 2 = four in flight; +10 = cap registers for 4 resident CTAs per SM
+        static const int variant = [] {
+            const char *e = getenv("PS_TRACE_VARIANT");
+            return e ? atoi(e) : 1;
+        }();
+        launch_trace(p, variant, sms, s);
     }
     // pass 2: blend
-    const size_t smem = blend_smem_bytes(p.rays_per_probe, PROBES_PER_CTA);
+    const size_t smem = blend_smem_bytes(p.rays_per_probe);
     static bool attr_set = false;
     if (!attr_set) {
-        check_cuda(cudaFuncSetAttribute(blend_kernel<PROBES_PER_CTA>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
+        check_cuda(cudaFuncSetAttribute(blend_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        200 * 1024),
                    "cudaFuncSetAttribute");
         attr_set = true;
     }
     if (smem > 200 * 1024) fail(PS_ERR_VALUE, "too many rays per probe for shared memory");
-    blend_kernel<PROBES_PER_CTA><<<unsigned(ceil_div(nloc, PROBES_PER_CTA)), THREADS, smem, s>>>(p);
+    blend_kernel<<<unsigned(ceil_div(nloc, BP)), THREADS, smem, s>>>(p);
     check_launch("blend_kernel");
     PS_ABI_END
 }

@@ -16,10 +16,20 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("report")
     ap.add_argument("--top", type=int, default=40)
+    ap.add_argument("--kernel", default=None, help="substring of the function name")
     args = ap.parse_args()
     out = subprocess.run(["ncu", "-i", args.report, "--page", "source", "--csv",
                           "--print-source=cuda,sass"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
+    if args.kernel:
+        # keep only the block of rows that belongs to the requested function
+        keep, on = [], False
+        for r in rows:
+            if r and r[0] == "Function Name":
+                on = args.kernel in r[1]
+            if on:
+                keep.append(r)
+        rows = keep
     hdr_i = next(i for i, r in enumerate(rows) if r and r[0] == "Line No")
     hdr = rows[hdr_i]
     si = hdr.index("Warp Stall Sampling (All Samples)")
@@ -27,7 +37,7 @@ def main():
     agg = defaultdict(lambda: [0.0, 0.0, ""])
     src_text = {}
     for r in rows[hdr_i + 1:]:
-        if len(r) <= ii or not r[0]:
+        if len(r) <= ii or not r[0] or r[0] == "Line No":
             continue
         line = r[0]
         src_text.setdefault(line, r[1])
