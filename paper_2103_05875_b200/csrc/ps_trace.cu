@@ -627,79 +627,106 @@ __device__ __forceinline__ void finalize_color(const ps_trace_params &prm, int64
     *core = texel;
 }
 
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+
+constexpr int RGB_STRIDE = BP * 3 + 4;  // padded [r] row of 16 probes x rgb (208 B)
+constexpr int DEP_STRIDE = BP + 4;      // padded [r] row of 16 probe depths (80 B)
+constexpr int W_CHUNK = RC * (256 + 64);  // floats per weight chunk
+
+__device__ __forceinline__ void issue_weight_chunk(float *dst, const float *wd, const float *wc,
+                                                   int r0, int rc, int tid) {
+    for (int i = tid; i < rc * 64; i += THREADS)  // depth weights: rc x 256 floats
+        cp_async16(dst + 4 * i, wd + size_t(r0) * 256 + 4 * i);
+    for (int i = tid; i < rc * 16; i += THREADS)  // colour weights: rc x 64 floats
+        cp_async16(dst + RC * 256 + 4 * i, wc + size_t(r0) * 64 + 4 * i);
+    cp_async_commit();
+}
+
 __global__ void __launch_bounds__(THREADS, 2) blend_kernel(ps_trace_params prm) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int R = prm.rays_per_probe;
-    float *s_rgb = reinterpret_cast<float *>(smem_raw);                 // [R][BP][3]
-    float2 *s_dep = reinterpret_cast<float2 *>(s_rgb + R * BP * 3);     // [R][BP]
-    float *s_wd = reinterpret_cast<float *>(s_dep + R * BP);            // [RC][256]
-    float *s_wc = s_wd + RC * 256;                                       // [RC][64]
-    uint32_t *s_ccore = reinterpret_cast<uint32_t *>(s_wd);             // [BP][64]  (aliases W after the loop)
-    uint32_t *s_vcore = s_ccore + BP * 64;                               // [BP][256]
+    float *s_rgb = reinterpret_cast<float *>(smem_raw);  // [R][RGB_STRIDE]
+    float *s_dep = s_rgb + R * RGB_STRIDE;                // [R][DEP_STRIDE]
+    float *s_w = s_dep + R * DEP_STRIDE;                  // 2 x [RC][256 + 64]
+    uint32_t *s_ccore = reinterpret_cast<uint32_t *>(s_w);  // [BP][64]  (aliases W after the loop)
+    uint32_t *s_vcore = s_ccore + BP * 64;                   // [BP][256]
 
     const int tid = threadIdx.x;
     const int64_t p0 = int64_t(prm.probe_begin) + int64_t(blockIdx.x) * BP;
     const int64_t left = int64_t(prm.probe_end) - p0;
     const int nq = int(left < BP ? left : BP);
     const int64_t pl0 = p0 - prm.probe_begin;
+    const int nchunks = (R + RC - 1) / RC;
+    // weights of the first chunk fly while the ray records are staged
+    issue_weight_chunk(s_w, prm.w_depth, prm.w_color, 0, min(RC, R), tid);
     const float4 *records = reinterpret_cast<const float4 *>(prm.records) + pl0 * R;
     for (int g = tid; g < BP * R; g += THREADS) {
         const int q = g / R, r = g - q * R;
         float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
         if (q < nq) v = __ldcs(records + g);  // streamed once
-        float *dst = s_rgb + (r * BP + q) * 3;
+        float *dst = s_rgb + r * RGB_STRIDE + q * 3;
         dst[0] = v.x;
         dst[1] = v.y;
         dst[2] = v.z;
-        s_dep[r * BP + q] = make_float2(v.w, v.w * v.w);
+        s_dep[r * DEP_STRIDE + q] = v.w;
     }
 
-    const int tg = tid & 63;       // colour texel / depth texel group
-    const int qg = tid >> 6;       // probe group (4 probes)
+    const int tg = tid & 63;  // colour texel / depth texel group
+    const int qg = tid >> 6;  // probe group (4 probes)
     float cacc[4][3];
-    float dacc[4][4][2];           // [texel][probe][moment]
+    float dacc[4][4][2];  // [texel][probe][moment]
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         cacc[q][0] = cacc[q][1] = cacc[q][2] = 0.f;
 #pragma unroll
         for (int k = 0; k < 4; ++k) dacc[k][q][0] = dacc[k][q][1] = 0.f;
     }
-    const float4 *wd_g = reinterpret_cast<const float4 *>(prm.w_depth);
-    const float4 *wc_g = reinterpret_cast<const float4 *>(prm.w_color);
-    for (int r0 = 0; r0 < R; r0 += RC) {
+    for (int c = 0; c < nchunks; ++c) {
+        const int r0 = c * RC;
         const int rc = min(RC, R - r0);
-        __syncthreads();  // previous chunk consumed (and records staged on the first pass)
-        for (int i = tid; i < rc * 64; i += THREADS)  // depth weights: rc x 256 floats
-            reinterpret_cast<float4 *>(s_wd)[i] = __ldg(wd_g + r0 * 64 + i);
-        for (int i = tid; i < rc * 16; i += THREADS)  // colour weights: rc x 64 floats
-            reinterpret_cast<float4 *>(s_wc)[i] = __ldg(wc_g + r0 * 16 + i);
-        __syncthreads();
+        if (c + 1 < nchunks) {
+            issue_weight_chunk(s_w + ((c + 1) & 1) * W_CHUNK, prm.w_depth, prm.w_color, r0 + RC,
+                               min(RC, R - r0 - RC), tid);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();  // chunk c landed for every thread (and the records are staged)
+        const float *wd = s_w + (c & 1) * W_CHUNK;
+        const float *wcol = wd + RC * 256;
 #pragma unroll 4
         for (int rr = 0; rr < rc; ++rr) {
             const int r = r0 + rr;
-            const float4 w4 = reinterpret_cast<const float4 *>(s_wd + rr * 256)[tg];
-            const float4 *dp = reinterpret_cast<const float4 *>(s_dep + r * BP + 4 * qg);
-            const float4 d01 = dp[0], d23 = dp[1];
-            const float dv[4][2] = {{d01.x, d01.y}, {d01.z, d01.w}, {d23.x, d23.y}, {d23.z, d23.w}};
+            const float4 w4 = reinterpret_cast<const float4 *>(wd + rr * 256)[tg];
+            const float4 dq = *reinterpret_cast<const float4 *>(s_dep + r * DEP_STRIDE + 4 * qg);
+            const float dv[4] = {dq.x, dq.y, dq.z, dq.w};
             const float wv[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
+            for (int q = 0; q < 4; ++q) {
+                const float d2 = dv[q] * dv[q];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    dacc[k][q][0] = fmaf(wv[k], dv[q][0], dacc[k][q][0]);
-                    dacc[k][q][1] = fmaf(wv[k], dv[q][1], dacc[k][q][1]);
+                for (int k = 0; k < 4; ++k) {
+                    dacc[k][q][0] = fmaf(wv[k], dv[q], dacc[k][q][0]);
+                    dacc[k][q][1] = fmaf(wv[k], d2, dacc[k][q][1]);
                 }
-            const float wc = s_wc[rr * 64 + tg];
-            const float4 *cp = reinterpret_cast<const float4 *>(s_rgb + (r * BP + 4 * qg) * 3);
+            }
+            const float wc = wcol[rr * 64 + tg];
+            const float4 *cp = reinterpret_cast<const float4 *>(s_rgb + r * RGB_STRIDE + 12 * qg);
             const float4 c0 = cp[0], c1 = cp[1], c2 = cp[2];
             const float cv[12] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w, c2.x, c2.y, c2.z, c2.w};
 #pragma unroll
             for (int q = 0; q < 4; ++q)
 #pragma unroll
-                for (int c = 0; c < 3; ++c) cacc[q][c] = fmaf(wc, cv[3 * q + c], cacc[q][c]);
+                for (int k = 0; k < 3; ++k) cacc[q][k] = fmaf(wc, cv[3 * q + k], cacc[q][k]);
         }
+        __syncthreads();  // buffer (c & 1) is refilled by the issue two chunks later
     }
-    __syncthreads();  // weights no longer read: their space holds the cores
 
     const float h = prm.hysteresis;
     const float qs = prm.irradiance_scale > 0.f ? 1.0f / prm.irradiance_scale : 0.f;
@@ -750,28 +777,32 @@ __global__ void __launch_bounds__(THREADS, 2) blend_kernel(ps_trace_params prm) 
     }
     __syncthreads();
 
-    // ---- atlas blocks with guard bands ----------------------------------------------------
+    // ---- atlas blocks with guard bands (32-bit index math: atlases < 2^31 texels) ----------
     {
         const int ppr = prm.probes_per_row_color;
-        const int64_t W = int64_t(ppr) * 10;
+        const int W = ppr * 10;
+        const int pb = int(p0);
         for (int idx = tid; idx < nq * 100; idx += THREADS) {
             const int q = idx / 100, k = idx - q * 100;
             const int r = k / 10, c = k - r * 10;
-            const int64_t p = p0 + q;
-            const int64_t y0 = (p / ppr) * 10, x0 = (p % ppr) * 10;
-            prm.color_atlas[(y0 + r) * W + x0 + c] = s_ccore[q * 64 + guard_source(r, c, 10)];
+            const int p = pb + q;
+            const int by = p / ppr;
+            const int y0 = by * 10, x0 = (p - by * ppr) * 10;
+            prm.color_atlas[size_t(y0 + r) * W + x0 + c] = s_ccore[q * 64 + guard_source(r, c, 10)];
         }
     }
     {
         const int ppr = prm.probes_per_row_vis;
-        const int64_t W = int64_t(ppr) * 18;
+        const int W = ppr * 18;
+        const int pb = int(p0);
         uint32_t *vis = reinterpret_cast<uint32_t *>(prm.vis_atlas);
         for (int idx = tid; idx < nq * 324; idx += THREADS) {
             const int q = idx / 324, k = idx - q * 324;
             const int r = k / 18, c = k - r * 18;
-            const int64_t p = p0 + q;
-            const int64_t y0 = (p / ppr) * 18, x0 = (p % ppr) * 18;
-            vis[(y0 + r) * W + x0 + c] = s_vcore[q * 256 + guard_source(r, c, 18)];
+            const int p = pb + q;
+            const int by = p / ppr;
+            const int y0 = by * 18, x0 = (p - by * ppr) * 18;
+            vis[size_t(y0 + r) * W + x0 + c] = s_vcore[q * 256 + guard_source(r, c, 18)];
         }
     }
 }
@@ -804,9 +835,9 @@ __global__ void wsum_kernel(int R, const float *w_color, const float *w_depth, f
 }
 
 size_t blend_smem_bytes(int R) {
-    const size_t w = size_t(RC) * (256 + 64) * 4;
+    const size_t w = size_t(2) * W_CHUNK * 4;
     const size_t cores = size_t(BP) * (64 + 256) * 4;
-    return size_t(R) * BP * 12 + size_t(R) * BP * 8 + (w > cores ? w : cores);
+    return size_t(R) * (RGB_STRIDE + DEP_STRIDE) * 4 + (w > cores ? w : cores);
 }
 
 template <class K>
