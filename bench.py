@@ -188,6 +188,7 @@ def run_ours(args, rank, world, local):
         for k in range(args.steps):
             f = args.warmup + k
             server.tick(f, frame_lights(f))
+        server.join()  # the last frame's colour / visibility chains run on side streams
         end.record(stream)
         barrier()
     ms = start.elapsed_time(end) / args.steps

@@ -338,7 +338,7 @@ class UpdateAtlasLayout:
             raise ValueError("layout has no probe capacity; pass probe_count")
         ids = ids.to(torch.int64).contiguous()
         nbytes = N.lib().ps_assign_workspace_bytes(self._cap, self.slot_count)
-        ws = D.Workspace.get(nbytes, self.device, "assign")
+        ws = D.Workspace.get(nbytes, self.device, f"assign.{id(self)}")
         N.call("ps_assign_slots", ids.data_ptr(), D.ptr(count), int(ids.numel()), self._cap,
                self.slot_count, self._probe_slot.data_ptr(), self._slot_probe.data_ptr(),
                self._last_selected.data_ptr(), self._meta.data_ptr(), self._entries.data_ptr(),

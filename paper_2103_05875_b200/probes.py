@@ -119,7 +119,7 @@ class ProbeUpdater:
                  irradiance_scale: float = 1.0, shadows="map", normal_bias: float | None = None,
                  seed: int = 0, probe_range=None, probes_per_row: int | None = None,
                  device=None, record_rays: bool = False, shadow_map_size: int = 256,
-                 shadow_bias: float = 0.02):
+                 shadow_bias: float = 0.02, atlas_buffers: int = 1):
         self.volume = volume
         self.device = torch.device(device) if device is not None else D.device_of()
         self.dscene = scene if isinstance(scene, DeviceScene) else scene.device(self.device)
@@ -151,8 +151,13 @@ class ProbeUpdater:
         dev = self.device
         self.irradiance = torch.zeros((max(nloc, 1), 64, 3), dtype=torch.float32, device=dev)
         self.moments = torch.zeros((max(nloc, 1), 256, 2), dtype=torch.float32, device=dev)
-        self.color = ProbeAtlas(AtlasKind.COLOR, n, probes_per_row, device=dev)
-        self.visibility = ProbeAtlas(AtlasKind.VISIBILITY, n, probes_per_row, device=dev)
+        # atlas_buffers = 2 lets frame f+1 be traced while the streaming
+        # stages still read frame f's atlases (server overlap)
+        self._color_bufs = [ProbeAtlas(AtlasKind.COLOR, n, probes_per_row, device=dev)
+                            for _ in range(atlas_buffers)]
+        self._vis_bufs = [ProbeAtlas(AtlasKind.VISIBILITY, n, probes_per_row, device=dev)
+                          for _ in range(atlas_buffers)]
+        self.color, self.visibility = self._color_bufs[0], self._vis_bufs[0]
         R = self.rays_per_probe
         self.texdir = torch.from_numpy(texel_direction_table()).to(dev)
         self.w_color = torch.empty((R, 64), dtype=torch.float32, device=dev)
@@ -226,6 +231,8 @@ class ProbeUpdater:
                self.texdir.data_ptr(), self.sharpness, self.w_color.data_ptr(),
                self.w_depth.data_ptr(), self.inv_wsum.data_ptr(), stream)
         h = 0.0 if self.frames_done == 0 else self.hysteresis
+        k = self.frames_done % len(self._color_bufs)
+        self.color, self.visibility = self._color_bufs[k], self._vis_bufs[k]
         params = self._params(h)
         N.call("ps_trace_blend", ctypes.byref(params), stream)
         self.frames_done += 1

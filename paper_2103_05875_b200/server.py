@@ -122,11 +122,21 @@ class ProbeStreamServer:
 
     def __init__(self, volume: ProbeVolume, scene, rays_per_probe: int = 256, device=None,
                  color_threshold: float = 0.0, visibility_threshold: float = 0.0,
-                 slot_count=None, budget=None, gop_length: int = DEFAULT_GOP, **probe_kwargs):
+                 slot_count=None, budget=None, gop_length: int = DEFAULT_GOP,
+                 overlap: bool = True, **probe_kwargs):
         self.device = torch.device(device) if device is not None else D.device_of()
         self.volume = volume
+        # overlap: the colour and visibility chains run on their own streams,
+        # concurrently with each other and with the next frame's trace (which
+        # writes the other half of double-buffered atlases)
+        self.overlap = overlap
         self.updater = ProbeUpdater(volume, scene, rays_per_probe=rays_per_probe,
-                                    device=self.device, **probe_kwargs)
+                                    device=self.device, atlas_buffers=2 if overlap else 1,
+                                    **probe_kwargs)
+        self.streams = ({"color": torch.cuda.Stream(self.device),
+                         "visibility": torch.cuda.Stream(self.device)} if overlap else None)
+        self._buf_done = [[], []]   # events: stages finished reading atlas buffer k
+        self._pending = []          # events of the last frame's stage chains
         ppr = self.updater.color.probes_per_row
         self.color = KindStream(AtlasKind.COLOR, volume, self.device, slot_count,
                                 threshold=color_threshold, gop_length=gop_length, budget=budget,
@@ -143,21 +153,55 @@ class ProbeStreamServer:
         self.visibility.timers = self.timers
 
     def tick(self, frame: int | None = None, lights=None, pvs_bits=None):
-        """One server frame; returns (colour KindOutput, visibility KindOutput)."""
+        """One server frame; returns (colour KindOutput, visibility KindOutput).
+
+        With ``overlap`` the outputs are produced on ``self.streams[kind]``;
+        call ``join()`` (or wait on those streams) before reading them."""
         frame = self.seq if frame is None else frame
-        if self.timers is not None:
+        main = torch.cuda.current_stream(self.device)
+        timing = self.timers is not None
+        if self.overlap:
+            buf = self.updater.frames_done % 2
+            for ev in self._buf_done[buf]:  # trace may overwrite that atlas half now
+                main.wait_event(ev)
+        if timing:
             e = torch.cuda.Event(enable_timing=True)
             e.record()
             self.timers.setdefault("trace_blend", []).append((0, e))
         color, vis = self.updater.update(frame, lights)
-        if self.timers is not None:
+        if timing:
             e = torch.cuda.Event(enable_timing=True)
             e.record()
             self.timers["trace_blend"].append((1, e))
-        out_c = self.color.tick(color, self.seq, pvs_bits)
-        out_v = self.visibility.tick(vis, self.seq, pvs_bits)
+        if not self.overlap:
+            out_c = self.color.tick(color, self.seq, pvs_bits)
+            out_v = self.visibility.tick(vis, self.seq, pvs_bits)
+            self.seq += 1
+            return out_c, out_v
+        traced = torch.cuda.Event()
+        traced.record(main)
+        outs, done = [], []
+        for ks, atlas in ((self.color, color), (self.visibility, vis)):
+            st = self.streams[ks.kind.value]
+            st.wait_event(traced)
+            with torch.cuda.stream(st):
+                outs.append(ks.tick(atlas, self.seq, pvs_bits))
+                ev = torch.cuda.Event()
+                ev.record(st)
+                done.append(ev)
+        self._buf_done[buf] = done
+        self._pending = done
         self.seq += 1
-        return out_c, out_v
+        return tuple(outs)
+
+    def join(self) -> None:
+        """Make the current stream wait for the last frame's stage chains."""
+        main = torch.cuda.current_stream(self.device)
+        for ev in self._pending:
+            main.wait_event(ev)
+
+    def output_stream(self, kind: str):
+        return self.streams[kind] if self.overlap else torch.cuda.current_stream(self.device)
 
     def h2d_bytes_per_frame(self) -> int:
         u = self.updater

@@ -42,6 +42,16 @@ class SlabServer:
     def tick(self, frame, lights=None):
         return self.impl.tick(frame, lights)
 
+    def join(self) -> None:
+        """Current stream waits for every stream the last frame used."""
+        if hasattr(self.impl, "join"):
+            self.impl.join()
+
+    def _out_stream(self, kind):
+        if hasattr(self.impl, "output_stream"):
+            return self.impl.output_stream(kind)
+        return torch.cuda.current_stream(self.device)
+
     # --- bench helpers ----------------------------------------------------------------
 
     def run_e2e(self, steps: int, first_frame: int, lights_for):
@@ -68,25 +78,35 @@ class SlabServer:
         for k in range(steps):
             f = first_frame + 1 + k
             outs = impl.tick(f, lights_for(f))
-            for o, h in zip(outs, host):
+            for kind, o, h in zip(("color", "visibility"), outs, host):
                 if o is None:
                     continue
-                h[0].copy_(o.entries, non_blocking=True)
-                h[1].copy_(o.entry_count, non_blocking=True)
-                h[2].copy_(o.skip, non_blocking=True)
+                with torch.cuda.stream(self._out_stream(kind)):  # ordered after the chain
+                    h[0].copy_(o.entries, non_blocking=True)
+                    h[1].copy_(o.entry_count, non_blocking=True)
+                    h[2].copy_(o.skip, non_blocking=True)
+        self.join()
         end.record(stream)
         torch.cuda.synchronize(self.device)
         return {"ms_per_step": start.elapsed_time(end) / steps, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h}
 
     def stage_times(self, frames: int, first_frame: int, lights_for) -> dict:
+        """Per-stage device times, measured with the stages serialised on one
+        stream (no overlap) so each interval is that stage alone."""
         impl = self.impl
+        torch.cuda.synchronize(self.device)
+        overlap = getattr(impl, "overlap", False)
+        if overlap:
+            impl.overlap = False
         impl.enable_stage_timers(True)
         for k in range(frames):
             impl.tick(first_frame + k, lights_for(first_frame + k))
         torch.cuda.synchronize(self.device)
         t = impl.stage_times_ms()
         impl.enable_stage_timers(False)
+        if overlap:
+            impl.overlap = True
         return t
 
     def count_launches(self, frame: int, lights_for):
