@@ -214,6 +214,12 @@ typedef struct ps_bvh_sizes {
 int ps_bvh_build(const double *vertices, int64_t tri_count, int leaf_size,
                  ps_bvh_sizes *sizes, float *nodes_out, float *tris_out);
 
+/* Same with a node width of 2 (16-float nodes) or 4 (32-float nodes: child
+ * boxes as lo.x[4] hi.x[4] lo.y[4] hi.y[4] lo.z[4] hi.z[4], child refs[4],
+ * pad[4]; unused slots have child 0x7fffffff). */
+int ps_bvh_build_wide(const double *vertices, int64_t tri_count, int leaf_size, int width,
+                      ps_bvh_sizes *sizes, float *nodes_out, float *tris_out);
+
 /* Trace parameters (device pointers inside). */
 typedef struct ps_trace_params {
     /* probe grid (volume.py:68-144) */
@@ -227,7 +233,8 @@ typedef struct ps_trace_params {
     const float *ray_dirs;
     int32_t rays_per_probe;
     /* scene */
-    const float *nodes;      /* BVH2 nodes */
+    const float *nodes;      /* BVH nodes (ps_bvh_build_wide layout) */
+    int32_t bvh_width;       /* 2 or 4 */
     const float *tris;       /* triangle records */
     const float *materials;  /* per original triangle, 12 floats: albedo rgb _, emission
                               * rgb _, unit face normal xyz _ (normal in double, rounded) */

@@ -51,7 +51,7 @@ class TraceParams(C.Structure):
         ("probe_begin", _i32), ("probe_end", _i32),
         ("origin", _f64 * 3), ("spacing", _f64 * 3),
         ("ray_dirs", _vp), ("rays_per_probe", _i32),
-        ("nodes", _vp), ("tris", _vp), ("materials", _vp),
+        ("nodes", _vp), ("bvh_width", _i32), ("tris", _vp), ("materials", _vp),
         ("light_count", _i32), ("lights", _vp),
         ("sky", _f32 * 3), ("max_distance", _f32), ("normal_bias", _f32),
         ("shadow_mode", _i32), ("shadow_map_size", _i32), ("shadow_maps", _vp),
@@ -97,6 +97,7 @@ _SIGNATURES = {
                                _i64, _vp]),
     "ps_import_tiles": (_int, [_int, _vp, _i64, _vp, _i32, _vp, _vp, _i64, _i64, _vp, _i64, _vp]),
     "ps_bvh_build": (_int, [_vp, _i64, _int, C.POINTER(BvhSizes), _vp, _vp]),
+    "ps_bvh_build_wide": (_int, [_vp, _i64, _int, _int, C.POINTER(BvhSizes), _vp, _vp]),
     "ps_blend_weights": (_int, [_vp, _i32, _vp, _f32, _vp, _vp, _vp, _vp]),
     "ps_trace_blend": (_int, [C.POINTER(TraceParams), _vp]),
 }

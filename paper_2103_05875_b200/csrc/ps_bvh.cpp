@@ -156,13 +156,41 @@ struct Builder {
 
 }  // namespace
 
-extern "C" int ps_bvh_build(const double *vertices, int64_t tri_count, int leaf_size,
-                            ps_bvh_sizes *sizes, float *nodes_out, float *tris_out) {
+namespace {
+
+constexpr int32_t EMPTY_CHILD = 0x7fffffff;
+
+// round outward so the float box contains the double box
+float round_down(double x) {
+    float f = float(x);
+    return double(f) > x ? std::nextafter(f, -INFINITY) : f;
+}
+float round_up(double x) {
+    float f = float(x);
+    return double(f) < x ? std::nextafter(f, INFINITY) : f;
+}
+void set_int(float *f, int32_t v) { std::memcpy(f, &v, 4); }
+
+struct Wide {
+    int kids[4];
+    int n;
+};
+
+}  // namespace
+
+// Shared implementation: binned-SAH binary build, then emission as BVH2
+// (16-float nodes, see the header comment) or BVH4 (32-float nodes: lo.x[4]
+// hi.x[4] lo.y[4] hi.y[4] lo.z[4] hi.z[4] child[4] pad[4]; a BVH2 node's
+// grandchildren are pulled up, largest surface area first, until four
+// children; unused slots hold child = 0x7fffffff).
+static int bvh_build_impl(const double *vertices, int64_t tri_count, int leaf_size, int width,
+                          ps_bvh_sizes *sizes, float *nodes_out, float *tris_out) {
     try {
         if (!sizes) throw std::invalid_argument("sizes must not be NULL");
         if (tri_count < 1) throw std::invalid_argument("scene needs at least one triangle");
-        if (tri_count > (int64_t(1) << 30)) throw std::invalid_argument("too many triangles");
+        if (tri_count > (int64_t(1) << 27)) throw std::invalid_argument("too many triangles");
         if (leaf_size < 1 || leaf_size > 7) throw std::invalid_argument("leaf_size in [1, 7]");
+        if (width != 2 && width != 4) throw std::invalid_argument("width must be 2 or 4");
         Builder b;
         b.v = vertices;
         b.leaf_size = leaf_size;
@@ -178,84 +206,97 @@ extern "C" int ps_bvh_build(const double *vertices, int64_t tri_count, int leaf_
         }
         b.nodes.reserve(2 * size_t(n));
         b.build(0, n);
-        // Flatten: inner nodes get GPU indices in DFS order (left child first);
-        // a scene that is a single leaf gets a root whose two children are
-        // that leaf and an empty box.
-        std::vector<int> gpu_index(b.nodes.size(), -1);
-        std::vector<int> inner;
-        std::vector<std::pair<int, int>> stack{{0, 1}};
-        int64_t max_depth = 0;
-        while (!stack.empty()) {
-            auto [id, depth] = stack.back();
-            stack.pop_back();
-            if (b.nodes[id].left < 0) continue;
-            max_depth = std::max<int64_t>(max_depth, depth);
-            gpu_index[id] = int(inner.size());
-            inner.push_back(id);
-            stack.push_back({b.nodes[id].right, depth + 1});
-            stack.push_back({b.nodes[id].left, depth + 1});
-        }
-        const bool single_leaf = inner.empty();
-        const int64_t node_count = single_leaf ? 1 : int64_t(inner.size());
-        // leaves in DFS order, triangles contiguous per leaf
-        std::vector<int> leaves;
+
+        // collapse into width-ary nodes (preorder), leaves numbered in DFS order
+        std::vector<Wide> wide;
+        std::vector<int> wide_of(b.nodes.size(), -1);
         std::vector<int> leaf_slot(b.nodes.size(), -1);
-        int64_t slots = 0;
-        {
-            std::vector<int> st{0};
-            while (!st.empty()) {
-                int id = st.back();
-                st.pop_back();
-                if (b.nodes[id].left < 0) {
-                    leaf_slot[id] = int(slots);
-                    leaves.push_back(id);
-                    slots += b.nodes[id].count;
-                } else {
-                    st.push_back(b.nodes[id].right);
-                    st.push_back(b.nodes[id].left);
+        std::vector<int> leaves;
+        int64_t slots = 0, max_depth = 0;
+        std::vector<std::pair<int, int>> st{{0, 1}};  // (build node, depth)
+        while (!st.empty()) {
+            auto [id, depth] = st.back();
+            st.pop_back();
+            Wide w{{0, 0, 0, 0}, 0};
+            if (b.nodes[id].left < 0) {
+                w.kids[0] = id;  // the whole scene is one leaf
+                w.n = 1;
+            } else {
+                std::vector<int> kids{b.nodes[id].left, b.nodes[id].right};
+                while (int(kids.size()) < width) {
+                    int best = -1;
+                    double area = -1.0;
+                    for (int k = 0; k < int(kids.size()); ++k)
+                        if (b.nodes[kids[k]].left >= 0 && b.nodes[kids[k]].box.area() > area) {
+                            area = b.nodes[kids[k]].box.area();
+                            best = k;
+                        }
+                    if (best < 0) break;
+                    const int c = kids[best];
+                    kids[best] = b.nodes[c].left;
+                    kids.insert(kids.begin() + best + 1, b.nodes[c].right);
+                }
+                for (int k = 0; k < int(kids.size()); ++k) w.kids[k] = kids[k];
+                w.n = int(kids.size());
+            }
+            wide_of[id] = int(wide.size());
+            wide.push_back(w);
+            max_depth = std::max<int64_t>(max_depth, depth);
+            // children: leaves get slots now (DFS order), inner ones are visited next
+            for (int k = w.n - 1; k >= 0; --k)
+                if (b.nodes[w.kids[k]].left >= 0) st.push_back({w.kids[k], depth + 1});
+            for (int k = 0; k < w.n; ++k) {
+                const int c = w.kids[k];
+                if (b.nodes[c].left < 0 && leaf_slot[c] < 0) {
+                    leaf_slot[c] = int(slots);
+                    leaves.push_back(c);
+                    slots += b.nodes[c].count;
                 }
             }
         }
-        sizes->node_count = node_count;
+        sizes->node_count = int64_t(wide.size());
         sizes->tri_count = tri_count;
         sizes->tri_slots = slots;
         sizes->max_depth = std::max<int64_t>(max_depth, 1);
         if (!nodes_out || !tris_out) return PS_OK;
 
         auto child_ref = [&](int id) -> int32_t {
-            if (b.nodes[id].left >= 0) return gpu_index[id];
+            if (b.nodes[id].left >= 0) return wide_of[id];
             return ~int32_t((leaf_slot[id] << 3) | b.nodes[id].count);
         };
-        auto put_box = [](float *nd, int which, const Aabb &bx) {
-            // round outward so the float box contains the double box
-            auto dn = [](double x) { float f = float(x); return double(f) > x ? std::nextafter(f, -INFINITY) : f; };
-            auto up = [](double x) { float f = float(x); return double(f) < x ? std::nextafter(f, INFINITY) : f; };
-            nd[which * 4 + 0] = dn(bx.lo[0]);
-            nd[which * 4 + 1] = up(bx.hi[0]);
-            nd[which * 4 + 2] = dn(bx.lo[1]);
-            nd[which * 4 + 3] = up(bx.hi[1]);
-            nd[8 + which * 2 + 0] = dn(bx.lo[2]);
-            nd[8 + which * 2 + 1] = up(bx.hi[2]);
-        };
-        auto set_int = [](float *f, int32_t v) { std::memcpy(f, &v, 4); };
-        if (single_leaf) {
-            float *nd = nodes_out;
-            std::memset(nd, 0, 64);
-            put_box(nd, 0, b.nodes[0].box);
-            Aabb empty;  // inverted box never hits
-            nd[4] = 1.f; nd[5] = -1.f; nd[6] = 1.f; nd[7] = -1.f; nd[10] = 1.f; nd[11] = -1.f;
-            (void)empty;
-            set_int(nd + 12, ~int32_t(b.nodes[0].count));  // leaf at record 0
-            set_int(nd + 13, ~int32_t(0));                 // empty leaf
-        } else {
-            for (size_t g = 0; g < inner.size(); ++g) {
-                const BuildNode &bn = b.nodes[inner[g]];
-                float *nd = nodes_out + 16 * g;
-                std::memset(nd, 0, 64);
-                put_box(nd, 0, b.nodes[bn.left].box);
-                put_box(nd, 1, b.nodes[bn.right].box);
-                set_int(nd + 12, child_ref(bn.left));
-                set_int(nd + 13, child_ref(bn.right));
+        const int nf = width == 2 ? 16 : 32;
+        for (size_t g = 0; g < wide.size(); ++g) {
+            const Wide &w = wide[g];
+            float *nd = nodes_out + nf * g;
+            std::memset(nd, 0, nf * 4);
+            for (int k = 0; k < width; ++k) {
+                if (k >= w.n) {  // unused slot
+                    set_int(nd + (width == 2 ? 12 : 24) + k, width == 2 ? ~int32_t(0) : EMPTY_CHILD);
+                    if (width == 2) {  // inverted box never hit by the BVH2 test
+                        nd[4 * k + 0] = 1.f; nd[4 * k + 1] = -1.f;
+                        nd[4 * k + 2] = 1.f; nd[4 * k + 3] = -1.f;
+                        nd[8 + 2 * k] = 1.f; nd[8 + 2 * k + 1] = -1.f;
+                    }
+                    continue;
+                }
+                const Aabb &bx = b.nodes[w.kids[k]].box;
+                if (width == 2) {
+                    nd[4 * k + 0] = round_down(bx.lo[0]);
+                    nd[4 * k + 1] = round_up(bx.hi[0]);
+                    nd[4 * k + 2] = round_down(bx.lo[1]);
+                    nd[4 * k + 3] = round_up(bx.hi[1]);
+                    nd[8 + 2 * k] = round_down(bx.lo[2]);
+                    nd[8 + 2 * k + 1] = round_up(bx.hi[2]);
+                    set_int(nd + 12 + k, child_ref(w.kids[k]));
+                } else {
+                    nd[0 + k] = round_down(bx.lo[0]);
+                    nd[4 + k] = round_up(bx.hi[0]);
+                    nd[8 + k] = round_down(bx.lo[1]);
+                    nd[12 + k] = round_up(bx.hi[1]);
+                    nd[16 + k] = round_down(bx.lo[2]);
+                    nd[20 + k] = round_up(bx.hi[2]);
+                    set_int(nd + 24 + k, child_ref(w.kids[k]));
+                }
             }
         }
         int64_t s = 0;
@@ -279,4 +320,15 @@ extern "C" int ps_bvh_build(const double *vertices, int64_t tri_count, int leaf_
         ps::set_last_error(e.what());
         return PS_ERR_VALUE;
     }
+}
+
+extern "C" int ps_bvh_build(const double *vertices, int64_t tri_count, int leaf_size,
+                            ps_bvh_sizes *sizes, float *nodes_out, float *tris_out) {
+    return bvh_build_impl(vertices, tri_count, leaf_size, 2, sizes, nodes_out, tris_out);
+}
+
+extern "C" int ps_bvh_build_wide(const double *vertices, int64_t tri_count, int leaf_size,
+                                 int width, ps_bvh_sizes *sizes, float *nodes_out,
+                                 float *tris_out) {
+    return bvh_build_impl(vertices, tri_count, leaf_size, width, sizes, nodes_out, tris_out);
 }

@@ -101,12 +101,55 @@ __device__ __forceinline__ void node_hits(const float4 *nodes, int node, float i
     c1 = __float_as_int(c.y);
 }
 
+// BVH4 node: four child slab tests from one 128-byte node (SoA boxes), the
+// hit children sorted by entry distance with a 5-comparator network.
+constexpr int EMPTY_CHILD = 0x7fffffff;
+
+__device__ __forceinline__ void cswap(float &da, int &ca, float &db, int &cb) {
+    const bool sw = db < da;
+    const float td = sw ? db : da;
+    const int tc = sw ? cb : ca;
+    db = sw ? da : db;
+    cb = sw ? ca : cb;
+    da = td;
+    ca = tc;
+}
+
+__device__ __forceinline__ void node4_hits(const float4 *nodes, int node, float ix, float iy,
+                                           float iz, float oix, float oiy, float oiz, float tmax,
+                                           float d[4], int c[4]) {
+    const float4 *nd = nodes + 8 * node;
+    const float4 lx = __ldg(nd + 0), hx = __ldg(nd + 1), ly = __ldg(nd + 2), hy = __ldg(nd + 3);
+    const float4 lz = __ldg(nd + 4), hz = __ldg(nd + 5);
+    const int4 ch = __ldg(reinterpret_cast<const int4 *>(nd + 6));
+    const float lxa[4] = {lx.x, lx.y, lx.z, lx.w}, hxa[4] = {hx.x, hx.y, hx.z, hx.w};
+    const float lya[4] = {ly.x, ly.y, ly.z, ly.w}, hya[4] = {hy.x, hy.y, hy.z, hy.w};
+    const float lza[4] = {lz.x, lz.y, lz.z, lz.w}, hza[4] = {hz.x, hz.y, hz.z, hz.w};
+    const int ca[4] = {ch.x, ch.y, ch.z, ch.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const float ax = fmaf(lxa[k], ix, -oix), bx = fmaf(hxa[k], ix, -oix);
+        const float ay = fmaf(lya[k], iy, -oiy), by = fmaf(hya[k], iy, -oiy);
+        const float az = fmaf(lza[k], iz, -oiz), bz = fmaf(hza[k], iz, -oiz);
+        const float tn = fmaxf(fmaxf(fminf(ax, bx), fminf(ay, by)), fmaxf(fminf(az, bz), 0.0f));
+        const float tf = fminf(fminf(fmaxf(ax, bx), fmaxf(ay, by)), fminf(fmaxf(az, bz), tmax));
+        const bool hit = tn <= tf && ca[k] != EMPTY_CHILD;
+        d[k] = hit ? tn : INFINITY;
+        c[k] = ca[k];
+    }
+    cswap(d[0], c[0], d[1], c[1]);
+    cswap(d[2], c[2], d[3], c[3]);
+    cswap(d[0], c[0], d[2], c[2]);
+    cswap(d[1], c[1], d[3], c[3]);
+    cswap(d[1], c[1], d[2], c[2]);
+}
+
 // Nearest hit (ANY_HIT = false) or occlusion test (ANY_HIT = true) with a
 // per-thread stack of (node, entry distance) pairs: popped entries farther
 // than the current hit are skipped.  Leaves carry their triangle count
 // (~ref = first << 3 | count), so all of a leaf's triangle records are
 // fetched before the first test.  Returns the hit record index (or -1).
-template <bool ANY_HIT, int LEAFV = 0>
+template <bool ANY_HIT, int LEAFV = 0, int WIDTH = 2>
 __device__ int traverse(const float4 *__restrict__ nodes, const float4 *__restrict__ tris,
                         const Ray &r, float tmax, float &t_best) {
     // reciprocal direction; tiny components replaced so the slabs stay finite
@@ -121,7 +164,18 @@ __device__ int traverse(const float4 *__restrict__ nodes, const float4 *__restri
     int hit_slot = -1;
     t_best = tmax;
     while (true) {
-        if (node >= 0) {
+        if (node >= 0 && WIDTH == 4) {
+            float d[4];
+            int c[4];
+            node4_hits(nodes, node, ix, iy, iz, oix, oiy, oiz, t_best, d, c);
+            if (d[0] != INFINITY) {
+                if (d[3] != INFINITY) stack[sp++] = make_int2(c[3], __float_as_int(d[3]));
+                if (d[2] != INFINITY) stack[sp++] = make_int2(c[2], __float_as_int(d[2]));
+                if (d[1] != INFINITY) stack[sp++] = make_int2(c[1], __float_as_int(d[1]));
+                node = c[0];
+                continue;
+            }
+        } else if (node >= 0) {
             bool h0, h1;
             float t0, t1;
             int c0, c1;
@@ -251,20 +305,20 @@ __device__ __forceinline__ int cube_texel(float vx, float vy, float vz, int S) {
     return (f * S + j) * S + i;
 }
 
-template <int SHADOW>
+template <int SHADOW, int WIDTH>
 __device__ Shade shade_hit(const ps_trace_params &p, const float4 *nodes, const float4 *tris,
                            const Ray &ray, int slot, float t);
 
-template <int SHADOW, int LEAFV>
+template <int SHADOW, int LEAFV, int WIDTH>
 __device__ Shade shade_ray(const ps_trace_params &p, const float4 *nodes, const float4 *tris,
                            const Ray &ray) {
     float t;
-    const int slot = traverse<false, LEAFV>(nodes, tris, ray, INFINITY, t);
-    return shade_hit<SHADOW>(p, nodes, tris, ray, slot, t);
+    const int slot = traverse<false, LEAFV, WIDTH>(nodes, tris, ray, INFINITY, t);
+    return shade_hit<SHADOW, WIDTH>(p, nodes, tris, ray, slot, t);
 }
 
 // radiance + depth of a ray given its nearest hit (slot < 0: miss)
-template <int SHADOW>
+template <int SHADOW, int WIDTH>
 __device__ Shade shade_hit(const ps_trace_params &p, const float4 *nodes, const float4 *tris,
                            const Ray &ray, int slot, float t) {
     Shade s;
@@ -307,7 +361,7 @@ __device__ Shade shade_hit(const ps_trace_params &p, const float4 *nodes, const 
         if (SHADOW == PS_SHADOW_RAYS) {
             Ray sh{sx, sy, sz, ux, uy, uz};
             float ts;
-            if (traverse<true>(nodes, tris, sh, dist, ts) >= 0) continue;
+            if (traverse<true, 1, WIDTH>(nodes, tris, sh, dist, ts) >= 0) continue;
         } else if (SHADOW == PS_SHADOW_MAP) {
             const float dm = __ldg(p.shadow_maps + int64_t(l) * 6 * S * S +
                                    cube_texel(-lx, -ly, -lz, S));
@@ -350,6 +404,7 @@ __device__ __forceinline__ int guard_source(int r, int c, int side) {
 // face f: axis a = f / 2, sign = f % 2 ? -1 : +1, (b, c) = ((a+1)%3, (a+2)%3);
 // texel (i, j): direction e_a*sign + e_b*u + e_c*w with u = (i+.5)/S*2-1,
 // w = (j+.5)/S*2-1, normalised; value = nearest hit distance (inf on a miss).
+template <int WIDTH>
 __global__ void __launch_bounds__(256) shadow_map_kernel(ps_trace_params prm) {
     const int S = prm.shadow_map_size;
     const int64_t per_light = int64_t(6) * S * S;
@@ -374,7 +429,7 @@ __global__ void __launch_bounds__(256) shadow_map_kernel(ps_trace_params prm) {
         Ray ray{__ldg(prm.lights + 6 * l), __ldg(prm.lights + 6 * l + 1),
                 __ldg(prm.lights + 6 * l + 2), d[0] * inv, d[1] * inv, d[2] * inv};
         float t;
-        const int slot = traverse<false>(nodes, tris, ray, INFINITY, t);
+        const int slot = traverse<false, 1, WIDTH>(nodes, tris, ray, INFINITY, t);
         prm.shadow_maps[idx] = slot < 0 ? INFINITY : t;
     }
 }
@@ -384,7 +439,7 @@ __global__ void __launch_bounds__(256) shadow_map_kernel(ps_trace_params prm) {
 // the coherence-ordered set) from a global counter, traces + shades them and
 // writes {rgb, depth}.  Dynamic claiming keeps every SM busy regardless of the
 // large per-direction cost differences.
-template <int SHADOW, int LEAFV, int MINB, int PROBE_PARALLEL = 0>
+template <int SHADOW, int LEAFV, int MINB, int PROBE_PARALLEL, int WIDTH>
 __global__ void __launch_bounds__(THREADS, MINB) trace_kernel(ps_trace_params prm) {
     const float4 *nodes = reinterpret_cast<const float4 *>(prm.nodes);
     const float4 *tris = reinterpret_cast<const float4 *>(prm.tris);
@@ -429,7 +484,7 @@ __global__ void __launch_bounds__(THREADS, MINB) trace_kernel(ps_trace_params pr
         ray.dx = d.x;
         ray.dy = d.y;
         ray.dz = d.z;
-        const Shade s = shade_ray<SHADOW, LEAFV>(prm, nodes, tris, ray);
+        const Shade s = shade_ray<SHADOW, LEAFV, WIDTH>(prm, nodes, tris, ray);
         const int64_t ray_id = q * R + r;
         records[ray_id] = make_float4(s.r, s.g, s.b, s.depth);
         if (prm.ray_records) {
@@ -485,7 +540,7 @@ __global__ void __launch_bounds__(THREADS, MINB) trace_ww_kernel(ps_trace_params
         // ---- finished rays: shade + write; then refill from the queue ----------------
         const bool idle = node == WW_SENTINEL;
         if (idle && has_ray) {
-            const Shade sh = shade_hit<SHADOW>(prm, nodes, tris, ray, hit, tb);
+            const Shade sh = shade_hit<SHADOW, 2>(prm, nodes, tris, ray, hit, tb);
             records[ray_id] = make_float4(sh.r, sh.g, sh.b, sh.depth);
             if (prm.ray_records) {
                 float4 *rec = reinterpret_cast<float4 *>(prm.ray_records) + 2 * int64_t(ray_id);
@@ -848,10 +903,10 @@ int resident_blocks(K kernel, int threads, size_t smem) {
     return n > 0 ? n : 1;
 }
 
-template <int SHADOW, int LEAFV, int MINB, int PP = 0>
+template <int SHADOW, int LEAFV, int MINB, int PP, int WIDTH>
 void launch_trace_t(const ps_trace_params &p, int sms, cudaStream_t s) {
-    const int per_sm = resident_blocks(trace_kernel<SHADOW, LEAFV, MINB, PP>, THREADS, 0);
-    trace_kernel<SHADOW, LEAFV, MINB, PP><<<sms * per_sm, THREADS, 0, s>>>(p);
+    const int per_sm = resident_blocks(trace_kernel<SHADOW, LEAFV, MINB, PP, WIDTH>, THREADS, 0);
+    trace_kernel<SHADOW, LEAFV, MINB, PP, WIDTH><<<sms * per_sm, THREADS, 0, s>>>(p);
 }
 
 template <int SHADOW, int MINB>
@@ -862,17 +917,23 @@ void launch_trace_ww(const ps_trace_params &p, int sms, cudaStream_t s) {
 
 template <int SHADOW>
 void launch_trace_s(const ps_trace_params &p, int variant, int sms, cudaStream_t s) {
+    if (p.bvh_width == 4) {
+        switch (variant) {
+            case 0: launch_trace_t<SHADOW, 0, 1, 0, 4>(p, sms, s); break;
+            case 10: launch_trace_t<SHADOW, 0, 4, 0, 4>(p, sms, s); break;
+            case 11: launch_trace_t<SHADOW, 1, 4, 0, 4>(p, sms, s); break;
+            case 30: launch_trace_t<SHADOW, 1, 1, 1, 4>(p, sms, s); break;
+            default: launch_trace_t<SHADOW, 1, 1, 0, 4>(p, sms, s); break;
+        }
+        return;
+    }
     switch (variant) {
         case 20: launch_trace_ww<SHADOW, 1>(p, sms, s); break;
-        case 30: launch_trace_t<SHADOW, 1, 1, 1>(p, sms, s); break;
-        case 31: launch_trace_t<SHADOW, 0, 4, 1>(p, sms, s); break;
-        case 21: launch_trace_ww<SHADOW, 3>(p, sms, s); break;
         case 22: launch_trace_ww<SHADOW, 4>(p, sms, s); break;
-        case 0: launch_trace_t<SHADOW, 0, 1>(p, sms, s); break;
-        case 2: launch_trace_t<SHADOW, 2, 1>(p, sms, s); break;
-        case 10: launch_trace_t<SHADOW, 0, 4>(p, sms, s); break;
-        case 11: launch_trace_t<SHADOW, 1, 4>(p, sms, s); break;
-        default: launch_trace_t<SHADOW, 1, 1>(p, sms, s); break;
+        case 30: launch_trace_t<SHADOW, 1, 1, 1, 2>(p, sms, s); break;
+        case 0: launch_trace_t<SHADOW, 0, 1, 0, 2>(p, sms, s); break;
+        case 10: launch_trace_t<SHADOW, 0, 4, 0, 2>(p, sms, s); break;
+        default: launch_trace_t<SHADOW, 1, 1, 0, 2>(p, sms, s); break;
     }
 }
 
@@ -920,6 +981,10 @@ int ps_trace_blend(const ps_trace_params *params, void *stream) {
     if (p.light_count < 0 || p.light_count > 30) fail(PS_ERR_VALUE, "light_count in [0, 30]");
     if (p.probes_per_row_color < 1 || p.probes_per_row_vis < 1) fail(PS_ERR_LAYOUT, "bad atlas layout");
     if (p.shadow_mode < PS_SHADOW_NONE || p.shadow_mode > PS_SHADOW_MAP) fail(PS_ERR_VALUE, "bad shadow_mode");
+    if (p.bvh_width != 2 && p.bvh_width != 4) fail(PS_ERR_VALUE, "bvh_width must be 2 or 4");
+    if (p.bvh_width == 4 && (p.shadow_mode == PS_SHADOW_RAYS || false)) {
+        // any-hit shadow rays use the same templated traversal: fine
+    }
     if (p.shadow_mode == PS_SHADOW_MAP && p.light_count > 0 &&
         (p.shadow_map_size < 1 || p.shadow_map_size > 4096 || !p.shadow_maps))
         fail(PS_ERR_VALUE, "shadow map size / buffer missing");
@@ -932,7 +997,10 @@ int ps_trace_blend(const ps_trace_params *params, void *stream) {
     if (p.shadow_mode == PS_SHADOW_MAP && p.light_count > 0) {
         const int64_t texels = int64_t(p.light_count) * 6 * p.shadow_map_size * p.shadow_map_size;
         const unsigned blocks = unsigned(std::min<int64_t>(ceil_div(texels, 256), int64_t(sms) * 32));
-        shadow_map_kernel<<<blocks, 256, 0, s>>>(p);
+        if (p.bvh_width == 4)
+            shadow_map_kernel<4><<<blocks, 256, 0, s>>>(p);
+        else
+            shadow_map_kernel<2><<<blocks, 256, 0, s>>>(p);
         check_launch("shadow_map_kernel");
     }
     // pass 1: persistent trace with dynamic chunk claiming

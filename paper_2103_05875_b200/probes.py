@@ -186,6 +186,7 @@ class ProbeUpdater:
         p.ray_dirs = self.ray_dirs.data_ptr()
         p.rays_per_probe = self.rays_per_probe
         p.nodes, p.tris, p.materials = s.nodes.data_ptr(), s.tris.data_ptr(), s.materials.data_ptr()
+        p.bvh_width = s.width
         p.light_count = s.light_count
         p.lights = s.lights.data_ptr()
         p.sky = (ctypes.c_float * 3)(*map(float, s.scene.sky))

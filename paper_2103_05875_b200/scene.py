@@ -68,31 +68,35 @@ class Scene:
         m[:, 8:11] = self.face_normals()
         return m
 
-    def device(self, device=None, leaf_size: int = 4) -> "DeviceScene":
-        return DeviceScene(self, device, leaf_size)
+    def device(self, device=None, leaf_size: int = 4, width: int = 4) -> "DeviceScene":
+        return DeviceScene(self, device, leaf_size, width)
 
 
 class DeviceScene:
     """BVH + triangles + materials + lights resident in HBM (replicated per GPU)."""
 
-    def __init__(self, scene: Scene, device=None, leaf_size: int = 4):
+    def __init__(self, scene: Scene, device=None, leaf_size: int = 4, width: int = 4):
         import torch
 
         from . import _device as D
 
         self.scene = scene
+        self.width = int(width)
         self.device = torch.device(device) if device is not None else D.device_of()
         verts = np.ascontiguousarray(scene.vertices, dtype=np.float64)
         sizes = N.BvhSizes()
         vp = verts.ctypes.data_as(ctypes.c_void_p)
-        N.check(N.lib().ps_bvh_build(vp, len(verts), leaf_size, ctypes.byref(sizes), None, None),
-                "ps_bvh_build")
-        nodes = np.zeros(sizes.node_count * 16, np.float32)
+        N.check(N.lib().ps_bvh_build_wide(vp, len(verts), leaf_size, self.width,
+                                          ctypes.byref(sizes), None, None), "ps_bvh_build_wide")
+        nodes = np.zeros(sizes.node_count * (16 if self.width == 2 else 32), np.float32)
         tris = np.zeros(sizes.tri_slots * 12, np.float32)
-        N.check(N.lib().ps_bvh_build(vp, len(verts), leaf_size, ctypes.byref(sizes),
-                                     nodes.ctypes.data_as(ctypes.c_void_p),
-                                     tris.ctypes.data_as(ctypes.c_void_p)), "ps_bvh_build")
-        if sizes.max_depth >= 64:
+        N.check(N.lib().ps_bvh_build_wide(vp, len(verts), leaf_size, self.width,
+                                          ctypes.byref(sizes),
+                                          nodes.ctypes.data_as(ctypes.c_void_p),
+                                          tris.ctypes.data_as(ctypes.c_void_p)),
+                "ps_bvh_build_wide")
+        # traversal stack: at most width - 1 pushes per level (64 entries)
+        if (self.width - 1) * sizes.max_depth + 1 > 64:
             raise ValueError(f"BVH depth {sizes.max_depth} exceeds the traversal stack (64)")
         self.sizes = (int(sizes.node_count), int(sizes.tri_slots), int(sizes.max_depth))
         self.host_nodes, self.host_tris = nodes, tris

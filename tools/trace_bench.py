@@ -17,6 +17,7 @@ def main():
     ap.add_argument("--frames", type=int, default=10)
     ap.add_argument("--shadows", default="map")
     ap.add_argument("--leaf-size", type=int, default=4)
+    ap.add_argument("--width", type=int, default=4)
     args = ap.parse_args()
     import torch
 
@@ -27,7 +28,7 @@ def main():
     dims, rays, scene_name = bench.CONFIGS[args.config]
     sc = bench.build_scene(scene_name)
     vol = S.volume_for(sc, dims)
-    ds = sc.device(leaf_size=args.leaf_size)
+    ds = sc.device(leaf_size=args.leaf_size, width=args.width)
     upd = ProbeUpdater(vol, ds, rays_per_probe=rays, shadows=args.shadows)
     for f in range(3):
         upd.update(f, S.moving_light(sc, f).lights)
@@ -41,7 +42,7 @@ def main():
     ms = a.elapsed_time(b) / args.frames
     import os
     print(json.dumps({"variant": os.environ.get("PS_TRACE_VARIANT", "default"),
-                      "leaf_size": args.leaf_size, "config": args.config, "shadows": args.shadows,
+                      "leaf_size": args.leaf_size, "width": args.width, "config": args.config, "shadows": args.shadows,
                       "ms": round(ms, 3), "grays": round(vol.probe_count * rays / ms / 1e6, 3),
                       "bvh": ds.sizes}))
 
