@@ -132,6 +132,19 @@ size_t ps_compact_workspace_bytes(int64_t probe_count);
 int ps_bits_to_ids(const uint32_t *bits, int64_t probe_count, int64_t *out_ids,
                    int64_t *out_count, void *workspace, size_t workspace_bytes, void *stream);
 
+/* Potentially visible probes (selection.py:384-407) over a triangle scene:
+ * ray_dirs (ray_count, 3) float64 from pvs_rays (frustum grid + fibonacci
+ * sphere), camera = pose.position, volume_origin / volume_spacing: HOST
+ * pointers to 3 doubles each; vertices (T, 3, 3) float64 on the device
+ * (the BVH's source triangles), BVH as built by ps_bvh_build_wide.  Writes
+ * the active-masked cage bitmap and (optionally) ascending ids + count. */
+size_t ps_pvs_workspace_bytes(int64_t probe_count);
+int ps_pvs(const float *nodes, int32_t bvh_width, const float *tris, const double *vertices,
+           const double *ray_dirs, int64_t ray_count, const double *camera, int32_t nx, int32_t ny,
+           int32_t nz, const double *volume_origin, const double *volume_spacing,
+           const uint8_t *active, uint32_t *mask_bits, int64_t *out_ids, int64_t *out_count,
+           void *workspace, size_t workspace_bytes, void *stream);
+
 /* ---------------------------------------------------------------------------
  * Stage (3) tail: budgeted selection (selection.py:413-437).
  * candidates = changed & pvs & active (bitmaps; pvs_bits NULL = all), ordered

@@ -85,6 +85,9 @@ _SIGNATURES = {
     "ps_ids_to_bits": (_int, [_vp, _vp, _i64, _i64, _vp, _vp, _vp]),
     "ps_compact_workspace_bytes": (_sz, [_i64]),
     "ps_bits_to_ids": (_int, [_vp, _i64, _vp, _vp, _vp, _sz, _vp]),
+    "ps_pvs_workspace_bytes": (_sz, [_i64]),
+    "ps_pvs": (_int, [_vp, _i32, _vp, _vp, _vp, _i64, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp,
+                      _vp, _vp, _vp, _sz, _vp]),
     "ps_select_workspace_bytes": (_sz, [_i64]),
     "ps_select": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _int, _i64, _vp, _vp, _vp, _sz, _vp]),
     "ps_assign_workspace_bytes": (_sz, [_i64, _i64]),

@@ -1,0 +1,256 @@
+// BVH traversal shared by the probe tracer (ps_trace.cu) and the PVS kernel
+// (ps_pvs.cu): ray/triangle test with the reference's semantics
+// (selection.py:123-139), BVH2 and BVH4 node tests, stack traversal.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+
+namespace ps {
+namespace trav {
+
+constexpr int STACK = 64;
+constexpr float RAY_EPS = 1e-6f;  // selection.py:22
+
+struct Ray {
+    float ox, oy, oz, dx, dy, dz;
+};
+
+__device__ __forceinline__ float3 f3(float4 v) { return make_float3(v.x, v.y, v.z); }
+
+__device__ __forceinline__ float dot3(float ax, float ay, float az, float bx, float by, float bz) {
+    return fmaf(az, bz, fmaf(ay, by, ax * bx));
+}
+
+// Moller-Trumbore with the reference's epsilons; returns t or +inf
+__device__ __forceinline__ float tri_hit(const Ray &r, float4 v0, float4 e1, float4 e2) {
+    const float px = r.dy * e2.z - r.dz * e2.y;
+    const float py = r.dz * e2.x - r.dx * e2.z;
+    const float pz = r.dx * e2.y - r.dy * e2.x;
+    const float det = dot3(e1.x, e1.y, e1.z, px, py, pz);
+    if (!(fabsf(det) > RAY_EPS)) return INFINITY;
+    const float inv = 1.0f / det;
+    const float tx = r.ox - v0.x, ty = r.oy - v0.y, tz = r.oz - v0.z;
+    const float u = dot3(tx, ty, tz, px, py, pz) * inv;
+    const float qx = ty * e1.z - tz * e1.y;
+    const float qy = tz * e1.x - tx * e1.z;
+    const float qz = tx * e1.y - ty * e1.x;
+    const float v = dot3(r.dx, r.dy, r.dz, qx, qy, qz) * inv;
+    const float t = dot3(e2.x, e2.y, e2.z, qx, qy, qz) * inv;
+    const bool ok = (u >= -RAY_EPS) && (v >= -RAY_EPS) && (u + v <= 1.0f + RAY_EPS) && (t > RAY_EPS);
+    return ok ? t : INFINITY;
+}
+
+// slab test against the two child boxes of a node
+__device__ __forceinline__ void node_hits(const float4 *nodes, int node, float ix, float iy,
+                                          float iz, float oix, float oiy, float oiz, float tmax,
+                                          bool &h0, bool &h1, float &t0, float &t1, int &c0,
+                                          int &c1) {
+    const float4 a = __ldg(nodes + 4 * node + 0);
+    const float4 b = __ldg(nodes + 4 * node + 1);
+    const float4 z = __ldg(nodes + 4 * node + 2);
+    const float4 c = __ldg(nodes + 4 * node + 3);
+    // child 0
+    float lx = fmaf(a.x, ix, -oix), hx = fmaf(a.y, ix, -oix);
+    float ly = fmaf(a.z, iy, -oiy), hy = fmaf(a.w, iy, -oiy);
+    float lz = fmaf(z.x, iz, -oiz), hz = fmaf(z.y, iz, -oiz);
+    float n0 = fmaxf(fmaxf(fminf(lx, hx), fminf(ly, hy)), fmaxf(fminf(lz, hz), 0.0f));
+    float f0 = fminf(fminf(fmaxf(lx, hx), fmaxf(ly, hy)), fminf(fmaxf(lz, hz), tmax));
+    // child 1
+    lx = fmaf(b.x, ix, -oix);
+    hx = fmaf(b.y, ix, -oix);
+    ly = fmaf(b.z, iy, -oiy);
+    hy = fmaf(b.w, iy, -oiy);
+    lz = fmaf(z.z, iz, -oiz);
+    hz = fmaf(z.w, iz, -oiz);
+    float n1 = fmaxf(fmaxf(fminf(lx, hx), fminf(ly, hy)), fmaxf(fminf(lz, hz), 0.0f));
+    float f1 = fminf(fminf(fmaxf(lx, hx), fmaxf(ly, hy)), fminf(fmaxf(lz, hz), tmax));
+    h0 = n0 <= f0;
+    h1 = n1 <= f1;
+    t0 = n0;
+    t1 = n1;
+    c0 = __float_as_int(c.x);
+    c1 = __float_as_int(c.y);
+}
+
+// BVH4 node: four child slab tests from one 128-byte node (SoA boxes), the
+// hit children sorted by entry distance with a 5-comparator network.
+constexpr int EMPTY_CHILD = 0x7fffffff;
+
+__device__ __forceinline__ void cswap(float &da, int &ca, float &db, int &cb) {
+    const bool sw = db < da;
+    const float td = sw ? db : da;
+    const int tc = sw ? cb : ca;
+    db = sw ? da : db;
+    cb = sw ? ca : cb;
+    da = td;
+    ca = tc;
+}
+
+__device__ __forceinline__ void node4_hits(const float4 *nodes, int node, float ix, float iy,
+                                           float iz, float oix, float oiy, float oiz, float tmax,
+                                           float d[4], int c[4]) {
+    const float4 *nd = nodes + 8 * node;
+    const float4 lx = __ldg(nd + 0), hx = __ldg(nd + 1), ly = __ldg(nd + 2), hy = __ldg(nd + 3);
+    const float4 lz = __ldg(nd + 4), hz = __ldg(nd + 5);
+    const int4 ch = __ldg(reinterpret_cast<const int4 *>(nd + 6));
+    const float lxa[4] = {lx.x, lx.y, lx.z, lx.w}, hxa[4] = {hx.x, hx.y, hx.z, hx.w};
+    const float lya[4] = {ly.x, ly.y, ly.z, ly.w}, hya[4] = {hy.x, hy.y, hy.z, hy.w};
+    const float lza[4] = {lz.x, lz.y, lz.z, lz.w}, hza[4] = {hz.x, hz.y, hz.z, hz.w};
+    const int ca[4] = {ch.x, ch.y, ch.z, ch.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const float ax = fmaf(lxa[k], ix, -oix), bx = fmaf(hxa[k], ix, -oix);
+        const float ay = fmaf(lya[k], iy, -oiy), by = fmaf(hya[k], iy, -oiy);
+        const float az = fmaf(lza[k], iz, -oiz), bz = fmaf(hza[k], iz, -oiz);
+        const float tn = fmaxf(fmaxf(fminf(ax, bx), fminf(ay, by)), fmaxf(fminf(az, bz), 0.0f));
+        const float tf = fminf(fminf(fmaxf(ax, bx), fmaxf(ay, by)), fminf(fmaxf(az, bz), tmax));
+        const bool hit = tn <= tf && ca[k] != EMPTY_CHILD;
+        d[k] = hit ? tn : INFINITY;
+        c[k] = ca[k];
+    }
+    cswap(d[0], c[0], d[1], c[1]);
+    cswap(d[2], c[2], d[3], c[3]);
+    cswap(d[0], c[0], d[2], c[2]);
+    cswap(d[1], c[1], d[3], c[3]);
+    cswap(d[1], c[1], d[2], c[2]);
+}
+
+// Nearest hit (ANY_HIT = false) or occlusion test (ANY_HIT = true) with a
+// per-thread stack of (node, entry distance) pairs: popped entries farther
+// than the current hit are skipped.  Leaves carry their triangle count
+// (~ref = first << 3 | count), so all of a leaf's triangle records are
+// fetched before the first test.  Returns the hit record index (or -1).
+template <bool ANY_HIT, int LEAFV = 0, int WIDTH = 2>
+__device__ int traverse(const float4 *__restrict__ nodes, const float4 *__restrict__ tris,
+                        const Ray &r, float tmax, float &t_best) {
+    // reciprocal direction; tiny components replaced so the slabs stay finite
+    const float sx = fabsf(r.dx) < 1e-12f ? copysignf(1e-12f, r.dx) : r.dx;
+    const float sy = fabsf(r.dy) < 1e-12f ? copysignf(1e-12f, r.dy) : r.dy;
+    const float sz = fabsf(r.dz) < 1e-12f ? copysignf(1e-12f, r.dz) : r.dz;
+    const float ix = 1.0f / sx, iy = 1.0f / sy, iz = 1.0f / sz;
+    const float oix = r.ox * ix, oiy = r.oy * iy, oiz = r.oz * iz;
+    int2 stack[STACK];
+    int sp = 0;
+    int node = 0;
+    int hit_slot = -1;
+    t_best = tmax;
+    while (true) {
+        if (node >= 0 && WIDTH == 4) {
+            float d[4];
+            int c[4];
+            node4_hits(nodes, node, ix, iy, iz, oix, oiy, oiz, t_best, d, c);
+            if (d[0] != INFINITY) {
+                if (d[3] != INFINITY) stack[sp++] = make_int2(c[3], __float_as_int(d[3]));
+                if (d[2] != INFINITY) stack[sp++] = make_int2(c[2], __float_as_int(d[2]));
+                if (d[1] != INFINITY) stack[sp++] = make_int2(c[1], __float_as_int(d[1]));
+                node = c[0];
+                continue;
+            }
+        } else if (node >= 0) {
+            bool h0, h1;
+            float t0, t1;
+            int c0, c1;
+            node_hits(nodes, node, ix, iy, iz, oix, oiy, oiz, t_best, h0, h1, t0, t1, c0, c1);
+            if (h0 && h1) {
+                const bool swap = t1 < t0;
+                node = swap ? c1 : c0;
+                stack[sp++] = make_int2(swap ? c0 : c1, __float_as_int(swap ? t0 : t1));
+                continue;
+            }
+            if (h0 || h1) {
+                node = h0 ? c0 : c1;
+                continue;
+            }
+        } else {
+            const int ref = ~node;
+            const int first = ref >> 3, cnt = ref & 7;
+            if (LEAFV == 2) {  // fetch up to 4 triangles before testing
+                float4 v0[4], e1[4], e2[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (k < cnt) {
+                        v0[k] = __ldg(tris + 3 * (first + k));
+                        e1[k] = __ldg(tris + 3 * (first + k) + 1);
+                        e2[k] = __ldg(tris + 3 * (first + k) + 2);
+                    }
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (k < cnt) {
+                        const float t = tri_hit(r, v0[k], e1[k], e2[k]);
+                        if (t < t_best) {
+                            t_best = t;
+                            hit_slot = first + k;
+                            if (ANY_HIT) return hit_slot;
+                        }
+                    }
+            } else if (LEAFV == 1) {  // two triangles in flight
+                for (int k = 0; k < cnt; k += 2) {
+                    const float4 a0 = __ldg(tris + 3 * (first + k));
+                    const float4 a1 = __ldg(tris + 3 * (first + k) + 1);
+                    const float4 a2 = __ldg(tris + 3 * (first + k) + 2);
+                    float4 b0, b1, b2;
+                    const bool two = k + 1 < cnt;
+                    if (two) {
+                        b0 = __ldg(tris + 3 * (first + k + 1));
+                        b1 = __ldg(tris + 3 * (first + k + 1) + 1);
+                        b2 = __ldg(tris + 3 * (first + k + 1) + 2);
+                    }
+                    float t = tri_hit(r, a0, a1, a2);
+                    if (t < t_best) {
+                        t_best = t;
+                        hit_slot = first + k;
+                        if (ANY_HIT) return hit_slot;
+                    }
+                    if (two) {
+                        t = tri_hit(r, b0, b1, b2);
+                        if (t < t_best) {
+                            t_best = t;
+                            hit_slot = first + k + 1;
+                            if (ANY_HIT) return hit_slot;
+                        }
+                    }
+                }
+            } else {
+                for (int k = 0; k < cnt; ++k) {
+                    const float t = tri_hit(r, __ldg(tris + 3 * (first + k)),
+                                            __ldg(tris + 3 * (first + k) + 1),
+                                            __ldg(tris + 3 * (first + k) + 2));
+                    if (t < t_best) {
+                        t_best = t;
+                        hit_slot = first + k;
+                        if (ANY_HIT) return hit_slot;
+                    }
+                }
+            }
+            if (LEAFV == 2)
+                for (int k = 4; k < cnt; ++k) {  // leaves larger than 4 (leaf_size > 4)
+                    const float t = tri_hit(r, __ldg(tris + 3 * (first + k)),
+                                            __ldg(tris + 3 * (first + k) + 1),
+                                            __ldg(tris + 3 * (first + k) + 2));
+                    if (t < t_best) {
+                        t_best = t;
+                        hit_slot = first + k;
+                        if (ANY_HIT) return hit_slot;
+                    }
+                }
+        }
+        // pop the nearest pending subtree that can still hold a closer hit
+        bool found = false;
+        while (sp > 0) {
+            const int2 e = stack[--sp];
+            if (__int_as_float(e.y) <= t_best) {
+                node = e.x;
+                found = true;
+                break;
+            }
+        }
+        if (!found) break;
+    }
+    return hit_slot;
+}
+
+
+}  // namespace trav
+}  // namespace ps

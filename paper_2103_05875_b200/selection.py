@@ -182,3 +182,166 @@ def select_for_client(changed, pvs, volume, last_sent_seq, current_seq: int, bud
     ids, count = select_device(cb, pb, volume, last_sent_seq, current_seq, budget)
     k = int(count.item())
     return ids[:k].cpu().tolist()
+
+
+# --- potentially visible set (selection.py:174-249, 329-407) --------------------------
+
+RAY_EPS = 1e-6  # selection.py:22
+
+
+class CameraPose:
+    """Client camera (selection.py:177-222): position, unit forward, up, fov, aspect."""
+
+    def __init__(self, position, forward, up=(0.0, 1.0, 0.0), fov_y_deg: float = 90.0,
+                 aspect: float = 1.0):
+        self.position = np.asarray(position, dtype=np.float64)
+        f = np.asarray(forward, dtype=np.float64)
+        length = np.linalg.norm(f)
+        if length < 1e-9:
+            raise ValueError("camera forward vector must be nonzero")
+        self.forward = f / length
+        self.up = np.asarray(up, dtype=np.float64)
+        self.fov_y_deg = fov_y_deg
+        self.aspect = aspect
+
+    def basis(self):
+        f = self.forward
+        right = np.cross(f, self.up)
+        for fallback in (np.array([1.0, 0.0, 0.0]), np.array([0.0, 0.0, 1.0])):
+            if np.linalg.norm(right) >= 1e-9:
+                break
+            right = np.cross(f, fallback)  # up parallel to forward
+        right = right / np.linalg.norm(right)
+        return f, right, np.cross(right, f)
+
+
+class SelectionParams:
+    """selection.py:255-267."""
+
+    def __init__(self, change_threshold: float = 0.0, sphere_rays: int = 1024,
+                 raster_cols: int = 64, raster_rows: int = 64, budget=None):
+        if raster_cols * raster_rows < 1 and sphere_rays < 1:
+            raise ValueError("at least one ray is required")
+        if budget is not None and budget < 0:
+            raise ValueError("budget must be >= 0")
+        self.change_threshold = change_threshold
+        self.sphere_rays = sphere_rays
+        self.raster_cols = raster_cols
+        self.raster_rows = raster_rows
+        self.budget = budget
+
+
+def frustum_directions(pose: CameraPose, cols: int, rows: int) -> np.ndarray:
+    """Unit directions through the centres of a cols x rows frustum grid."""
+    f, r, u = pose.basis()
+    ty = np.tan(np.radians(pose.fov_y_deg) / 2.0)
+    tx = ty * pose.aspect
+    sx = (np.arange(cols) + 0.5) / cols * 2.0 - 1.0
+    sy = (np.arange(rows) + 0.5) / rows * 2.0 - 1.0
+    gx, gy = np.meshgrid(sx, sy, indexing="xy")
+    d = f[None, :] + (gx.reshape(-1, 1) * tx) * r[None, :] + (gy.reshape(-1, 1) * ty) * u[None, :]
+    return d / np.linalg.norm(d, axis=1, keepdims=True)
+
+
+def fibonacci_sphere(count: int) -> np.ndarray:
+    from .probes import fibonacci_sphere as _fib
+
+    return _fib(count)
+
+
+def pvs_rays(pose: CameraPose, params: SelectionParams) -> np.ndarray:
+    parts = []
+    if params.raster_cols > 0 and params.raster_rows > 0:
+        parts.append(frustum_directions(pose, params.raster_cols, params.raster_rows))
+    if params.sphere_rays > 0:
+        parts.append(fibonacci_sphere(params.sphere_rays))
+    return np.concatenate(parts) if parts else np.zeros((0, 3))
+
+
+def cage_probes(points, volume) -> np.ndarray:
+    """The 8 corner probe ids of the cell enclosing each point (clamped);
+    host helper for small point sets -- the GPU PVS kernel does the same per
+    hit point."""
+    p = np.atleast_2d(np.asarray(points, dtype=np.float64))
+    dims = np.asarray(volume.dims)
+    rel = (p - np.asarray(volume.origin)) / np.asarray(volume.spacing)
+    low = np.clip(np.floor(rel).astype(np.int64), 0, np.maximum(dims - 2, 0))
+    nx, ny, _ = volume.dims
+    out = np.empty((len(p), 8), dtype=np.int64)
+    col = 0
+    for dk in (0, 1):
+        for dj in (0, 1):
+            for di in (0, 1):
+                ijk = np.minimum(low + np.array([di, dj, dk]), dims - 1)
+                out[:, col] = ijk[:, 0] + nx * (ijk[:, 1] + ny * ijk[:, 2])
+                col += 1
+    return out
+
+
+def probes_for_point(point, volume) -> set:
+    return set(int(p) for p in cage_probes(np.asarray(point), volume)[0])
+
+
+_PVS_SCENES: dict = {}
+
+
+def _pvs_scene(scene, device):
+    """DeviceScene + float64 vertex table for a scene (cached per object)."""
+    from .scene import DeviceScene, Scene
+
+    key = (id(scene), str(device))
+    hit = _PVS_SCENES.get(key)
+    if hit is not None and hit[0] is scene:
+        return hit[1], hit[2]
+    if isinstance(scene, DeviceScene):
+        ds = scene
+        verts = ds.scene.vertices
+    else:
+        if not isinstance(scene, Scene):  # the reference's SceneGeometry
+            boxes = getattr(scene, "boxes", np.zeros((0, 2, 3)))
+            if len(boxes):
+                raise ValueError("the GPU PVS supports triangle scenes; triangulate boxes")
+            tris = np.asarray(scene.triangles, dtype=np.float64).reshape(-1, 3, 3)
+            n = len(tris)
+            scene = Scene(tris, np.zeros((n, 3), np.float32), np.zeros((n, 3), np.float32))
+        ds = scene.device(device)
+        verts = scene.vertices
+    v64 = torch.from_numpy(np.ascontiguousarray(verts, dtype=np.float64)).to(device)
+    _PVS_SCENES[key] = (scene, ds, v64)
+    return ds, v64
+
+
+def pvs_probes_device(pose: CameraPose, scene, volume, params: SelectionParams, rays=None,
+                      *, bits=None, ids=None, count=None):
+    """Stream-ordered PVS: returns (active-masked bitmap, ids, count) on the device."""
+    dev = D.device_of()
+    if rays is None:
+        rays = pvs_rays(pose, params)
+    rays = np.ascontiguousarray(np.asarray(rays, dtype=np.float64).reshape(-1, 3))
+    ds, v64 = _pvs_scene(scene, dev)
+    n = volume.probe_count
+    if bits is None:
+        bits = torch.empty((n + 31) // 32, dtype=torch.int32, device=dev)
+    if ids is None:
+        ids = torch.empty(n, dtype=torch.int64, device=dev)
+    if count is None:
+        count = torch.empty(1, dtype=torch.int64, device=dev)
+    d_rays = torch.from_numpy(rays).to(dev) if len(rays) else torch.zeros((1, 3), dtype=torch.float64, device=dev)
+    # camera / volume placement are host scalars of the call (C doubles)
+    cam = np.ascontiguousarray(np.asarray(pose.position, dtype=np.float64).reshape(3))
+    vo = np.ascontiguousarray(np.asarray(volume.origin, dtype=np.float64).reshape(3))
+    vs = np.ascontiguousarray(np.asarray(volume.spacing, dtype=np.float64).reshape(3))
+    ws = D.Workspace.get(N.lib().ps_pvs_workspace_bytes(n), dev, "pvs")
+    nx, ny, nz = volume.dims
+    N.call("ps_pvs", ds.nodes.data_ptr(), ds.width, ds.tris.data_ptr(), v64.data_ptr(),
+           d_rays.data_ptr(), len(rays), cam.ctypes.data, nx, ny, nz, vo.ctypes.data, vs.ctypes.data,
+           volume.active_device(dev).data_ptr(), bits.data_ptr(), ids.data_ptr(), count.data_ptr(),
+           ws.data_ptr(), ws.numel(), D.stream_ptr(dev))
+    return bits, ids, count
+
+
+def pvs_probes(pose: CameraPose, scene, volume, params: SelectionParams, rays=None) -> np.ndarray:
+    """Active probes that could shade any point visible from the camera
+    (selection.py:384-407); ascending int64 ids."""
+    _, ids, count = pvs_probes_device(pose, scene, volume, params, rays)
+    return D.to_numpy(ids[: int(count.item())])

@@ -368,7 +368,53 @@ def gen_geometry():
     save("geometry", **arrays)
 
 
+def gen_pvs():
+    """pvs_probes on triangle scenes (selection.py:384-407) with the frustum +
+    fibonacci ray set, plus cage_probes on random points."""
+    sys.path.insert(0, str(OUT.parents[1]))
+    from paper_2103_05875_b200 import scene as S  # geometry construction only
+
+    rng = np.random.default_rng(108)
+    arrays = {}
+    scenes = {"cornell": (S.cornell_box(), (8, 8, 8)),
+              "hall": (S.interior_hall(detail=0.12), (16, 8, 16))}
+    case = 0
+    for name, (sc, dims) in scenes.items():
+        vol_ours = S.volume_for(sc, dims)
+        active = rng.random(int(np.prod(dims))) < 0.85
+        vol = rvol.ProbeVolume(dims, vol_ours.origin, vol_ours.spacing, active=active)
+        geo = rsel.SceneGeometry(None, sc.vertices)
+        (x0, y0, z0), (x1, y1, z1) = sc.bounds
+        for k in range(4):
+            pos = np.array([x0, y0, z0]) + rng.random(3) * (np.array([x1, y1, z1]) - np.array([x0, y0, z0]))
+            fwd = rng.normal(size=3)
+            pose = rsel.CameraPose(pos, fwd, fov_y_deg=float(rng.uniform(50, 100)),
+                                   aspect=float(rng.uniform(1.0, 1.8)))
+            params = rsel.SelectionParams(raster_cols=24, raster_rows=16, sphere_rays=300)
+            rays = rsel.pvs_rays(pose, params)
+            ids = rsel.pvs_probes(pose, geo, vol, params)
+            arrays[f"c{case}_tris"] = sc.vertices if k == 0 else np.zeros(0)
+            arrays[f"c{case}_scene"] = np.array(name)
+            arrays[f"c{case}_dims"] = np.array(dims)
+            arrays[f"c{case}_origin"] = np.array(vol.origin)
+            arrays[f"c{case}_spacing"] = np.array(vol.spacing)
+            arrays[f"c{case}_active"] = active
+            arrays[f"c{case}_pose"] = np.concatenate([pose.position, fwd, pose.up,
+                                                      [pose.fov_y_deg, pose.aspect]])
+            arrays[f"c{case}_rays"] = rays
+            arrays[f"c{case}_ids"] = ids.astype(np.int64)
+            case += 1
+    arrays["ncases"] = np.int64(case)
+    # cage_probes on random points incl. outside the volume (clamping)
+    vol = rvol.ProbeVolume((5, 4, 3), (0.5, -1.0, 2.0), (0.7, 1.1, 0.9))
+    pts = rng.uniform(-3, 8, size=(500, 3))
+    arrays["cage_points"] = pts
+    arrays["cage_ids"] = rsel.cage_probes(pts, vol)
+    save("pvs", **{k: v for k, v in arrays.items() if not (k.endswith("_tris") and v.size == 0)})
+
+
 if __name__ == "__main__":
+    gen_pvs()
     gen_pack()
     gen_guard()
     gen_detect()
