@@ -210,6 +210,7 @@ def run_ours(args, rank, world, local):
     base = args.warmup + 2 * args.steps + 1
     stages = server.stage_times(3, base, frame_lights)
     launches_per_step, kernel_names = server.count_launches(base + 3, frame_lights)
+    encode = server.encode_times() if world == 1 else {}
 
     if rank != 0:
         if world > 1:
@@ -276,6 +277,8 @@ def run_ours(args, rank, world, local):
                 "d2h_bytes_per_step": e2e["d2h_bytes_per_step"],
                 "path": "ProbeStreamServer.tick via the C ABI; per-frame ray table + lights "
                         "H2D from pinned host memory, index entries + counts + SKIP maps D2H"},
+        "encode_lpf1": {"note": "§8(f)1 GPU LPF1 encoder (bit-exact with codec.encode_frame) on "
+                                "this frame's planes; not inside the step", **encode},
         "gpu_launches": launches_per_step * args.steps,
         "gpu_launches_per_step": launches_per_step,
         "kernels": kernel_names,

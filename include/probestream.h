@@ -94,6 +94,19 @@ int ps_pack_delta(int kind, const void *texels, int64_t h, int64_t w, int64_t ro
                   void *planes_cur, const void *planes_prev, void *residual,
                   uint8_t *skip, void *stream);
 
+/* LPF1 frame encoding (codec.py:335-366), bit-exact: planes (3, h, w) of
+ * elem_bytes (2 colour, 1 visibility) elements; reference == NULL encodes a
+ * key frame (left-neighbour intra prediction), else a P-frame against the
+ * reference planes (SKIP / DELTA / RAW blocks).  Writes header + payload +
+ * CRC32 into `out` (capacity from ps_encode_frame_capacity) and the frame
+ * length into the device scalar *frame_len. */
+int64_t ps_encode_frame_capacity(int64_t h, int64_t w, int elem_bytes);
+size_t ps_encode_workspace_bytes(int64_t h, int64_t w, int elem_bytes);
+int ps_encode_frame(int elem_bytes, const void *planes, const void *reference, int64_t h,
+                    int64_t w, uint32_t stream_id, uint32_t frame_seq, uint8_t *out,
+                    int64_t out_capacity, int64_t *frame_len, void *workspace,
+                    size_t workspace_bytes, void *stream);
+
 /* ---------------------------------------------------------------------------
  * Stage (3): change detection and compaction (selection.py:284-323).
  * ------------------------------------------------------------------------- */

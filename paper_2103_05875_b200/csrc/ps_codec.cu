@@ -1,0 +1,514 @@
+// §8(f) row 1: bit-exact LPF1 frame encoding on the GPU (codec.py:76-201,
+// 207-292, 335-366; varint.py:16-84).
+//
+// The reference encodes 16x16 blocks one by one in Python (2.5 s / 12.8 s per
+// colour / visibility I-frame at 32x16x32).  Here every block is one warp:
+//
+//   size pass   SKIP test against the reference block (P-frames); otherwise
+//               the raw byte stream and, when a predictor exists (reference
+//               block, or the left neighbour in a key frame), the zig-zag
+//               LEB128 residual stream are built in shared memory and their
+//               zero-run-length encodings are sized with warp scans; DELTA
+//               wins only if strictly shorter (ties go to RAW, codec.py:283).
+//   scan        exclusive prefix sum of the block sizes (payload offsets).
+//   emit pass   the chosen stream is rebuilt and written at its offset:
+//               mode byte, LEB128 length, tokens -- literal bytes land at
+//               offsets given by per-segment prefix sums, so stores from a
+//               warp are contiguous.
+//   container   LPF1 header (<4sBIIHHBBI), then CRC32 of header+payload in
+//               4 KB chunks combined with GF(2) polynomial shifts (the zlib
+//               crc32_combine algorithm), appended little-endian.
+//
+// Entropy tokens (codec.py:76-103): a maximal zero run of >= 2 bytes becomes
+// uvarint(len << 1 | 1); every other stretch is a literal segment
+// uvarint(len << 1) + bytes.  A zero byte belongs to such a run iff a
+// neighbouring byte is also zero.
+#include <cub/device/device_scan.cuh>
+#include <cuda_runtime.h>
+
+#include "ps_common.cuh"
+
+namespace ps {
+namespace {
+
+constexpr int WARPS = 4;           // warps (blocks) per CTA
+constexpr int MAXS = 768;          // max stream bytes per block (256 x 3-byte varints)
+constexpr int HDR = 23;            // LPF1 header bytes
+constexpr uint32_t CRC_POLY = 0xEDB88320u;
+constexpr int CRC_CHUNK = 4096;
+
+struct WarpScratch {
+    uint8_t s[MAXS];               // stream bytes
+    uint8_t e[MAXS];               // zero byte inside a run of >= 2
+    uint16_t seg[MAXS];            // segment index of each byte
+    uint16_t start[MAXS + 1];      // segment start positions (+ sentinel n)
+    uint16_t off[MAXS + 1];        // segment output offsets
+};
+
+__device__ __forceinline__ int vlen(uint32_t v) { return v < 128u ? 1 : (v < 16384u ? 2 : (v < 2097152u ? 3 : 4)); }
+
+__device__ __forceinline__ int put_varint(uint8_t *dst, uint32_t v) {
+    int k = 0;
+    while (true) {
+        const uint32_t b = v & 0x7Fu;
+        v >>= 7;
+        if (v) {
+            dst[k++] = uint8_t(b | 0x80u);
+        } else {
+            dst[k++] = uint8_t(b);
+            return k;
+        }
+    }
+}
+
+// warp-wide exclusive scan of v with a running carry; returns exclusive prefix
+__device__ __forceinline__ uint32_t warp_excl(uint32_t v, uint32_t &carry, int lane) {
+    uint32_t inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+    }
+    const uint32_t ex = carry + inc - v;
+    carry += __shfl_sync(0xffffffffu, inc, 31);
+    return ex;
+}
+
+// Zero-run-length encoding of ws.s[0..n) by one warp.  Returns the encoded
+// length; writes the tokens to `out` when it is non-null.
+__device__ int warp_entropy(WarpScratch &ws, int n, uint8_t *out, int lane) {
+    if (n == 0) return 0;
+    // pass 1: run-eligible zeros, segment starts and indices
+    uint32_t kcarry = 0;
+    int e_last = 0;  // e of the previous tile's last byte
+    for (int t0 = 0; t0 < n; t0 += 32) {
+        const int i = t0 + lane;
+        const bool valid = i < n;
+        const bool z = valid && ws.s[i] == 0;
+        const bool zp = valid && i > 0 && ws.s[i - 1] == 0;
+        const bool zn = valid && i + 1 < n && ws.s[i + 1] == 0;
+        const int e = (z && (zp || zn)) ? 1 : 0;
+        int ep = __shfl_up_sync(0xffffffffu, e, 1);
+        if (lane == 0) ep = e_last;
+        const bool st = valid && (i == 0 || e != ep);
+        const unsigned m = __ballot_sync(0xffffffffu, st);
+        const unsigned lt = (1u << lane) - 1u;
+        if (valid) {
+            ws.e[i] = uint8_t(e);
+            ws.seg[i] = uint16_t(kcarry + __popc(m & (lt | (1u << lane))) - 1);
+            if (st) ws.start[kcarry + __popc(m & lt)] = uint16_t(i);
+        }
+        kcarry += __popc(m);
+        e_last = __shfl_sync(0xffffffffu, e, 31);
+    }
+    const int K = int(kcarry);
+    if (lane == 0) ws.start[K] = uint16_t(n);
+    __syncwarp();
+    // pass 2: segment sizes and output offsets
+    uint32_t ocarry = 0;
+    for (int k0 = 0; k0 < K; k0 += 32) {
+        const int k = k0 + lane;
+        uint32_t sz = 0;
+        if (k < K) {
+            const uint32_t L = uint32_t(ws.start[k + 1] - ws.start[k]);
+            sz = ws.e[ws.start[k]] ? uint32_t(vlen((L << 1) | 1u)) : uint32_t(vlen(L << 1)) + L;
+        }
+        const uint32_t ex = warp_excl(sz, ocarry, lane);
+        if (k < K) ws.off[k] = uint16_t(ex);
+    }
+    const int total = int(ocarry);
+    if (!out) return total;
+    __syncwarp();
+    // pass 3: token headers
+    for (int k = lane; k < K; k += 32) {
+        const uint32_t L = uint32_t(ws.start[k + 1] - ws.start[k]);
+        const bool zr = ws.e[ws.start[k]] != 0;
+        put_varint(out + ws.off[k], zr ? ((L << 1) | 1u) : (L << 1));
+    }
+    // pass 4: literal bytes
+    for (int i = lane; i < n; i += 32) {
+        if (ws.e[i]) continue;
+        const int k = ws.seg[i];
+        const uint32_t L = uint32_t(ws.start[k + 1] - ws.start[k]);
+        out[ws.off[k] + vlen(L << 1) + (i - ws.start[k])] = ws.s[i];
+    }
+    return total;
+}
+
+struct EncArgs {
+    const uint8_t *cur;
+    const uint8_t *ref;  // null: key frame
+    int eb;              // element bytes (2 colour, 1 visibility)
+    int h, w, nby, nbx;
+    int64_t nblocks;
+    uint32_t *sizes;     // bytes of each block in the payload
+    uint32_t *lens;      // entropy payload length (non-SKIP)
+    uint8_t *modes;
+    const uint64_t *offsets;
+    uint8_t *out;        // frame buffer (header at 0, payload at HDR)
+};
+
+__device__ __forceinline__ uint32_t load_elem(const uint8_t *plane, int w, int y, int x, int eb) {
+    const int64_t idx = int64_t(y) * w + x;
+    return eb == 2 ? uint32_t(reinterpret_cast<const uint16_t *>(plane)[idx]) : uint32_t(plane[idx]);
+}
+
+// builds the RAW (mode 2) or residual (mode 1) stream of block b into ws.s
+__device__ int build_stream(const EncArgs &a, WarpScratch &ws, int mode, int pl, int y0, int x0,
+                            int bh, int bw, bool intra, int lane) {
+    const int64_t psz = int64_t(a.h) * a.w * a.eb;
+    const uint8_t *cur = a.cur + pl * psz;
+    const int m = bh * bw;
+    if (mode == 2) {
+        for (int j = lane; j < m; j += 32) {
+            const uint32_t v = load_elem(cur, a.w, y0 + j / bw, x0 + j % bw, a.eb);
+            ws.s[j * a.eb] = uint8_t(v);
+            if (a.eb == 2) ws.s[j * 2 + 1] = uint8_t(v >> 8);
+        }
+        __syncwarp();
+        return m * a.eb;
+    }
+    const uint8_t *pred = intra ? cur : a.ref + pl * psz;
+    const int px = intra ? x0 - 16 : x0;
+    uint32_t carry = 0;
+    for (int j0 = 0; j0 < m; j0 += 32) {
+        const int j = j0 + lane;
+        uint32_t z = 0;
+        int c = 0;
+        if (j < m) {
+            const int y = y0 + j / bw, xo = j % bw;
+            const uint32_t cv = load_elem(cur, a.w, y, x0 + xo, a.eb);
+            const uint32_t pv = load_elem(pred, a.w, y, px + xo, a.eb);
+            int32_t r;
+            if (a.eb == 2) r = int32_t(int16_t(uint16_t(cv - pv)));
+            else r = int32_t(int8_t(uint8_t(cv - pv)));
+            z = (uint32_t(r) << 1) ^ uint32_t(r >> 31);  // zig-zag
+            c = vlen(z);
+        }
+        const uint32_t pos = warp_excl(uint32_t(c), carry, lane);
+        if (j < m) put_varint(ws.s + pos, z);
+    }
+    __syncwarp();
+    return int(carry);
+}
+
+__device__ __forceinline__ void block_coords(const EncArgs &a, int64_t b, int &pl, int &y0, int &x0,
+                                             int &bh, int &bw) {
+    const int64_t per = int64_t(a.nby) * a.nbx;
+    pl = int(b / per);
+    const int64_t r = b - pl * per;
+    const int by = int(r / a.nbx), bx = int(r - int64_t(by) * a.nbx);
+    y0 = by * 16;
+    x0 = bx * 16;
+    bh = min(16, a.h - y0);
+    bw = min(16, a.w - x0);
+}
+
+__global__ void __launch_bounds__(WARPS * 32) encode_size_kernel(EncArgs a) {
+    __shared__ WarpScratch scratch[WARPS];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    WarpScratch &ws = scratch[wid];
+    for (int64_t b = int64_t(blockIdx.x) * WARPS + wid; b < a.nblocks; b += int64_t(gridDim.x) * WARPS) {
+        int pl, y0, x0, bh, bw;
+        block_coords(a, b, pl, y0, x0, bh, bw);
+        const int64_t psz = int64_t(a.h) * a.w * a.eb;
+        bool has_pred = false, intra = false;
+        if (a.ref) {
+            // SKIP iff bit-identical to the reference block (codec.py:264-272)
+            bool diff = false;
+            for (int j = lane; j < bh * bw; j += 32) {
+                const int y = y0 + j / bw, x = x0 + j % bw;
+                diff |= load_elem(a.cur + pl * psz, a.w, y, x, a.eb) !=
+                        load_elem(a.ref + pl * psz, a.w, y, x, a.eb);
+            }
+            if (!__any_sync(0xffffffffu, diff)) {
+                if (lane == 0) {
+                    a.sizes[b] = 1;
+                    a.modes[b] = 0;
+                    a.lens[b] = 0;
+                }
+                continue;
+            }
+            has_pred = true;
+        } else if (x0 >= 16) {
+            has_pred = intra = true;
+        }
+        int n = build_stream(a, ws, 2, pl, y0, x0, bh, bw, intra, lane);
+        const int raw_len = warp_entropy(ws, n, nullptr, lane);
+        __syncwarp();
+        int mode = 2, len = raw_len;
+        if (has_pred) {
+            n = build_stream(a, ws, 1, pl, y0, x0, bh, bw, intra, lane);
+            const int delta_len = warp_entropy(ws, n, nullptr, lane);
+            __syncwarp();
+            if (delta_len < raw_len) {
+                mode = 1;
+                len = delta_len;
+            }
+        }
+        if (lane == 0) {
+            a.sizes[b] = uint32_t(1 + vlen(uint32_t(len)) + len);
+            a.modes[b] = uint8_t(mode);
+            a.lens[b] = uint32_t(len);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(WARPS * 32) encode_emit_kernel(EncArgs a) {
+    __shared__ WarpScratch scratch[WARPS];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    WarpScratch &ws = scratch[wid];
+    for (int64_t b = int64_t(blockIdx.x) * WARPS + wid; b < a.nblocks; b += int64_t(gridDim.x) * WARPS) {
+        uint8_t *dst = a.out + HDR + a.offsets[b];
+        const int mode = a.modes[b];
+        if (mode == 0) {
+            if (lane == 0) dst[0] = 0;
+            continue;
+        }
+        int pl, y0, x0, bh, bw;
+        block_coords(a, b, pl, y0, x0, bh, bw);
+        const bool intra = a.ref == nullptr;
+        const int n = build_stream(a, ws, mode, pl, y0, x0, bh, bw, intra, lane);
+        const uint32_t len = a.lens[b];
+        int hl = 1;
+        if (lane == 0) dst[0] = uint8_t(mode);
+        hl += vlen(len);
+        if (lane == 0) put_varint(dst + 1, len);
+        warp_entropy(ws, n, dst + hl, lane);
+        __syncwarp();
+    }
+}
+
+// ---- container + CRC32 ----------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t multmodp(uint32_t a, uint32_t b) {
+    uint32_t m = 1u << 31, p = 0;
+    while (true) {
+        if (a & m) {
+            p ^= b;
+            if ((a & (m - 1)) == 0) break;
+        }
+        m >>= 1;
+        b = (b & 1) ? (b >> 1) ^ CRC_POLY : b >> 1;
+    }
+    return p;
+}
+
+__global__ void header_kernel(uint8_t *out, const uint64_t *offsets, const uint32_t *sizes,
+                              int64_t nblocks, int key, uint32_t stream_id, uint32_t seq, int w,
+                              int h, int bits, uint64_t *frame_len) {
+    const uint64_t payload = offsets[nblocks - 1] + sizes[nblocks - 1];
+    uint8_t hdr[HDR] = {'L', 'P', 'F', '1'};
+    hdr[4] = uint8_t(key ? 1 : 0);
+    for (int k = 0; k < 4; ++k) {
+        hdr[5 + k] = uint8_t(stream_id >> (8 * k));
+        hdr[9 + k] = uint8_t(seq >> (8 * k));
+        hdr[19 + k] = uint8_t(uint32_t(payload) >> (8 * k));
+    }
+    hdr[13] = uint8_t(w);
+    hdr[14] = uint8_t(w >> 8);
+    hdr[15] = uint8_t(h);
+    hdr[16] = uint8_t(h >> 8);
+    hdr[17] = 3;
+    hdr[18] = uint8_t(bits);
+    for (int k = 0; k < HDR; ++k) out[k] = hdr[k];
+    *frame_len = HDR + payload + 4;
+}
+
+// CRC32 of 4 KB chunks, one thread per chunk: 16-byte loads, slicing-by-4
+__global__ void __launch_bounds__(128) crc_chunk_kernel(const uint8_t *data, const uint64_t *frame_len,
+                                                       uint32_t *crcs, int64_t max_chunks) {
+    __shared__ uint32_t T[4][256];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+        uint32_t c = uint32_t(i);
+        for (int k = 0; k < 8; ++k) c = (c & 1) ? CRC_POLY ^ (c >> 1) : c >> 1;
+        T[0][i] = c;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+        uint32_t c = T[0][i];
+        for (int k = 1; k < 4; ++k) {
+            c = (c >> 8) ^ T[0][c & 0xFFu];
+            T[k][i] = c;
+        }
+    }
+    __syncthreads();
+    const uint64_t len = *frame_len - 4;  // CRC covers header + payload
+    const int64_t chunks = int64_t((len + CRC_CHUNK - 1) / CRC_CHUNK);
+    for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < chunks && c < max_chunks;
+         c += int64_t(gridDim.x) * blockDim.x) {
+        const uint64_t b0 = uint64_t(c) * CRC_CHUNK;
+        const uint64_t b1 = b0 + CRC_CHUNK < len ? b0 + CRC_CHUNK : len;
+        uint32_t crc = 0xFFFFFFFFu;
+        uint64_t i = b0;
+        const uint4 *v = reinterpret_cast<const uint4 *>(data + b0);  // chunk starts are 16-B aligned
+        for (; i + 16 <= b1; i += 16, ++v) {
+            const uint4 q = __ldg(v);
+            const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                crc ^= w4[k];
+                crc = T[3][crc & 0xFFu] ^ T[2][(crc >> 8) & 0xFFu] ^ T[1][(crc >> 16) & 0xFFu] ^
+                      T[0][crc >> 24];
+            }
+        }
+        for (; i < b1; ++i) crc = T[0][(crc ^ data[i]) & 0xFFu] ^ (crc >> 8);
+        crcs[c] = crc ^ 0xFFFFFFFFu;
+    }
+}
+
+// x^(8n) mod P from a table X8[k] = x^(8 * 2^k)
+__device__ __forceinline__ uint32_t x8n_table(const uint32_t *X8, uint64_t n) {
+    uint32_t p = 1u << 31;
+    for (int k = 0; n; ++k, n >>= 1)
+        if (n & 1) p = multmodp(X8[k], p);
+    return p;
+}
+
+// one CTA: 1024 threads fold contiguous runs of equal 4 KB chunks with a
+// constant shift, then a 10-level tree combines the 1024 partial CRCs
+// (crc(A|B) = crc(A) * x^(8|B|) ^ crc(B), the zlib crc32_combine rule)
+__global__ void __launch_bounds__(1024) crc_combine_kernel(uint8_t *out, const uint64_t *frame_len,
+                                                          const uint32_t *crcs) {
+    __shared__ uint32_t X8[48];
+    __shared__ uint32_t part[1024];
+    __shared__ uint64_t plen[1024];
+    if (threadIdx.x == 0) {
+        uint32_t x = 1u << 23;  // x^8
+        for (int k = 0; k < 48; ++k) {
+            X8[k] = x;
+            x = multmodp(x, x);
+        }
+    }
+    __syncthreads();
+    const uint64_t len = *frame_len - 4;
+    const int64_t chunks = int64_t((len + CRC_CHUNK - 1) / CRC_CHUNK);
+    const int64_t per = (chunks + 1023) / 1024;
+    const int64_t c0 = threadIdx.x * per, c1 = c0 + per < chunks ? c0 + per : chunks;
+    const uint32_t shift_full = X8[12];  // x^(8 * 4096)
+    uint32_t crc = 0;
+    uint64_t bytes = 0;
+    for (int64_t c = c0; c < c1; ++c) {
+        const uint64_t clen = (c == chunks - 1) ? len - uint64_t(c) * CRC_CHUNK : CRC_CHUNK;
+        const uint32_t sh = (clen == CRC_CHUNK) ? shift_full : x8n_table(X8, clen);
+        crc = (bytes ? multmodp(sh, crc) : 0u) ^ crcs[c];
+        bytes += clen;
+    }
+    part[threadIdx.x] = crc;
+    plen[threadIdx.x] = bytes;
+    __syncthreads();
+    for (int stride = 1; stride < 1024; stride <<= 1) {
+        const int t = threadIdx.x;
+        if ((t % (2 * stride)) == 0 && plen[t + stride]) {
+            const uint64_t rl = plen[t + stride];
+            part[t] = (plen[t] ? multmodp(x8n_table(X8, rl), part[t]) : 0u) ^ part[t + stride];
+            plen[t] += rl;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const uint32_t acc = part[0];
+        for (int k = 0; k < 4; ++k) out[len + k] = uint8_t(acc >> (8 * k));
+    }
+}
+
+struct EncWs {
+    uint32_t *sizes, *lens, *crcs;
+    uint8_t *modes;
+    uint64_t *offsets, *frame_len;
+    void *scan_tmp;
+    size_t scan_bytes;
+    int64_t max_chunks;
+    size_t total;
+};
+
+EncWs carve_enc(void *ws, size_t bytes, int64_t nblocks, int64_t capacity) {
+    Carver c(ws, bytes);
+    EncWs w;
+    w.sizes = c.take<uint32_t>(size_t(nblocks));
+    w.lens = c.take<uint32_t>(size_t(nblocks));
+    w.modes = c.take<uint8_t>(size_t(nblocks));
+    w.offsets = c.take<uint64_t>(size_t(nblocks));
+    w.frame_len = c.take<uint64_t>(1);
+    w.max_chunks = ceil_div(capacity, CRC_CHUNK);
+    w.crcs = c.take<uint32_t>(size_t(w.max_chunks));
+    w.scan_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, w.scan_bytes, (const uint32_t *)nullptr,
+                                  (uint64_t *)nullptr, int(nblocks));
+    w.scan_tmp = c.take<char>(w.scan_bytes);
+    c.take<char>(1);
+    w.total = c.off;
+    if (ws) c.check();
+    return w;
+}
+
+int64_t frame_capacity(int64_t h, int64_t w, int eb) {
+    const int64_t nb = 3 * ceil_div(h, 16) * ceil_div(w, 16);
+    return HDR + 4 + nb * (1 + 3 + 2 * 256 * eb + 8);
+}
+
+}  // namespace
+}  // namespace ps
+
+using namespace ps;
+
+extern "C" {
+
+int64_t ps_encode_frame_capacity(int64_t h, int64_t w, int elem_bytes) {
+    return frame_capacity(h, w, elem_bytes);
+}
+
+size_t ps_encode_workspace_bytes(int64_t h, int64_t w, int elem_bytes) {
+    const int64_t nb = std::max<int64_t>(3 * ceil_div(h, 16) * ceil_div(w, 16), 1);
+    return carve_enc(nullptr, 0, nb, frame_capacity(h, w, elem_bytes)).total + 256;
+}
+
+int ps_encode_frame(int elem_bytes, const void *planes, const void *reference, int64_t h,
+                    int64_t w, uint32_t stream_id, uint32_t frame_seq, uint8_t *out,
+                    int64_t out_capacity, int64_t *frame_len, void *workspace,
+                    size_t workspace_bytes, void *stream) {
+    PS_ABI_BEGIN
+    if (elem_bytes != 1 && elem_bytes != 2) fail(PS_ERR_VALUE, "element bytes must be 1 or 2");
+    if (h < 1 || w < 1 || h > 65535 || w > 65535) fail(PS_ERR_VALUE, "plane dims must be in [1, 65535]");
+    if (out_capacity < frame_capacity(h, w, elem_bytes)) fail(PS_ERR_VALUE, "output buffer too small");
+    const int64_t nb = 3 * ceil_div(h, 16) * ceil_div(w, 16);
+    if (workspace_bytes < ps_encode_workspace_bytes(h, w, elem_bytes))
+        fail(PS_ERR_WORKSPACE, "encode workspace too small");
+    EncWs ws = carve_enc(workspace, workspace_bytes, nb, frame_capacity(h, w, elem_bytes));
+    auto s = as_stream(stream);
+    EncArgs a;
+    a.cur = static_cast<const uint8_t *>(planes);
+    a.ref = static_cast<const uint8_t *>(reference);
+    a.eb = elem_bytes;
+    a.h = int(h);
+    a.w = int(w);
+    a.nby = int(ceil_div(h, 16));
+    a.nbx = int(ceil_div(w, 16));
+    a.nblocks = nb;
+    a.sizes = ws.sizes;
+    a.lens = ws.lens;
+    a.modes = ws.modes;
+    a.offsets = ws.offsets;
+    a.out = out;
+    const unsigned grid = unsigned(std::min<int64_t>(ceil_div(nb, WARPS), int64_t(sm_count()) * 64));
+    encode_size_kernel<<<grid, WARPS * 32, 0, s>>>(a);
+    check_launch("encode_size_kernel");
+    size_t tmp = ws.scan_bytes;
+    check_cuda(cub::DeviceScan::ExclusiveSum(ws.scan_tmp, tmp, ws.sizes, ws.offsets, int(nb), s),
+               "cub ExclusiveSum");
+    encode_emit_kernel<<<grid, WARPS * 32, 0, s>>>(a);
+    check_launch("encode_emit_kernel");
+    header_kernel<<<1, 1, 0, s>>>(out, ws.offsets, ws.sizes, nb, reference == nullptr, stream_id,
+                                   frame_seq, int(w), int(h), elem_bytes * 8, ws.frame_len);
+    check_launch("header_kernel");
+    const unsigned cgrid = unsigned(std::max<int64_t>(1, std::min<int64_t>(ceil_div(ws.max_chunks, 128), 4096)));
+    crc_chunk_kernel<<<cgrid, 128, 0, s>>>(out, ws.frame_len, ws.crcs, ws.max_chunks);
+    check_launch("crc_chunk_kernel");
+    crc_combine_kernel<<<1, 1024, 0, s>>>(out, ws.frame_len, ws.crcs);
+    check_launch("crc_combine_kernel");
+    check_cuda(cudaMemcpyAsync(frame_len, ws.frame_len, sizeof(int64_t), cudaMemcpyDeviceToDevice, s),
+               "copy frame length");
+    PS_ABI_END
+}
+
+}  // extern "C"

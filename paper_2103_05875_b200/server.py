@@ -42,6 +42,8 @@ class KindOutput:
     entries: torch.Tensor      # (slot_count, 2) int64 (slot, probe), first entry_count valid
     entry_count: torch.Tensor  # (1,) int64
     key: bool                  # key frame (no temporal reference)
+    frame: torch.Tensor | None = None      # LPF1 wire frame (encode=True), first frame_len bytes
+    frame_len: torch.Tensor | None = None  # (1,) int64
 
 
 class KindStream:
@@ -49,8 +51,10 @@ class KindStream:
 
     def __init__(self, kind: AtlasKind, volume: ProbeVolume, device, slot_count=None,
                  slots_per_row=None, threshold: float = 0.0, gop_length: int = DEFAULT_GOP,
-                 budget=None, probes_per_row=None):
+                 budget=None, probes_per_row=None, encode: bool = False, stream_id: int = 0):
         self.kind = kind
+        self.encode = encode
+        self.stream_id = stream_id
         self.volume = volume
         self.device = device
         n = volume.probe_count
@@ -112,9 +116,16 @@ class KindStream:
         pack_delta(self.update_texels, self.kind, prev, planes_out=cur, residual=self.residual,
                    skip=self.skip)
         self._mark(f"{tag}.pack_delta", 1)
+        frame = frame_len = None
+        if self.encode:  # §8(f)1: LPF1 bitstream, bit-exact with codec.encode_frame
+            from .codec import encode_frame_device
+
+            self._mark(f"{tag}.encode", 0)
+            frame, frame_len = encode_frame_device(cur, prev, self.stream_id, self.frame_count)
+            self._mark(f"{tag}.encode", 1)
         self._cur = 1 - self._cur
         self.frame_count += 1
-        return KindOutput(cur, self.residual, self.skip, entries, count, key)
+        return KindOutput(cur, self.residual, self.skip, entries, count, key, frame, frame_len)
 
 
 class ProbeStreamServer:
@@ -123,7 +134,7 @@ class ProbeStreamServer:
     def __init__(self, volume: ProbeVolume, scene, rays_per_probe: int = 256, device=None,
                  color_threshold: float = 0.0, visibility_threshold: float = 0.0,
                  slot_count=None, budget=None, gop_length: int = DEFAULT_GOP,
-                 overlap: bool = True, **probe_kwargs):
+                 overlap: bool = True, encode: bool = False, **probe_kwargs):
         self.device = torch.device(device) if device is not None else D.device_of()
         self.volume = volume
         # overlap: the colour and visibility chains run on their own streams,
@@ -140,10 +151,11 @@ class ProbeStreamServer:
         ppr = self.updater.color.probes_per_row
         self.color = KindStream(AtlasKind.COLOR, volume, self.device, slot_count,
                                 threshold=color_threshold, gop_length=gop_length, budget=budget,
-                                probes_per_row=ppr)
+                                probes_per_row=ppr, encode=encode, stream_id=1)
         self.visibility = KindStream(AtlasKind.VISIBILITY, volume, self.device, slot_count,
                                      threshold=visibility_threshold, gop_length=gop_length,
-                                     budget=budget, probes_per_row=ppr)
+                                     budget=budget, probes_per_row=ppr, encode=encode,
+                                     stream_id=2)
         self.seq = 0
         self.timers = None
 

@@ -136,3 +136,29 @@ class SlabServer:
 
     def pack_delta_bytes(self) -> dict:
         return self.impl.pack_delta_bytes()
+
+    def encode_times(self, reps: int = 3) -> dict:
+        """§8(f)1 LPF1 encoding of the last frame's planes (key and P-frame),
+        device time per frame and compression ratio; not part of the step."""
+        from .codec import encode_frame_device
+
+        impl = self.impl
+        if not hasattr(impl, "color") or getattr(impl.color, "planes", None) is None:
+            return {}
+        torch.cuda.synchronize(self.device)
+        out = {}
+        for ks in (impl.color, impl.visibility):
+            cur, prev = ks.planes[ks._cur - 1 if ks._cur else 1], ks.planes[ks._cur]
+            raw = cur.numel() * cur.element_size()
+            for tag, ref in (("key", None), ("p", prev)):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                encode_frame_device(cur, ref, 99, 0)  # warm
+                a.record()
+                for _ in range(reps):
+                    _, ln = encode_frame_device(cur, ref, 99, 0)
+                b.record()
+                torch.cuda.synchronize(self.device)
+                n = int(ln.item())
+                out[f"{ks.kind.value}.{tag}"] = {"ms": round(a.elapsed_time(b) / reps, 4),
+                                                 "bytes": n, "ratio": round(raw / n, 3)}
+        return out

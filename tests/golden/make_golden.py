@@ -413,7 +413,50 @@ def gen_pvs():
     save("pvs", **{k: v for k, v in arrays.items() if not (k.endswith("_tris") and v.size == 0)})
 
 
+def gen_codec():
+    """encode_frame byte streams (codec.py:335-366) over short sequences of
+    colour and visibility plane sets: key frames with intra prediction,
+    P-frames with SKIP / DELTA / RAW blocks, clipped edge blocks, zero runs."""
+    rng = np.random.default_rng(109)
+    arrays = {}
+    seqs = 0
+    for kind, dtype, hi, shape in ((rpack.PlaneKind.COLOR_10IN16, np.uint16, 1024, (3, 37, 53)),
+                                   (rpack.PlaneKind.VISIBILITY_BYTES, np.uint8, 256, (3, 45, 70)),
+                                   (rpack.PlaneKind.COLOR_10IN16, np.uint16, 1024, (3, 64, 64)),
+                                   (rpack.PlaneKind.VISIBILITY_BYTES, np.uint8, 256, (3, 16, 16))):
+        enc = rcodec.CodecStreamState(seqs + 1, role="encoder", gop_length=4)
+        # smooth-ish content so DELTA wins somewhere, plus zero areas for runs
+        base = (np.add.outer(np.arange(shape[1]), np.arange(shape[2])) % hi).astype(dtype)
+        cur = np.stack([base, (base // 3).astype(dtype), np.zeros_like(base)])
+        cur[2, : shape[1] // 2] = rng.integers(0, hi, size=(shape[1] // 2, shape[2]), dtype=dtype)
+        frames = []
+        for f in range(6):
+            if f > 0:
+                m = rng.random(shape) < (0.02 if f % 2 else 0.3)
+                cur = cur.copy()
+                cur[m] = ((cur[m].astype(np.int64) + rng.integers(1, 5, size=int(m.sum()))) % hi).astype(dtype)
+                if f == 3:
+                    cur[1, :16, :16] = 0  # zero runs
+            frame = rcodec.encode_frame(rpack.PlaneSet(kind, cur.copy()), enc, force_key=(f == 5))
+            arrays[f"s{seqs}_f{f}_planes"] = cur.copy()
+            arrays[f"s{seqs}_f{f}_bytes"] = np.frombuffer(frame.to_bytes(), np.uint8)
+            arrays[f"s{seqs}_f{f}_key"] = np.int64(frame.key)
+        arrays[f"s{seqs}_frames"] = np.int64(6)
+        arrays[f"s{seqs}_gop"] = np.int64(4)
+        arrays[f"s{seqs}_stream"] = np.int64(seqs + 1)
+        seqs += 1
+    arrays["nseq"] = np.int64(seqs)
+    # entropy coder KATs
+    for i, data in enumerate([b"", b"\x00" * 4096, b"\x01\x00\x02\x00\x03", bytes(range(256)) * 3,
+                              b"\x00\x00\x05" * 100]):
+        arrays[f"ent{i}_in"] = np.frombuffer(data, np.uint8)
+        arrays[f"ent{i}_out"] = np.frombuffer(rcodec.entropy_encode(data), np.uint8)
+    arrays["nent"] = np.int64(5)
+    save("codec", **arrays)
+
+
 if __name__ == "__main__":
+    gen_codec()
     gen_pvs()
     gen_pack()
     gen_guard()
