@@ -107,6 +107,21 @@ int ps_encode_frame(int elem_bytes, const void *planes, const void *reference, i
                     int64_t out_capacity, int64_t *frame_len, void *workspace,
                     size_t workspace_bytes, void *stream);
 
+/* Client side (verifier of the server path): LPF1 decode (codec.py:369-395)
+ * of a frame whose bytes are on the device (`frame` points at the header,
+ * payload_len from the header); reference planes for P-frames, NULL for a
+ * key frame.  Structural errors set bits in *status_dev (1 corrupt frame, 2
+ * malformed entropy stream); nothing is raised from the device. */
+size_t ps_decode_workspace_bytes(int64_t h, int64_t w);
+int ps_decode_frame(int elem_bytes, const uint8_t *frame, int64_t payload_len,
+                    const void *reference, int64_t h, int64_t w, void *planes_out,
+                    uint32_t *status_dev, void *workspace, size_t workspace_bytes, void *stream);
+/* apply_update_entries (packing.py:341-350): slot cores into probe blocks of
+ * `atlas` with the guard band rebuilt. */
+int ps_apply_entries(int kind, const void *update_texels, int64_t update_row_stride,
+                     int64_t slots_per_row, const int64_t *entries, const int64_t *entry_count,
+                     int64_t max_entries, void *atlas, int64_t probes_per_row, void *stream);
+
 /* ---------------------------------------------------------------------------
  * Stage (3): change detection and compaction (selection.py:284-323).
  * ------------------------------------------------------------------------- */

@@ -81,6 +81,9 @@ _SIGNATURES = {
     "ps_encode_workspace_bytes": (_sz, [_i64, _i64, _int]),
     "ps_encode_frame": (_int, [_int, _vp, _vp, _i64, _i64, C.c_uint32, C.c_uint32, _vp, _i64, _vp,
                                _vp, _sz, _vp]),
+    "ps_decode_workspace_bytes": (_sz, [_i64, _i64]),
+    "ps_decode_frame": (_int, [_int, _vp, _i64, _vp, _i64, _i64, _vp, _vp, _vp, _sz, _vp]),
+    "ps_apply_entries": (_int, [_int, _vp, _i64, _i64, _vp, _vp, _i64, _vp, _i64, _vp]),
     "ps_detect_workspace_bytes": (_sz, [_i64]),
     "ps_detect_changed": (_int, [_int, _vp, _vp, _i64, _i64, _i64, _vp, _f64, _int,
                                  _vp, _vp, _vp, _vp, _sz, _vp]),

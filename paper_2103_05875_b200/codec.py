@@ -35,7 +35,23 @@ class CodecError(Exception):
     pass
 
 
+class CorruptFrameError(CodecError):
+    pass
+
+
+class MissingReferenceError(CodecError):
+    pass
+
+
+class SequenceError(CodecError):
+    pass
+
+
 class DimensionMismatchError(CodecError):
+    pass
+
+
+class EntropyDecodeError(CodecError):
     pass
 
 
@@ -172,3 +188,54 @@ def compression_ratio(planes: PlaneSet, frame: EncodedFrame) -> float:
     nbytes = planes.data.numel() * planes.data.element_size() if D.is_tensor(planes.data) \
         else planes.data.nbytes
     return nbytes / frame.encoded_size
+
+
+# --- client side: decode (codec.py:369-395) ------------------------------------------
+
+
+def decode_frame_device(frame: torch.Tensor, payload_len: int, reference: torch.Tensor | None,
+                        h: int, w: int, elem_bytes: int, out: torch.Tensor | None = None):
+    """Decode a frame whose bytes are on the device; returns (planes, status)
+    where status is an int32[1] device word (0 = ok, 1 corrupt, 2 entropy)."""
+    dev = frame.device
+    tdt = torch.uint16 if elem_bytes == 2 else torch.uint8
+    if out is None:
+        out = torch.empty((3, h, w), dtype=tdt, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    ws = torch.empty(N.lib().ps_decode_workspace_bytes(h, w), dtype=torch.uint8, device=dev)
+    ref = reference.contiguous() if reference is not None else None
+    N.call("ps_decode_frame", elem_bytes, frame.data_ptr(), int(payload_len), D.ptr(ref), h, w,
+           out.data_ptr(), status.data_ptr(), ws.data_ptr(), ws.numel(), D.stream_ptr(dev))
+    return out, status
+
+
+def decode_frame(frame: EncodedFrame, state: CodecStreamState) -> PlaneSet:
+    """Decode one frame, verify sequencing, advance the stream state."""
+    if state.role != "decoder":
+        raise CodecError("decode_frame requires a decoder stream state")
+    if not frame.key:
+        if state.reference is None:
+            raise MissingReferenceError(f"P-frame seq {frame.frame_seq} with no prior state")
+        if frame.frame_seq != state.frame_count:
+            raise SequenceError(f"frame seq {frame.frame_seq}, decoder expected {state.frame_count}")
+        if tuple(state.reference.data.shape[1:]) != (frame.height, frame.width):
+            raise DimensionMismatchError("frame dims do not match stream state")
+    eb = frame.element_bits // 8
+    dev = D.device_of()
+    wire = np.frombuffer(frame.to_bytes(), np.uint8)
+    buf = torch.from_numpy(wire.copy()).to(dev)
+    ref = None
+    if not frame.key:
+        rd = state.reference.data
+        ref = rd if D.is_tensor(rd) else torch.from_numpy(np.ascontiguousarray(rd)).to(dev)
+    planes, status = decode_frame_device(buf, len(frame.payload), ref, frame.height, frame.width, eb)
+    st = int(status.item())
+    if st & 1:
+        raise CorruptFrameError("malformed frame payload")
+    if st & 2:
+        raise EntropyDecodeError("malformed entropy-coded block")
+    kind = frame.plane_kind
+    result = PlaneSet(kind, planes)
+    state.reference = PlaneSet(kind, planes.clone())
+    state.frame_count = frame.frame_seq + 1
+    return result

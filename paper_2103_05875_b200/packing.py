@@ -472,9 +472,40 @@ def build_update_atlas(selected, layout: UpdateAtlasLayout, source, update_texel
     return upd, ent
 
 
+def apply_update_entries_device(entries: torch.Tensor, entry_count: torch.Tensor,
+                                update_texels: torch.Tensor, layout: UpdateAtlasLayout,
+                                target) -> None:
+    """Stream-ordered client apply: (slot, probe) int64 entries (first
+    ``entry_count`` valid) from the update atlas into ``target`` (a device
+    ProbeAtlas), guard bands rebuilt on the GPU."""
+    kind = kind_of(target.kind)
+    N.call("ps_apply_entries", kind.native, update_texels.data_ptr(), update_texels.shape[1],
+           layout.slots_per_row, entries.data_ptr(), entry_count.data_ptr(), entries.shape[0],
+           target.texels.data_ptr(), target.probes_per_row, D.stream_ptr(update_texels.device))
+
+
 def apply_update_entries(entries, update_texels, layout: UpdateAtlasLayout, target) -> None:
     """Client-side apply (packing.py:341-350): slot cores into target blocks
-    with rebuilt guard bands.  A verifier for the server path."""
-    for slot, probe in entries:
-        core = layout.slot_region(update_texels, slot)
-        reconstruct_guard_band(core, out=target.probe_block(probe))
+    with rebuilt guard bands (mutates ``target``)."""
+    kind = kind_of(target.kind)
+    tdt = torch.uint32 if kind is AtlasKind.COLOR else torch.uint16
+    npd = np.uint32 if kind is AtlasKind.COLOR else np.uint16
+    dev = D.device_of(update_texels, target.texels)
+    ent = torch.as_tensor(np.asarray(list(entries), dtype=np.int64).reshape(-1, 2), device=dev)
+    cnt = torch.tensor([ent.shape[0]], dtype=torch.int64, device=dev)
+    upd = (update_texels.contiguous() if D.is_tensor(update_texels)
+           else torch.from_numpy(np.ascontiguousarray(update_texels, dtype=npd)).to(dev))
+    on_host = not D.is_tensor(target.texels)
+    dst = (torch.from_numpy(np.ascontiguousarray(target.texels)).to(dev) if on_host
+           else target.texels)
+    if not dst.is_contiguous():
+        raise ValueError("target atlas texels must be contiguous")
+    if ent.shape[0]:
+        if int(ent[:, 1].min()) < 0 or int(ent[:, 1].max()) >= target.probe_count:
+            raise IndexError("entry probe outside the target atlas")
+        if int(ent[:, 0].min()) < 0 or int(ent[:, 0].max()) >= layout.slot_count:
+            raise IndexError("entry slot outside the layout")
+        view = type("A", (), {"kind": kind, "texels": dst, "probes_per_row": target.probes_per_row})
+        apply_update_entries_device(ent, cnt, upd.view(tdt) if upd.dtype != tdt else upd, layout, view)
+    if on_host:
+        target.texels[...] = D.to_numpy(dst)
