@@ -230,6 +230,16 @@ int ps_import_tiles(int kind, const void *payloads, int64_t payload_stride,
                     const int64_t *entry_count, int64_t max_entries, int64_t slots_per_row,
                     void *update_texels, int64_t update_row_stride, void *stream);
 
+/* Probe index buffer (the server module is absent from the
+ * reference): uvarint(count), then per (slot, probe) entry sorted by slot
+ * uvarint(slot - prev_slot) and uvarint(zigzag(probe - prev_probe)), prev
+ * starting at (0, 0).  `out` holds >= 1 + 20 * max_entries bytes; the length
+ * goes to the device scalar *out_len. */
+size_t ps_index_workspace_bytes(int64_t max_entries);
+int ps_encode_index(const int64_t *entries, const int64_t *entry_count, int64_t max_entries,
+                    uint8_t *out, int64_t *out_len, void *workspace, size_t workspace_bytes,
+                    void *stream);
+
 /* Guard-band reconstruct over a whole atlas (packing.py:180-196 applied to
  * every probe block): rewrites each block's border from its core. */
 int ps_reconstruct_guard_bands(int kind, void *atlas, int64_t probe_count,

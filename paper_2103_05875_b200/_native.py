@@ -103,6 +103,8 @@ _SIGNATURES = {
     "ps_build_update": (_int, [_int, _vp, _i64, _i64, _vp, _vp, _i64, _i64, _vp, _i64, _vp,
                                _vp, _i64, _vp]),
     "ps_reconstruct_guard_bands": (_int, [_int, _vp, _i64, _i64, _vp]),
+    "ps_index_workspace_bytes": (_sz, [_i64]),
+    "ps_encode_index": (_int, [_vp, _vp, _i64, _vp, _vp, _vp, _sz, _vp]),
     "ps_export_tiles": (_int, [_int, _vp, _i64, _i64, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp,
                                _i64, _vp]),
     "ps_import_tiles": (_int, [_int, _vp, _i64, _vp, _i32, _vp, _vp, _i64, _i64, _vp, _i64, _vp]),

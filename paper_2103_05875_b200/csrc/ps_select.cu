@@ -4,6 +4,7 @@
 // SPEC.md:341).  Everything is stream-ordered with device-resident counts,
 // so a whole frame needs no host round trip.
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 
 #include "ps_common.cuh"
@@ -276,6 +277,69 @@ __global__ void __launch_bounds__(256)
             const int rr = k / CORE, cc = k % CORE;
             dst[(sy + rr) * dst_w + sx + cc] = srcp[k];
         }
+    }
+}
+
+// probe index buffer: count, then per entry the slot delta
+// and the zig-zag probe delta as LEB128 varints (pass 1: byte counts)
+__device__ __forceinline__ int ib_vlen(uint64_t v) {
+    int n = 1;
+    while (v >= 128) {
+        v >>= 7;
+        ++n;
+    }
+    return n;
+}
+
+__device__ __forceinline__ void ib_deltas(const int64_t *entries, int64_t e, uint64_t &ds,
+                                          uint64_t &dp) {
+    const int64_t ps = e ? entries[2 * (e - 1)] : 0, pp = e ? entries[2 * (e - 1) + 1] : 0;
+    ds = uint64_t(entries[2 * e] - ps);
+    const int64_t d = entries[2 * e + 1] - pp;
+    dp = (uint64_t(d) << 1) ^ uint64_t(d >> 63);
+}
+
+__global__ void index_len_kernel(const int64_t *entries, const int64_t *count, int64_t cap,
+                                 uint32_t *lens) {
+    const int64_t c = *count;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < cap;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        if (e >= c) {
+            lens[e] = 0;
+            continue;
+        }
+        uint64_t ds, dp;
+        ib_deltas(entries, e, ds, dp);
+        lens[e] = uint32_t(ib_vlen(ds) + ib_vlen(dp));
+    }
+}
+
+__device__ __forceinline__ int ib_put(uint8_t *dst, uint64_t v) {
+    int k = 0;
+    while (v >= 128) {
+        dst[k++] = uint8_t(v | 0x80);
+        v >>= 7;
+    }
+    dst[k++] = uint8_t(v);
+    return k;
+}
+
+__global__ void index_write_kernel(const int64_t *entries, const int64_t *count,
+                                   const uint64_t *offsets, const uint32_t *lens, int64_t cap,
+                                   uint8_t *out, int64_t *out_len) {
+    const int64_t c = *count;
+    const int head = ib_vlen(uint64_t(c));
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < c;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        uint64_t ds, dp;
+        ib_deltas(entries, e, ds, dp);
+        uint8_t *d = out + head + offsets[e];
+        d += ib_put(d, ds);
+        ib_put(d, dp);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        ib_put(out, uint64_t(c));
+        *out_len = head + (c ? int64_t(offsets[c - 1] + lens[c - 1]) : 0);
     }
 }
 
@@ -558,6 +622,35 @@ int ps_import_tiles(int kind, const void *payloads, int64_t payload_stride,
                                                  static_cast<uint32_t *>(update_texels),
                                                  update_row_stride);
     check_launch("import_kernel");
+    PS_ABI_END
+}
+
+size_t ps_index_workspace_bytes(int64_t max_entries) {
+    const int64_t n = std::max<int64_t>(max_entries, 1);
+    size_t scan = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, scan, (const uint32_t *)nullptr, (uint64_t *)nullptr, int(n));
+    return size_t(n) * (4 + 8) + scan + 1024;
+}
+
+int ps_encode_index(const int64_t *entries, const int64_t *entry_count, int64_t max_entries,
+                    uint8_t *out, int64_t *out_len, void *workspace, size_t workspace_bytes,
+                    void *stream) {
+    PS_ABI_BEGIN
+    const int64_t n = std::max<int64_t>(max_entries, 1);
+    if (workspace_bytes < ps_index_workspace_bytes(max_entries)) fail(PS_ERR_WORKSPACE, "index workspace");
+    Carver c(workspace, workspace_bytes);
+    uint32_t *lens = c.take<uint32_t>(size_t(n));
+    uint64_t *offsets = c.take<uint64_t>(size_t(n));
+    size_t scan = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, scan, lens, offsets, int(n));
+    void *tmp = c.take<char>(scan);
+    c.check();
+    auto s = as_stream(stream);
+    index_len_kernel<<<grid_for(n), 256, 0, s>>>(entries, entry_count, n, lens);
+    check_launch("index_len_kernel");
+    check_cuda(cub::DeviceScan::ExclusiveSum(tmp, scan, lens, offsets, int(n), s), "index scan");
+    index_write_kernel<<<grid_for(n), 256, 0, s>>>(entries, entry_count, offsets, lens, n, out, out_len);
+    check_launch("index_write_kernel");
     PS_ABI_END
 }
 

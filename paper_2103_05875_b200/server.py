@@ -44,6 +44,8 @@ class KindOutput:
     key: bool                  # key frame (no temporal reference)
     frame: torch.Tensor | None = None      # LPF1 wire frame (encode=True), first frame_len bytes
     frame_len: torch.Tensor | None = None  # (1,) int64
+    index: torch.Tensor | None = None      # probe index buffer (encode=True), first index_len bytes
+    index_len: torch.Tensor | None = None
 
 
 class KindStream:
@@ -116,16 +118,19 @@ class KindStream:
         pack_delta(self.update_texels, self.kind, prev, planes_out=cur, residual=self.residual,
                    skip=self.skip)
         self._mark(f"{tag}.pack_delta", 1)
-        frame = frame_len = None
+        frame = frame_len = index = index_len = None
         if self.encode:  # §8(f)1: LPF1 bitstream, bit-exact with codec.encode_frame
             from .codec import encode_frame_device
+            from .index_buffer import encode_index_device
 
             self._mark(f"{tag}.encode", 0)
             frame, frame_len = encode_frame_device(cur, prev, self.stream_id, self.frame_count)
+            index, index_len = encode_index_device(entries, count)  # §8(f)4
             self._mark(f"{tag}.encode", 1)
         self._cur = 1 - self._cur
         self.frame_count += 1
-        return KindOutput(cur, self.residual, self.skip, entries, count, key, frame, frame_len)
+        return KindOutput(cur, self.residual, self.skip, entries, count, key, frame, frame_len,
+                          index, index_len)
 
 
 class ProbeStreamServer:
