@@ -206,6 +206,9 @@ def run_ours(args, rank, world, local):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
 
+    e2e_enc = server.run_e2e_encoded(args.steps, args.warmup + 2 * args.steps + 40,
+                                     frame_lights) if world == 1 else {}
+
     # ---- per-stage device times + launch count (untimed instrumented frames) ---------
     base = args.warmup + 2 * args.steps + 1
     stages = server.stage_times(3, base, frame_lights)
@@ -279,6 +282,11 @@ def run_ours(args, rank, world, local):
                         "H2D from pinned host memory, index entries + counts + SKIP maps D2H"},
         "encode_lpf1": {"note": "§8(f)1 GPU LPF1 encoder (bit-exact with codec.encode_frame) on "
                                 "this frame's planes; not inside the step", **encode},
+        "e2e_encoded": ({"value": round(n / (e2e_enc["ms_per_step"] / 1e3), 1),
+                         "unit": "probe updates/s", **{k: (round(v, 4) if isinstance(v, float) else v)
+                                                        for k, v in e2e_enc.items()},
+                         "path": "as e2e, plus GPU LPF1 encoding (§8(f)1) + index buffer (§8(f)4) "
+                                 "and D2H of the wire bytes each frame"} if e2e_enc else None),
         "gpu_launches": launches_per_step * args.steps,
         "gpu_launches_per_step": launches_per_step,
         "kernels": kernel_names,

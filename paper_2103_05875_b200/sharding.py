@@ -91,6 +91,47 @@ class SlabServer:
         return {"ms_per_step": start.elapsed_time(end) / steps, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h}
 
+    def run_e2e_encoded(self, steps: int, first_frame: int, lights_for) -> dict:
+        """End to end including §8(f)1/4: every frame is encoded to LPF1 on the
+        device and the wire bytes (frames + index buffers) are read back to
+        pinned host memory -- what a server sends to its client."""
+        impl = self.impl
+        if not hasattr(impl, "color") or not hasattr(impl.color, "encode"):
+            return {}
+        kinds = (impl.color, impl.visibility)
+        for ks in kinds:
+            ks.encode = True
+        try:
+            impl.tick(first_frame, lights_for(first_frame))  # buffers + warm
+            torch.cuda.synchronize(self.device)
+            host = {ks.kind.value: torch.empty(256 << 20, dtype=torch.uint8).pin_memory() for ks in kinds}
+            d2h = 0
+            stream = torch.cuda.current_stream(self.device)
+            start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize(self.device)
+            start.record(stream)
+            for k in range(steps):
+                f = first_frame + 1 + k
+                outs = impl.tick(f, lights_for(f))
+                for ks, o in zip(kinds, outs):
+                    st = self._out_stream(ks.kind.value)
+                    st.synchronize()  # frame / index lengths are needed on the host
+                    n, ni = int(o.frame_len.item()), int(o.index_len.item())
+                    hb = host[ks.kind.value]
+                    with torch.cuda.stream(st):
+                        hb[:n].copy_(o.frame[:n], non_blocking=True)
+                        hb[n:n + ni].copy_(o.index[:ni], non_blocking=True)
+                    d2h += n + ni + 16
+            self.join()
+            end.record(stream)
+            torch.cuda.synchronize(self.device)
+            return {"ms_per_step": start.elapsed_time(end) / steps,
+                    "h2d_bytes_per_step": impl.h2d_bytes_per_frame(),
+                    "d2h_bytes_per_step": d2h // steps}
+        finally:
+            for ks in kinds:
+                ks.encode = False
+
     def stage_times(self, frames: int, first_frame: int, lights_for) -> dict:
         """Per-stage device times, measured with the stages serialised on one
         stream (no overlap) so each interval is that stage alone."""
