@@ -323,6 +323,9 @@ typedef struct ps_trace_params {
     float *records;
     /* scratch: one uint32 work counter (dynamic ray-chunk scheduling) */
     uint32_t *work_counter;
+    /* SMs the persistent trace grid leaves free for concurrent streams (the
+     * previous frame's streaming stages) */
+    int32_t reserve_sms;
     /* optional per-ray debug record ((probe_end - probe_begin) * rays, 8
      * floats: radiance rgb, depth, hit t (inf = miss), prim id (int bits,
      * -1 = miss), shadow mask (int bits, bit l = light l visible), 0);

@@ -61,7 +61,7 @@ class TraceParams(C.Structure):
         ("irradiance", _vp), ("moments", _vp),
         ("color_atlas", _vp), ("vis_atlas", _vp),
         ("probes_per_row_color", _i32), ("probes_per_row_vis", _i32),
-        ("records", _vp), ("work_counter", _vp),
+        ("records", _vp), ("work_counter", _vp), ("reserve_sms", _i32),
         ("ray_records", _vp),
     ]
 

@@ -176,6 +176,41 @@ struct Wide {
     int n;
 };
 
+// IEEE binary16 helpers for the fp16-box BVH4 (round to nearest even, then
+// nudged outward so the half box contains the double box)
+uint16_t f2h_rne(float f) {
+    uint32_t x;
+    std::memcpy(&x, &f, 4);
+    const uint32_t sign = (x >> 16) & 0x8000u;
+    x &= 0x7FFFFFFFu;
+    if (x >= 0x47800000u) return uint16_t(sign | 0x7C00u);  // overflow -> inf
+    if (x < 0x38800000u) {  // subnormal half
+        const float a = std::fabs(f) * 16777216.0f;  // / 2^-24
+        return uint16_t(sign | uint16_t(std::nearbyint(a)));
+    }
+    uint32_t m = x + 0xFFFu + ((x >> 13) & 1u);  // round mantissa to 10 bits, ties to even
+    return uint16_t(sign | ((m - 0x38000000u) >> 13));
+}
+double h2d(uint16_t h) {
+    const int e = (h >> 10) & 0x1F, m = h & 0x3FF;
+    const double s = (h & 0x8000) ? -1.0 : 1.0;
+    if (e == 0) return s * std::ldexp(double(m), -24);
+    if (e == 31) return m ? NAN : s * INFINITY;
+    return s * std::ldexp(double(m | 0x400), e - 25);
+}
+uint16_t h_up(uint16_t h) { return h == 0x8000u ? 1 : ((h & 0x8000u) ? h - 1 : h + 1); }
+uint16_t h_down(uint16_t h) { return h == 0 ? 0x8001u : ((h & 0x8000u) ? h + 1 : h - 1); }
+uint16_t half_down(double x) {
+    uint16_t h = f2h_rne(float(x));
+    while (h2d(h) > x) h = h_down(h);
+    return h;
+}
+uint16_t half_up(double x) {
+    uint16_t h = f2h_rne(float(x));
+    while (h2d(h) < x) h = h_up(h);
+    return h;
+}
+
 }  // namespace
 
 // Shared implementation: binned-SAH binary build, then emission as BVH2
@@ -190,7 +225,10 @@ static int bvh_build_impl(const double *vertices, int64_t tri_count, int leaf_si
         if (tri_count < 1) throw std::invalid_argument("scene needs at least one triangle");
         if (tri_count > (int64_t(1) << 27)) throw std::invalid_argument("too many triangles");
         if (leaf_size < 1 || leaf_size > 7) throw std::invalid_argument("leaf_size in [1, 7]");
-        if (width != 2 && width != 4) throw std::invalid_argument("width must be 2 or 4");
+        // width 5 = BVH4 with fp16 child boxes (64-byte nodes)
+        if (width != 2 && width != 4 && width != 5) throw std::invalid_argument("width must be 2, 4 or 5");
+        const bool half_boxes = width == 5;
+        if (half_boxes) width = 4;
         Builder b;
         b.v = vertices;
         b.leaf_size = leaf_size;
@@ -264,10 +302,31 @@ static int bvh_build_impl(const double *vertices, int64_t tri_count, int leaf_si
             if (b.nodes[id].left >= 0) return wide_of[id];
             return ~int32_t((leaf_slot[id] << 3) | b.nodes[id].count);
         };
-        const int nf = width == 2 ? 16 : 32;
+        const int nf = (width == 2 || half_boxes) ? 16 : 32;
+        if (half_boxes) {
+            // node: [lo_x[4] hi_x[4]] [lo_y[4] hi_y[4]] [lo_z[4] hi_z[4]] as halves, child[4]
+            for (size_t g = 0; g < wide.size(); ++g) {
+                const Wide &w = wide[g];
+                float *nd = nodes_out + 16 * g;
+                std::memset(nd, 0, 64);
+                uint16_t *hb = reinterpret_cast<uint16_t *>(nd);
+                for (int k = 0; k < 4; ++k) {
+                    if (k >= w.n) {
+                        set_int(nd + 12 + k, EMPTY_CHILD);
+                        continue;
+                    }
+                    const Aabb &bx = b.nodes[w.kids[k]].box;
+                    for (int a = 0; a < 3; ++a) {
+                        hb[8 * a + k] = half_down(bx.lo[a]);
+                        hb[8 * a + 4 + k] = half_up(bx.hi[a]);
+                    }
+                    set_int(nd + 12 + k, child_ref(w.kids[k]));
+                }
+            }
+        } else
         for (size_t g = 0; g < wide.size(); ++g) {
             const Wide &w = wide[g];
-            float *nd = nodes_out + nf * g;
+            float *nd = nodes_out + nf * g;  // fp32 boxes
             std::memset(nd, 0, nf * 4);
             for (int k = 0; k < width; ++k) {
                 if (k >= w.n) {  // unused slot

@@ -679,6 +679,13 @@ void launch_trace_ww(const ps_trace_params &p, int sms, cudaStream_t s) {
 
 template <int SHADOW>
 void launch_trace_s(const ps_trace_params &p, int variant, int sms, cudaStream_t s) {
+    if (p.bvh_width == 5) {
+        switch (variant) {
+            case 11: launch_trace_t<SHADOW, 1, 4, 0, 5>(p, sms, s); break;
+            default: launch_trace_t<SHADOW, 1, 1, 0, 5>(p, sms, s); break;
+        }
+        return;
+    }
     if (p.bvh_width == 4) {
         switch (variant) {
             case 0: launch_trace_t<SHADOW, 0, 1, 0, 4>(p, sms, s); break;
@@ -743,7 +750,8 @@ int ps_trace_blend(const ps_trace_params *params, void *stream) {
     if (p.light_count < 0 || p.light_count > 30) fail(PS_ERR_VALUE, "light_count in [0, 30]");
     if (p.probes_per_row_color < 1 || p.probes_per_row_vis < 1) fail(PS_ERR_LAYOUT, "bad atlas layout");
     if (p.shadow_mode < PS_SHADOW_NONE || p.shadow_mode > PS_SHADOW_MAP) fail(PS_ERR_VALUE, "bad shadow_mode");
-    if (p.bvh_width != 2 && p.bvh_width != 4) fail(PS_ERR_VALUE, "bvh_width must be 2 or 4");
+    if (p.bvh_width != 2 && p.bvh_width != 4 && p.bvh_width != 5)
+        fail(PS_ERR_VALUE, "bvh_width must be 2, 4 or 5 (BVH4 with fp16 boxes)");
     if (p.bvh_width == 4 && (p.shadow_mode == PS_SHADOW_RAYS || false)) {
         // any-hit shadow rays use the same templated traversal: fine
     }
@@ -759,7 +767,9 @@ int ps_trace_blend(const ps_trace_params *params, void *stream) {
     if (p.shadow_mode == PS_SHADOW_MAP && p.light_count > 0) {
         const int64_t texels = int64_t(p.light_count) * 6 * p.shadow_map_size * p.shadow_map_size;
         const unsigned blocks = unsigned(std::min<int64_t>(ceil_div(texels, 256), int64_t(sms) * 32));
-        if (p.bvh_width == 4)
+        if (p.bvh_width == 5)
+            shadow_map_kernel<5><<<blocks, 256, 0, s>>>(p);
+        else if (p.bvh_width == 4)
             shadow_map_kernel<4><<<blocks, 256, 0, s>>>(p);
         else
             shadow_map_kernel<2><<<blocks, 256, 0, s>>>(p);
@@ -774,7 +784,8 @@ int ps_trace_blend(const ps_trace_params *params, void *stream) {
             const char *e = getenv("PS_TRACE_VARIANT");
             return e ? atoi(e) : 1;
         }();
-        launch_trace(p, variant, sms, s);
+        const int keep = p.reserve_sms > 0 && p.reserve_sms < sms / 2 ? p.reserve_sms : 0;
+        launch_trace(p, variant, sms - keep, s);
     }
     // pass 2: blend
     const size_t smem = blend_smem_bytes(p.rays_per_probe);

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cuda_fp16.h>
 
 namespace ps {
 namespace trav {
@@ -122,6 +123,45 @@ __device__ __forceinline__ void node4_hits(const float4 *nodes, int node, float 
 // than the current hit are skipped.  Leaves carry their triangle count
 // (~ref = first << 3 | count), so all of a leaf's triangle records are
 // fetched before the first test.  Returns the hit record index (or -1).
+// BVH4 with fp16 child boxes (64-byte nodes, "width" 5): boxes were rounded
+// outward on the host, so the half box contains the float box.
+__device__ __forceinline__ void node4h_hits(const float4 *nodes, int node, float ix, float iy,
+                                            float iz, float oix, float oiy, float oiz, float tmax,
+                                            float d[4], int c[4]) {
+    const uint4 *nd = reinterpret_cast<const uint4 *>(nodes) + 4 * node;
+    const uint4 qx = __ldg(nd + 0), qy = __ldg(nd + 1), qz = __ldg(nd + 2);
+    const int4 ch = __ldg(reinterpret_cast<const int4 *>(nd + 3));
+    float lx[4], hx[4], ly[4], hy[4], lz[4], hz[4];
+    auto unpack = [](uint32_t w, float &a, float &b) {
+        const float2 f = __half22float2(*reinterpret_cast<const __half2 *>(&w));
+        a = f.x;
+        b = f.y;
+    };
+    unpack(qx.x, lx[0], lx[1]); unpack(qx.y, lx[2], lx[3]);
+    unpack(qx.z, hx[0], hx[1]); unpack(qx.w, hx[2], hx[3]);
+    unpack(qy.x, ly[0], ly[1]); unpack(qy.y, ly[2], ly[3]);
+    unpack(qy.z, hy[0], hy[1]); unpack(qy.w, hy[2], hy[3]);
+    unpack(qz.x, lz[0], lz[1]); unpack(qz.y, lz[2], lz[3]);
+    unpack(qz.z, hz[0], hz[1]); unpack(qz.w, hz[2], hz[3]);
+    const int ca[4] = {ch.x, ch.y, ch.z, ch.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const float ax = fmaf(lx[k], ix, -oix), bx = fmaf(hx[k], ix, -oix);
+        const float ay = fmaf(ly[k], iy, -oiy), by = fmaf(hy[k], iy, -oiy);
+        const float az = fmaf(lz[k], iz, -oiz), bz = fmaf(hz[k], iz, -oiz);
+        const float tn = fmaxf(fmaxf(fminf(ax, bx), fminf(ay, by)), fmaxf(fminf(az, bz), 0.0f));
+        const float tf = fminf(fminf(fmaxf(ax, bx), fmaxf(ay, by)), fminf(fmaxf(az, bz), tmax));
+        const bool hit = tn <= tf && ca[k] != EMPTY_CHILD;
+        d[k] = hit ? tn : INFINITY;
+        c[k] = ca[k];
+    }
+    cswap(d[0], c[0], d[1], c[1]);
+    cswap(d[2], c[2], d[3], c[3]);
+    cswap(d[0], c[0], d[2], c[2]);
+    cswap(d[1], c[1], d[3], c[3]);
+    cswap(d[1], c[1], d[2], c[2]);
+}
+
 template <bool ANY_HIT, int LEAFV = 0, int WIDTH = 2>
 __device__ int traverse(const float4 *__restrict__ nodes, const float4 *__restrict__ tris,
                         const Ray &r, float tmax, float &t_best) {
@@ -137,10 +177,13 @@ __device__ int traverse(const float4 *__restrict__ nodes, const float4 *__restri
     int hit_slot = -1;
     t_best = tmax;
     while (true) {
-        if (node >= 0 && WIDTH == 4) {
+        if (node >= 0 && (WIDTH == 4 || WIDTH == 5)) {
             float d[4];
             int c[4];
-            node4_hits(nodes, node, ix, iy, iz, oix, oiy, oiz, t_best, d, c);
+            if (WIDTH == 5)
+                node4h_hits(nodes, node, ix, iy, iz, oix, oiy, oiz, t_best, d, c);
+            else
+                node4_hits(nodes, node, ix, iy, iz, oix, oiy, oiz, t_best, d, c);
             if (d[0] != INFINITY) {
                 if (d[3] != INFINITY) stack[sp++] = make_int2(c[3], __float_as_int(d[3]));
                 if (d[2] != INFINITY) stack[sp++] = make_int2(c[2], __float_as_int(d[2]));

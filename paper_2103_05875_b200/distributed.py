@@ -34,7 +34,7 @@ from .delta import pack_delta, skip_shape
 from .packing import UpdateAtlasLayout, widened_width
 from .probes import ProbeUpdater
 from .selection import detect_changed_device, select_device
-from .server import DEFAULT_GOP, KindOutput
+from .server import DEFAULT_GOP, RESERVE_SMS, KindOutput
 from .volume import AtlasKind, ProbeAtlas
 
 
@@ -170,11 +170,20 @@ class DistributedFrame:
 
     def __init__(self, volume, scene, rays_per_probe, device, rank, world, encoder=0,
                  color_threshold=0.0, visibility_threshold=0.0, slot_count=None, budget=None,
-                 gop_length=DEFAULT_GOP, **probe_kwargs):
+                 gop_length=DEFAULT_GOP, overlap: bool = True, **probe_kwargs):
         self.volume, self.device, self.rank, self.world = volume, device, rank, world
         self.ranges = [slab_range(volume, r, world) for r in range(world)]
+        # overlap: both kind chains (with their NCCL exchanges) run on side
+        # streams concurrently with the next frame's trace, as on one GPU
+        self.overlap = overlap
         self.updater = ProbeUpdater(volume, scene, rays_per_probe=rays_per_probe, device=device,
-                                    probe_range=self.ranges[rank], **probe_kwargs)
+                                    probe_range=self.ranges[rank],
+                                    atlas_buffers=2 if overlap else 1,
+                                    reserve_sms=probe_kwargs.pop("reserve_sms", RESERVE_SMS) if overlap else 0, **probe_kwargs)
+        self.streams = {"color": torch.cuda.Stream(device, priority=-1),
+                        "visibility": torch.cuda.Stream(device, priority=-1)}
+        self._buf_done = [[], []]
+        self._pending = []
         ppr = self.updater.color.probes_per_row
         kw = dict(encoder=encoder, slot_count=slot_count, gop_length=gop_length, budget=budget,
                   probes_per_row=ppr)
@@ -192,6 +201,11 @@ class DistributedFrame:
 
     def tick(self, frame=None, lights=None, pvs_bits=None):
         frame = self.seq if frame is None else frame
+        main = torch.cuda.current_stream(self.device)
+        if self.overlap:
+            buf = self.updater.frames_done % 2
+            for ev in self._buf_done[buf]:
+                main.wait_event(ev)
         if self.timers is not None:
             e = torch.cuda.Event(enable_timing=True)
             e.record()
@@ -201,10 +215,35 @@ class DistributedFrame:
             e = torch.cuda.Event(enable_timing=True)
             e.record()
             self.timers["trace_blend"].append((1, e))
-        out_c = self.color.tick(color, self.seq, pvs_bits)
-        out_v = self.visibility.tick(vis, self.seq, pvs_bits)
+        if not self.overlap:
+            out_c = self.color.tick(color, self.seq, pvs_bits)
+            out_v = self.visibility.tick(vis, self.seq, pvs_bits)
+            self.seq += 1
+            return out_c, out_v
+        traced = torch.cuda.Event()
+        traced.record(main)
+        outs, done = [], []
+        # same program order on every rank: colour's collectives, then visibility's
+        for ks, atlas in ((self.color, color), (self.visibility, vis)):
+            st = self.streams[ks.kind.value]
+            st.wait_event(traced)
+            with torch.cuda.stream(st):
+                outs.append(ks.tick(atlas, self.seq, pvs_bits))
+                ev = torch.cuda.Event()
+                ev.record(st)
+                done.append(ev)
+        self._buf_done[buf] = done
+        self._pending = done
         self.seq += 1
-        return out_c, out_v
+        return tuple(outs)
+
+    def join(self) -> None:
+        main = torch.cuda.current_stream(self.device)
+        for ev in self._pending:
+            main.wait_event(ev)
+
+    def output_stream(self, kind: str):
+        return self.streams[kind] if self.overlap else torch.cuda.current_stream(self.device)
 
     def h2d_bytes_per_frame(self) -> int:
         u = self.updater

@@ -119,7 +119,7 @@ class ProbeUpdater:
                  irradiance_scale: float = 1.0, shadows="map", normal_bias: float | None = None,
                  seed: int = 0, probe_range=None, probes_per_row: int | None = None,
                  device=None, record_rays: bool = False, shadow_map_size: int = 256,
-                 shadow_bias: float = 0.02, atlas_buffers: int = 1):
+                 shadow_bias: float = 0.02, atlas_buffers: int = 1, reserve_sms: int = 0):
         self.volume = volume
         self.device = torch.device(device) if device is not None else D.device_of()
         self.dscene = scene if isinstance(scene, DeviceScene) else scene.device(self.device)
@@ -143,6 +143,7 @@ class ProbeUpdater:
         self.shadows = shadows
         self.shadow_map_size = int(shadow_map_size)
         self.shadow_bias = float(shadow_bias)
+        self.reserve_sms = int(reserve_sms)
         self.normal_bias = float(normal_bias if normal_bias is not None else 1e-3 * diag)
         self.seed = int(seed)
         n = volume.probe_count
@@ -198,6 +199,7 @@ class ProbeUpdater:
         p.shadow_bias = self.shadow_bias
         p.records = self.records.data_ptr()
         p.work_counter = self.work_counter.data_ptr()
+        p.reserve_sms = self.reserve_sms
         p.w_color, p.w_depth, p.inv_wsum = (self.w_color.data_ptr(), self.w_depth.data_ptr(),
                                             self.inv_wsum.data_ptr())
         p.hysteresis = hysteresis

@@ -68,14 +68,23 @@ class Scene:
         m[:, 8:11] = self.face_normals()
         return m
 
-    def device(self, device=None, leaf_size: int = 4, width: int = 4) -> "DeviceScene":
+    def device(self, device=None, leaf_size: int = 4, width: int | None = None) -> "DeviceScene":
+        """BVH layouts: 2 = BVH2, 4 = BVH4 (fp32 boxes), 5 = BVH4 with fp16
+        boxes (64-byte nodes); default from PS_BVH_WIDTH or BVH4."""
+        import os
+
+        if width is None:
+            width = int(os.environ.get("PS_BVH_WIDTH", DEFAULT_BVH_WIDTH))
         return DeviceScene(self, device, leaf_size, width)
+
+
+DEFAULT_BVH_WIDTH = 4
 
 
 class DeviceScene:
     """BVH + triangles + materials + lights resident in HBM (replicated per GPU)."""
 
-    def __init__(self, scene: Scene, device=None, leaf_size: int = 4, width: int = 4):
+    def __init__(self, scene: Scene, device=None, leaf_size: int = 4, width: int = DEFAULT_BVH_WIDTH):
         import torch
 
         from . import _device as D
@@ -88,15 +97,15 @@ class DeviceScene:
         vp = verts.ctypes.data_as(ctypes.c_void_p)
         N.check(N.lib().ps_bvh_build_wide(vp, len(verts), leaf_size, self.width,
                                           ctypes.byref(sizes), None, None), "ps_bvh_build_wide")
-        nodes = np.zeros(sizes.node_count * (16 if self.width == 2 else 32), np.float32)
+        nodes = np.zeros(sizes.node_count * (32 if self.width == 4 else 16), np.float32)
         tris = np.zeros(sizes.tri_slots * 12, np.float32)
         N.check(N.lib().ps_bvh_build_wide(vp, len(verts), leaf_size, self.width,
                                           ctypes.byref(sizes),
                                           nodes.ctypes.data_as(ctypes.c_void_p),
                                           tris.ctypes.data_as(ctypes.c_void_p)),
                 "ps_bvh_build_wide")
-        # traversal stack: at most width - 1 pushes per level (64 entries)
-        if (self.width - 1) * sizes.max_depth + 1 > 64:
+        # traversal stack: at most (children - 1) pushes per level (64 entries)
+        if (min(self.width, 4) - 1) * sizes.max_depth + 1 > 64:
             raise ValueError(f"BVH depth {sizes.max_depth} exceeds the traversal stack (64)")
         self.sizes = (int(sizes.node_count), int(sizes.tri_slots), int(sizes.max_depth))
         self.host_nodes, self.host_tris = nodes, tris

@@ -32,6 +32,9 @@ from .selection import detect_changed_device, select_device
 from .volume import AtlasKind, ProbeAtlas, ProbeVolume
 
 DEFAULT_GOP = 30  # codec.py:46
+# SMs the persistent tracer leaves to the previous frame's stage chains when
+# they overlap (high-priority side streams); tunable via PS_RESERVE_SMS
+RESERVE_SMS = int(__import__("os").environ.get("PS_RESERVE_SMS", "8"))
 
 
 @dataclass
@@ -148,9 +151,10 @@ class ProbeStreamServer:
         self.overlap = overlap
         self.updater = ProbeUpdater(volume, scene, rays_per_probe=rays_per_probe,
                                     device=self.device, atlas_buffers=2 if overlap else 1,
+                                    reserve_sms=probe_kwargs.pop("reserve_sms", RESERVE_SMS) if overlap else 0,
                                     **probe_kwargs)
-        self.streams = ({"color": torch.cuda.Stream(self.device),
-                         "visibility": torch.cuda.Stream(self.device)} if overlap else None)
+        self.streams = ({"color": torch.cuda.Stream(self.device, priority=-1),
+                         "visibility": torch.cuda.Stream(self.device, priority=-1)} if overlap else None)
         self._buf_done = [[], []]   # events: stages finished reading atlas buffer k
         self._pending = []          # events of the last frame's stage chains
         ppr = self.updater.color.probes_per_row
