@@ -166,7 +166,7 @@ def run_ours(args, rank, world, local):
     n = vol.probe_count
     server = SlabServer(vol, sc, rays_per_probe=rays, device=dev, rank=rank, world=world,
                         irradiance_scale=4.0 if scene_name == "hall" else 2.0,
-                        shadows=args.shadows)
+                        shadows=args.shadows, graphs=not args.eager)
     stream = torch.cuda.current_stream(dev)
 
     def barrier():
@@ -251,6 +251,7 @@ def run_ours(args, rank, world, local):
             if hasattr(server.impl, "updater") else "map",
             "l2": "per-frame working set (atlases, float state, planes) > 126 MB L2; no flush",
             "parallelism": f"z-slab x{world}",
+            "launch": "eager" if args.eager else "CUDA graphs (trace+blend, one chain per kind)",
         },
         "grays_per_s": round(rays_total / (ms_max / 1e3) / 1e9, 4),
         "frame_hz": round(1e3 / ms_max, 2),
@@ -370,6 +371,8 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--shadows", default="map", choices=["map", "rays", "none"])
+    ap.add_argument("--eager", action="store_true",
+                    help="issue every kernel from the host instead of replaying CUDA graphs")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warmup raised to 3 (timing rules)")

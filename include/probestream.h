@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define PS_ABI_VERSION 1
+#define PS_ABI_VERSION 2
 
 /* status codes */
 #define PS_OK 0
@@ -89,10 +89,11 @@ int ps_temporal_delta(int elem_bytes, const void *cur, const void *prev, int64_t
 
 /* Fused pack + temporal delta over a whole update atlas: writes planes_cur,
  * residual (vs planes_prev) and skip in one pass.  planes_prev == NULL is a
- * key frame (residual untouched, skip 0). */
+ * key frame (residual untouched, skip 0); so is a non-zero *key_dev (optional
+ * device flag, lets a captured CUDA graph decide per replay). */
 int ps_pack_delta(int kind, const void *texels, int64_t h, int64_t w, int64_t row_stride,
                   void *planes_cur, const void *planes_prev, void *residual,
-                  uint8_t *skip, void *stream);
+                  uint8_t *skip, const int32_t *key_dev, void *stream);
 
 /* LPF1 frame encoding (codec.py:335-366), bit-exact: planes (3, h, w) of
  * elem_bytes (2 colour, 1 visibility) elements; reference == NULL encodes a
@@ -204,12 +205,14 @@ int ps_assign_slots(const int64_t *selected, const int64_t *n_dev, int64_t n_hos
 /* Copy each entry's stripped core (block[1:-1,1:-1]) into its slot region of
  * update_texels (packing.py:335-337).  Optional commit: when
  * last_sent != NULL also copies the full block into last_sent and stamps
- * last_sent_seq[p] = current_seq.  Work is bounded by *entry_count (device). */
+ * last_sent_seq[p] = current_seq (or *current_seq_dev when non-NULL).  Work
+ * is bounded by *entry_count (device). */
 int ps_build_update(int kind, const void *source, int64_t probe_count,
                     int64_t probes_per_row, const int64_t *entries,
                     const int64_t *entry_count, int64_t max_entries, int64_t slots_per_row,
                     void *update_texels, int64_t update_row_stride, void *last_sent,
-                    int64_t *last_sent_seq, int64_t current_seq, void *stream);
+                    int64_t *last_sent_seq, int64_t current_seq,
+                    const int64_t *current_seq_dev, void *stream);
 
 /* Slab-sharded build (multi-GPU, single encoder stream).  Every rank runs
  * the same selection + slot assignment; a rank then
@@ -224,11 +227,20 @@ int ps_build_update(int kind, const void *source, int64_t probe_count,
 int ps_export_tiles(int kind, const void *source, int64_t probe_count, int64_t probes_per_row,
                     const int64_t *entries, const int64_t *entry_count, int64_t max_entries,
                     int64_t probe_begin, int64_t probe_end, void *payload, void *last_sent,
-                    int64_t *last_sent_seq, int64_t current_seq, void *stream);
+                    int64_t *last_sent_seq, int64_t current_seq,
+                    const int64_t *current_seq_dev, void *stream);
 int ps_import_tiles(int kind, const void *payloads, int64_t payload_stride,
                     const int64_t *rank_begin, int32_t world, const int64_t *entries,
                     const int64_t *entry_count, int64_t max_entries, int64_t slots_per_row,
                     void *update_texels, int64_t update_row_stride, void *stream);
+
+/* Device-resident per-stream frame counters for CUDA-graph replay (no host
+ * scalar is baked into a captured frame).  state = int64[3]
+ * {seq, frame_count, key}; one launch advances seq and frame_count by one and
+ * sets key = (frame_count % gop_length == 0), the codec's key-frame rule
+ * (codec.py:348).  Pass &state[0] as current_seq_dev and (int32_t *)&state[2]
+ * as key_dev. */
+int ps_frame_advance(int64_t *state, int64_t gop_length, void *stream);
 
 /* Probe index buffer (the server module is absent from the
  * reference): uvarint(count), then per (slot, probe) entry sorted by slot

@@ -16,7 +16,7 @@ from pathlib import Path
 from .errors import LayoutMismatchError, NativeLibraryError, SlotOverflowError
 
 LIB_PATH = Path(os.environ.get("PROBESTREAM_LIB", Path(__file__).resolve().parent / "libprobestream.so"))
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 PS_OK = 0
 PS_ERR_VALUE = -1
@@ -76,7 +76,7 @@ _SIGNATURES = {
     "ps_unpack_color": (_int, [_vp, _i64, _i64, _vp, _vp]),
     "ps_unpack_visibility": (_int, [_vp, _i64, _i64, _vp, _vp]),
     "ps_temporal_delta": (_int, [_int, _vp, _vp, _i64, _i64, _vp, _vp, _vp]),
-    "ps_pack_delta": (_int, [_int, _vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp]),
+    "ps_pack_delta": (_int, [_int, _vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "ps_encode_frame_capacity": (_i64, [_i64, _i64, _int]),
     "ps_encode_workspace_bytes": (_sz, [_i64, _i64, _int]),
     "ps_encode_frame": (_int, [_int, _vp, _vp, _i64, _i64, C.c_uint32, C.c_uint32, _vp, _i64, _vp,
@@ -101,12 +101,13 @@ _SIGNATURES = {
     "ps_assign_slots": (_int, [_vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp,
                                _vp, _vp, _sz, _vp]),
     "ps_build_update": (_int, [_int, _vp, _i64, _i64, _vp, _vp, _i64, _i64, _vp, _i64, _vp,
-                               _vp, _i64, _vp]),
+                               _vp, _i64, _vp, _vp]),
     "ps_reconstruct_guard_bands": (_int, [_int, _vp, _i64, _i64, _vp]),
     "ps_index_workspace_bytes": (_sz, [_i64]),
     "ps_encode_index": (_int, [_vp, _vp, _i64, _vp, _vp, _vp, _sz, _vp]),
+    "ps_frame_advance": (_int, [_vp, _i64, _vp]),
     "ps_export_tiles": (_int, [_int, _vp, _i64, _i64, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp,
-                               _i64, _vp]),
+                               _i64, _vp, _vp]),
     "ps_import_tiles": (_int, [_int, _vp, _i64, _vp, _i32, _vp, _vp, _i64, _i64, _vp, _i64, _vp]),
     "ps_bvh_build": (_int, [_vp, _i64, _int, C.POINTER(BvhSizes), _vp, _vp]),
     "ps_bvh_build_wide": (_int, [_vp, _i64, _int, _int, C.POINTER(BvhSizes), _vp, _vp]),

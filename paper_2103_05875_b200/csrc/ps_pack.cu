@@ -54,6 +54,7 @@ struct PackArgs {
     uint8_t *skip;          // (3, ceil(h/16), nseg) or nullptr
     int vec_in;             // texel rows 16-byte aligned
     int vec_out;            // plane rows 16-byte aligned
+    const int32_t *key_dev; // optional device flag: non-zero = key frame (ignore prev)
 };
 
 // Loads the 16-element segment `seg` of row `r` for all three planes into
@@ -169,6 +170,7 @@ __device__ __forceinline__ void store_plane_words(uint8_t *base, int64_t x0_b, i
 template <int KIND>
 __global__ void __launch_bounds__(TILE_X *TILE_Y)
     pack_delta_kernel(PackArgs a) {
+    if (a.key_dev && *a.key_dev) a.prev = nullptr;  // key frame decided on the device
     constexpr int EB = (KIND == PS_KIND_COLOR) ? 2 : 1;  // element bytes
     constexpr int NB = SEG * EB;                         // bytes per plane segment
     __shared__ uint32_t dirty[3][TILE_X];
@@ -283,7 +285,7 @@ inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 
 
 int launch_pack_delta(int kind, const void *texels, int64_t h, int64_t w, int64_t row_stride,
                       void *planes_cur, const void *planes_prev, void *residual,
-                      uint8_t *skip, cudaStream_t stream) {
+                      uint8_t *skip, cudaStream_t stream, const int32_t *key_dev = nullptr) {
     if (h < 0 || w < 0) fail(PS_ERR_VALUE, "negative texel region shape");
     if (row_stride < w) fail(PS_ERR_VALUE, "row stride smaller than width");
     if (kind != PS_KIND_COLOR && kind != PS_KIND_VISIBILITY) fail(PS_ERR_VALUE, "bad kind");
@@ -298,6 +300,7 @@ int launch_pack_delta(int kind, const void *texels, int64_t h, int64_t w, int64_
     a.prev = static_cast<const uint8_t *>(planes_prev);
     a.residual = static_cast<uint8_t *>(residual);
     a.skip = skip;
+    a.key_dev = key_dev;
     a.vec_in = aligned16(texels) && (a.row_stride_b % 16 == 0);
     const int eb = (kind == PS_KIND_COLOR) ? 2 : 1;
     a.vec_out = aligned16(planes_cur) && (!planes_prev || aligned16(planes_prev)) &&
@@ -353,10 +356,10 @@ int ps_pack_visibility(const uint16_t *texels, int64_t h, int64_t w, int64_t row
 
 int ps_pack_delta(int kind, const void *texels, int64_t h, int64_t w, int64_t row_stride,
                   void *planes_cur, const void *planes_prev, void *residual, uint8_t *skip,
-                  void *stream) {
+                  const int32_t *key_dev, void *stream) {
     PS_ABI_BEGIN
     launch_pack_delta(kind, texels, h, w, row_stride, planes_cur, planes_prev, residual, skip,
-                      as_stream(stream));
+                      as_stream(stream), key_dev);
     PS_ABI_END
 }
 

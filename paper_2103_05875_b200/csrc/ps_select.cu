@@ -201,10 +201,11 @@ __global__ void __launch_bounds__(256)
     build_kernel(const uint32_t *src, int64_t src_w, int64_t ppr, const int64_t *entries,
                  const int64_t *entry_count, int64_t slots_per_row, uint32_t *dst,
                  int64_t dst_w, uint32_t *last_sent, int64_t *last_sent_seq,
-                 int64_t current_seq) {
+                 int64_t current_seq, const int64_t *seq_dev) {
     constexpr int CORE = SIDE - 2;
     constexpr int WORDS = SIDE * SIDE;
     const int64_t count = *entry_count;
+    if (seq_dev) current_seq = *seq_dev;
     const int lane = threadIdx.x & 31;
     const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
@@ -230,10 +231,11 @@ __global__ void __launch_bounds__(256)
     export_kernel(const uint32_t *src, int64_t src_w, int64_t ppr, const int64_t *entries,
                   const int64_t *entry_count, int64_t probe_begin, int64_t probe_end,
                   uint32_t *payload, uint32_t *last_sent, int64_t *last_sent_seq,
-                  int64_t current_seq) {
+                  int64_t current_seq, const int64_t *seq_dev) {
     constexpr int CORE = SIDE - 2;
     constexpr int WORDS = SIDE * SIDE;
     const int64_t count = *entry_count;
+    if (seq_dev) current_seq = *seq_dev;
     const int lane = threadIdx.x & 31;
     const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
@@ -454,6 +456,15 @@ AssignWs carve_assign(void *ws, size_t bytes, int64_t n, int64_t slots) {
 }  // namespace
 }  // namespace ps
 
+namespace ps {
+__global__ void frame_advance_kernel(int64_t *state, int64_t gop) {
+    const int64_t fc = state[1] + 1;
+    state[0] += 1;
+    state[1] = fc;
+    state[2] = (fc % gop == 0) ? 1 : 0;
+}
+}  // namespace ps
+
 using namespace ps;
 
 extern "C" {
@@ -548,7 +559,7 @@ int ps_build_update(int kind, const void *source, int64_t probe_count, int64_t p
                     const int64_t *entries, const int64_t *entry_count, int64_t max_entries,
                     int64_t slots_per_row, void *update_texels, int64_t update_row_stride,
                     void *last_sent, int64_t *last_sent_seq, int64_t current_seq,
-                    void *stream) {
+                    const int64_t *current_seq_dev, void *stream) {
     PS_ABI_BEGIN
     if (kind != PS_KIND_COLOR && kind != PS_KIND_VISIBILITY) fail(PS_ERR_VALUE, "bad kind");
     if (probes_per_row < 1 || slots_per_row < 1) fail(PS_ERR_VALUE, "bad layout");
@@ -562,12 +573,12 @@ int ps_build_update(int kind, const void *source, int64_t probe_count, int64_t p
         build_kernel<10><<<blocks, 256, 0, s>>>(
             static_cast<const uint32_t *>(source), src_w, probes_per_row, entries, entry_count,
             slots_per_row, static_cast<uint32_t *>(update_texels), update_row_stride,
-            static_cast<uint32_t *>(last_sent), last_sent_seq, current_seq);
+            static_cast<uint32_t *>(last_sent), last_sent_seq, current_seq, current_seq_dev);
     else
         build_kernel<18><<<blocks, 256, 0, s>>>(
             static_cast<const uint32_t *>(source), src_w, probes_per_row, entries, entry_count,
             slots_per_row, static_cast<uint32_t *>(update_texels), update_row_stride,
-            static_cast<uint32_t *>(last_sent), last_sent_seq, current_seq);
+            static_cast<uint32_t *>(last_sent), last_sent_seq, current_seq, current_seq_dev);
     check_launch("build_kernel");
     PS_ABI_END
 }
@@ -575,7 +586,8 @@ int ps_build_update(int kind, const void *source, int64_t probe_count, int64_t p
 int ps_export_tiles(int kind, const void *source, int64_t probe_count, int64_t probes_per_row,
                     const int64_t *entries, const int64_t *entry_count, int64_t max_entries,
                     int64_t probe_begin, int64_t probe_end, void *payload, void *last_sent,
-                    int64_t *last_sent_seq, int64_t current_seq, void *stream) {
+                    int64_t *last_sent_seq, int64_t current_seq,
+                    const int64_t *current_seq_dev, void *stream) {
     PS_ABI_BEGIN
     if (kind != PS_KIND_COLOR && kind != PS_KIND_VISIBILITY) fail(PS_ERR_VALUE, "bad kind");
     if (probe_begin < 0 || probe_end > probe_count || probe_begin > probe_end)
@@ -588,13 +600,22 @@ int ps_export_tiles(int kind, const void *source, int64_t probe_count, int64_t p
         export_kernel<10><<<blocks, 256, 0, s>>>(
             static_cast<const uint32_t *>(source), probes_per_row * 10, probes_per_row, entries,
             entry_count, probe_begin, probe_end, static_cast<uint32_t *>(payload),
-            static_cast<uint32_t *>(last_sent), last_sent_seq, current_seq);
+            static_cast<uint32_t *>(last_sent), last_sent_seq, current_seq, current_seq_dev);
     else
         export_kernel<18><<<blocks, 256, 0, s>>>(
             static_cast<const uint32_t *>(source), probes_per_row * 18, probes_per_row, entries,
             entry_count, probe_begin, probe_end, static_cast<uint32_t *>(payload),
-            static_cast<uint32_t *>(last_sent), last_sent_seq, current_seq);
+            static_cast<uint32_t *>(last_sent), last_sent_seq, current_seq, current_seq_dev);
     check_launch("export_kernel");
+    PS_ABI_END
+}
+
+int ps_frame_advance(int64_t *state, int64_t gop_length, void *stream) {
+    PS_ABI_BEGIN
+    if (!state) fail(PS_ERR_VALUE, "state must not be NULL");
+    if (gop_length < 1) fail(PS_ERR_VALUE, "gop_length must be >= 1");
+    frame_advance_kernel<<<1, 1, 0, as_stream(stream)>>>(state, gop_length);
+    check_launch("frame_advance_kernel");
     PS_ABI_END
 }
 

@@ -55,7 +55,7 @@ def temporal_delta(cur: PlaneSet, prev: PlaneSet | None):
 
 def pack_delta(texels: torch.Tensor, kind, planes_prev: torch.Tensor | None, *,
                planes_out: torch.Tensor | None = None, residual: torch.Tensor | None = None,
-               skip: torch.Tensor | None = None):
+               skip: torch.Tensor | None = None, key_dev: torch.Tensor | None = None):
     """Pack a (contiguous) update atlas and diff it against the previous planes
     in one kernel.  Returns (planes, residual, skip) CUDA tensors."""
     k = kind_of(kind)
@@ -73,5 +73,6 @@ def pack_delta(texels: torch.Tensor, kind, planes_prev: torch.Tensor | None, *,
     if skip is None:
         skip = torch.empty(skip_shape(pshape[1], pshape[2]), dtype=torch.uint8, device=dev)
     N.call("ps_pack_delta", k.native, texels.data_ptr(), h, w, w, planes_out.data_ptr(),
-           D.ptr(planes_prev), residual.data_ptr(), skip.data_ptr(), D.stream_ptr(dev))
+           D.ptr(planes_prev), residual.data_ptr(), skip.data_ptr(), D.ptr(key_dev),
+           D.stream_ptr(dev))
     return planes_out, residual, skip

@@ -109,6 +109,13 @@ class DistKindStream:
             self.payloads = None
             self.payload = torch.zeros(self.slab_max * core, dtype=torch.int32, device=device)
         self.timers = None
+        self.graphs = None
+        self.frame_state = torch.zeros(3, dtype=torch.int64, device=device)
+        self._state_synced = False
+
+    def enable_graphs(self, on: bool = True) -> None:
+        self.graphs = {} if on else None
+        self._state_synced = False
 
     def _mark(self, name, stage):
         if self.timers is not None:
@@ -117,52 +124,105 @@ class DistKindStream:
             self.timers.setdefault(name, []).append((stage, e))
 
     def tick(self, rendered: ProbeAtlas, seq: int, pvs_bits=None):
-        tag = self.kind.value
-        dev = self.device
-        self._mark(f"{tag}.detect", 0)
-        detect_changed_device(rendered, self.last_sent, self.volume, self.threshold,
-                              bits=self.bits, with_ids=False, workspace_slot=f"detect.{tag}",
-                              probe_range=(self.begin, self.end))
-        self._mark(f"{tag}.detect", 1)
-        self._mark(f"{tag}.exchange_bits", 0)
-        exchange_bitmap(self.bits)
-        self._mark(f"{tag}.exchange_bits", 1)
-        self._mark(f"{tag}.select", 0)
-        select_device(self.bits, pvs_bits, self.volume, self.last_sent_seq, seq, self.budget,
-                      out_ids=self.sel_ids, out_count=self.sel_count,
-                      workspace_slot=f"select.{tag}")
-        self._mark(f"{tag}.select", 1)
-        self._mark(f"{tag}.assign", 0)
-        entries, count = self.layout.assign_device(self.sel_ids, self.sel_count)
-        self._mark(f"{tag}.assign", 1)
-        self._mark(f"{tag}.export", 0)
-        N.call("ps_export_tiles", self.kind.native, rendered.texels.data_ptr(),
-               self.volume.probe_count, rendered.probes_per_row, entries.data_ptr(),
-               count.data_ptr(), self.layout.slot_count, self.begin, self.end,
-               self.payload.data_ptr(), self.last_sent.texels.data_ptr(),
-               self.last_sent_seq.data_ptr(), int(seq), D.stream_ptr(dev))
-        self._mark(f"{tag}.export", 1)
-        self._mark(f"{tag}.gather", 0)
-        gather_payloads(self.payload, self.payloads, self.rank, self.world, self.encoder)
-        self._mark(f"{tag}.gather", 1)
+        graphed = self.graphs is not None and self.frame_count >= 1 and self.timers is None
+        if not graphed:
+            self._state_synced = False
+        elif not self._state_synced:
+            # state holds the previous frame's values; segment A advances it
+            self.frame_state.copy_(torch.tensor([seq - 1, self.frame_count - 1, 0],
+                                                dtype=torch.int64))
+            self._state_synced = True
+        return self._issue(rendered, seq, pvs_bits, graphed)
+
+    def _segment(self, name: str, key: tuple, fn, graphed: bool) -> None:
+        """Run ``fn`` eagerly, or replay its captured graph.  The NCCL
+        exchanges stay outside the graphs (issued eagerly between segments),
+        so a frame is 3 graph launches + 2 collectives per kind."""
+        if not graphed:
+            fn()
+            return
+        k = (name,) + key
+        g = self.graphs.get(k)
+        if g is None:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, capture_error_mode="thread_local"):
+                fn()
+            self.graphs[k] = g
+        g.replay()
+
+    def _finish(self):
         key = self.frame_count % self.gop_length == 0
         self.frame_count += 1
         if not self.is_encoder:
             return None
-        self._mark(f"{tag}.import", 0)
-        N.call("ps_import_tiles", self.kind.native, self.payloads.data_ptr(), self.slab_max,
-               self.rank_begin.data_ptr(), self.world, entries.data_ptr(), count.data_ptr(),
-               self.layout.slot_count, self.layout.slots_per_row, self.update_texels.data_ptr(),
-               self.update_texels.shape[1], D.stream_ptr(dev))
-        self._mark(f"{tag}.import", 1)
-        prev = None if key else self.planes[self._cur]
         cur = self.planes[1 - self._cur]
-        self._mark(f"{tag}.pack_delta", 0)
-        pack_delta(self.update_texels, self.kind, prev, planes_out=cur, residual=self.residual,
-                   skip=self.skip)
-        self._mark(f"{tag}.pack_delta", 1)
         self._cur = 1 - self._cur
-        return KindOutput(cur, self.residual, self.skip, entries, count, key)
+        return KindOutput(cur, self.residual, self.skip, self.layout._entries,
+                          self.layout._entry_count, key)
+
+    def _issue(self, rendered: ProbeAtlas, seq: int, pvs_bits, graphed: bool):
+        tag = self.kind.value
+        dev = self.device
+        seq_dev = self.frame_state[0:1] if graphed else None
+        key_dev = self.frame_state[2:3].view(torch.int32)[:1] if graphed else None
+        gkey = (rendered.texels.data_ptr(), getattr(self, "_cur", 0), D.ptr(pvs_bits))
+
+        def seg_detect():
+            if graphed:
+                N.call("ps_frame_advance", self.frame_state.data_ptr(), self.gop_length,
+                       D.stream_ptr(dev))
+            self._mark(f"{tag}.detect", 0)
+            detect_changed_device(rendered, self.last_sent, self.volume, self.threshold,
+                                  bits=self.bits, with_ids=False, workspace_slot=f"detect.{tag}",
+                                  probe_range=(self.begin, self.end))
+            self._mark(f"{tag}.detect", 1)
+
+        def seg_select_export():
+            self._mark(f"{tag}.select", 0)
+            select_device(self.bits, pvs_bits, self.volume, self.last_sent_seq, seq, self.budget,
+                          out_ids=self.sel_ids, out_count=self.sel_count,
+                          workspace_slot=f"select.{tag}")
+            self._mark(f"{tag}.select", 1)
+            self._mark(f"{tag}.assign", 0)
+            entries, count = self.layout.assign_device(self.sel_ids, self.sel_count)
+            self._mark(f"{tag}.assign", 1)
+            self._mark(f"{tag}.export", 0)
+            N.call("ps_export_tiles", self.kind.native, rendered.texels.data_ptr(),
+                   self.volume.probe_count, rendered.probes_per_row, entries.data_ptr(),
+                   count.data_ptr(), self.layout.slot_count, self.begin, self.end,
+                   self.payload.data_ptr(), self.last_sent.texels.data_ptr(),
+                   self.last_sent_seq.data_ptr(), int(seq), D.ptr(seq_dev), D.stream_ptr(dev))
+            self._mark(f"{tag}.export", 1)
+
+        def seg_import_pack():
+            entries, count = self.layout._entries, self.layout._entry_count
+            self._mark(f"{tag}.import", 0)
+            N.call("ps_import_tiles", self.kind.native, self.payloads.data_ptr(), self.slab_max,
+                   self.rank_begin.data_ptr(), self.world, entries.data_ptr(), count.data_ptr(),
+                   self.layout.slot_count, self.layout.slots_per_row,
+                   self.update_texels.data_ptr(), self.update_texels.shape[1],
+                   D.stream_ptr(dev))
+            self._mark(f"{tag}.import", 1)
+            key = self.frame_count % self.gop_length == 0
+            # graphed: the device flag decides key frames per replay
+            prev = self.planes[self._cur] if graphed or not key else None
+            cur = self.planes[1 - self._cur]
+            self._mark(f"{tag}.pack_delta", 0)
+            pack_delta(self.update_texels, self.kind, prev, planes_out=cur,
+                       residual=self.residual, skip=self.skip, key_dev=key_dev)
+            self._mark(f"{tag}.pack_delta", 1)
+
+        self._segment("detect", gkey, seg_detect, graphed)
+        self._mark(f"{tag}.exchange_bits", 0)
+        exchange_bitmap(self.bits)
+        self._mark(f"{tag}.exchange_bits", 1)
+        self._segment("select", gkey, seg_select_export, graphed)
+        self._mark(f"{tag}.gather", 0)
+        gather_payloads(self.payload, self.payloads, self.rank, self.world, self.encoder)
+        self._mark(f"{tag}.gather", 1)
+        if self.is_encoder:
+            self._segment("pack", gkey, seg_import_pack, graphed)
+        return self._finish()
 
 
 class DistributedFrame:
@@ -170,7 +230,8 @@ class DistributedFrame:
 
     def __init__(self, volume, scene, rays_per_probe, device, rank, world, encoder=0,
                  color_threshold=0.0, visibility_threshold=0.0, slot_count=None, budget=None,
-                 gop_length=DEFAULT_GOP, overlap: bool = True, **probe_kwargs):
+                 gop_length=DEFAULT_GOP, overlap: bool = True, graphs: bool = False,
+                 **probe_kwargs):
         self.volume, self.device, self.rank, self.world = volume, device, rank, world
         self.ranges = [slab_range(volume, r, world) for r in range(world)]
         # overlap: both kind chains (with their NCCL exchanges) run on side
@@ -193,6 +254,15 @@ class DistributedFrame:
                                          self.ranges, threshold=visibility_threshold, **kw)
         self.seq = 0
         self.timers = None
+        self.enable_graphs(graphs)
+
+    def enable_graphs(self, on: bool = True) -> None:
+        """Replay each frame as three captured CUDA graphs (trace + blend on
+        the main stream, one stage chain per kind on its side stream) instead
+        of ~130 individual launches; frame 0 always runs eagerly."""
+        self.graphs = bool(on)
+        for part in (self.updater, self.color, self.visibility):
+            part.enable_graphs(on)
 
     def enable_stage_timers(self, on=True):
         self.timers = {} if on else None

@@ -463,7 +463,7 @@ def build_update_atlas(selected, layout: UpdateAtlasLayout, source, update_texel
     layout.raise_pending()
     N.call("ps_build_update", kind.native, src_t.data_ptr(), n, ppr, entries.data_ptr(),
            count.data_ptr(), layout.slot_count, layout.slots_per_row, upd.data_ptr(),
-           shape[1], None, None, 0, D.stream_ptr(dev))
+           shape[1], None, None, 0, None, D.stream_ptr(dev))
     k = int(count.item())
     ent = [tuple(r) for r in entries[:k].cpu().tolist()]
     if out_np is not None:

@@ -39,6 +39,7 @@ even), visibility raw float16 halves; border texels by the guard-band rule
 from __future__ import annotations
 
 import ctypes
+import functools
 import math
 
 import numpy as np
@@ -72,13 +73,20 @@ def _morton2(x: np.ndarray, y: np.ndarray) -> np.ndarray:
     return spread(x) | (spread(y) << np.uint32(1))
 
 
-def base_ray_set(count: int) -> np.ndarray:
-    """fibonacci_sphere(count) reordered by octahedral Morton code (float64)."""
+@functools.lru_cache(maxsize=8)
+def _base_ray_set(count: int) -> np.ndarray:
     fib = fibonacci_sphere(count)
     uv = oct_encode(fib, validate=False)
     q = np.clip((uv * 1024.0).astype(np.int64), 0, 1023)
     order = np.argsort(_morton2(q[:, 0], q[:, 1]), kind="stable")
-    return fib[order]
+    out = fib[order]
+    out.setflags(write=False)
+    return out
+
+
+def base_ray_set(count: int) -> np.ndarray:
+    """fibonacci_sphere(count) reordered by octahedral Morton code (float64)."""
+    return _base_ray_set(int(count)).copy()
 
 
 def frame_rotation(seed: int, frame: int) -> np.ndarray:
@@ -94,7 +102,7 @@ def frame_rotation(seed: int, frame: int) -> np.ndarray:
 
 def frame_ray_directions(count: int, seed: int, frame: int) -> np.ndarray:
     """(count, 4) float32 table [dx dy dz 0] for a frame."""
-    d = base_ray_set(count) @ frame_rotation(seed, frame).T
+    d = _base_ray_set(int(count)) @ frame_rotation(seed, frame).T
     out = np.zeros((count, 4), np.float32)
     out[:, :3] = d
     return out
@@ -176,6 +184,15 @@ class ProbeUpdater:
         self.shadow_maps = (torch.empty((self.dscene.MAX_LIGHTS, 6, S, S), dtype=torch.float32,
                                         device=dev) if self.shadow_mode == N.PS_SHADOW_MAP else None)
         self.frames_done = 0
+        # CUDA-graph replay (enable_graphs): one graph per frame parity; the
+        # ray table and lights still go H2D every frame, from per-parity
+        # pinned buffers the graph's copy nodes read
+        self.graphs = None
+        self._graph_evt = [None, None]
+        self._pinned_lights = None
+
+    def enable_graphs(self, on: bool = True) -> None:
+        self.graphs = {} if on else None
 
     def _params(self, hysteresis: float) -> N.TraceParams:
         v, s = self.volume, self.dscene
@@ -212,32 +229,78 @@ class ProbeUpdater:
         p.ray_records = self.ray_records.data_ptr() if self.ray_records is not None else None
         return p
 
+    def _wait_pinned(self, k: int) -> None:
+        """Host waits until the copy (eager or graph replay) that last read
+        pinned ray buffer k has completed."""
+        for evs in (self._pinned_evt, self._graph_evt):
+            if evs[k] is not None:
+                evs[k].synchronize()
+
     def upload_rays(self, frame: int) -> None:
         k = frame & 1
-        if self._pinned_evt[k] is not None:
-            self._pinned_evt[k].synchronize()  # the copy that last read this buffer is done
+        self._wait_pinned(k)
         self._pinned_dirs[k].numpy()[...] = frame_ray_directions(self.rays_per_probe, self.seed, frame)
         self.ray_dirs.copy_(self._pinned_dirs[k], non_blocking=True)
         evt = torch.cuda.Event()
         evt.record(torch.cuda.current_stream(self.device))
         self._pinned_evt[k] = evt
 
-    def update(self, frame: int | None = None, lights=None):
-        """Trace + blend one frame; returns (colour atlas, visibility atlas)."""
-        if frame is None:
-            frame = self.frames_done
-        if lights is not None:
-            self.dscene.set_lights(lights)
-        self.upload_rays(frame)
+    def _issue(self, hysteresis: float) -> None:
+        """Weights + shadow maps + trace + blend on the current stream."""
         stream = D.stream_ptr(self.device)
         N.call("ps_blend_weights", self.ray_dirs.data_ptr(), self.rays_per_probe,
                self.texdir.data_ptr(), self.sharpness, self.w_color.data_ptr(),
                self.w_depth.data_ptr(), self.inv_wsum.data_ptr(), stream)
+        params = self._params(hysteresis)
+        N.call("ps_trace_blend", ctypes.byref(params), stream)
+
+    def _update_graphed(self, frame: int, lights):
+        k = self.frames_done & 1
+        self._wait_pinned(k)
+        s = self.dscene
+        if self._pinned_lights is None:
+            self._pinned_lights = [torch.zeros((s.MAX_LIGHTS, 6), dtype=torch.float32).pin_memory()
+                                   for _ in range(2)]
+        if lights is not None:
+            arr = np.array([list(l.position) + list(l.intensity) for l in lights],
+                           np.float32).reshape(-1, 6)
+            if len(arr) > s.MAX_LIGHTS:
+                raise ValueError(f"at most {s.MAX_LIGHTS} lights")
+            s.light_count = len(arr)
+            s.light_host = arr
+        self._pinned_lights[k].numpy()[: s.light_count] = s.light_host
+        self._pinned_dirs[k].numpy()[...] = frame_ray_directions(self.rays_per_probe, self.seed, frame)
+        kb = self.frames_done % len(self._color_bufs)
+        self.color, self.visibility = self._color_bufs[kb], self._vis_bufs[kb]
+        key = (k, kb, s.light_count)
+        g = self.graphs.get(key)
+        if g is None:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, capture_error_mode="thread_local"):
+                self.ray_dirs.copy_(self._pinned_dirs[k], non_blocking=True)
+                s.lights.copy_(self._pinned_lights[k], non_blocking=True)
+                self._issue(self.hysteresis)
+            self.graphs[key] = g
+        g.replay()
+        evt = torch.cuda.Event()
+        evt.record(torch.cuda.current_stream(self.device))
+        self._graph_evt[k] = evt
+        self.frames_done += 1
+        return self.color, self.visibility
+
+    def update(self, frame: int | None = None, lights=None):
+        """Trace + blend one frame; returns (colour atlas, visibility atlas)."""
+        if frame is None:
+            frame = self.frames_done
+        if self.graphs is not None and self.frames_done >= 1:
+            return self._update_graphed(frame, lights)
+        if lights is not None:
+            self.dscene.set_lights(lights)
+        self.upload_rays(frame)
         h = 0.0 if self.frames_done == 0 else self.hysteresis
         k = self.frames_done % len(self._color_bufs)
         self.color, self.visibility = self._color_bufs[k], self._vis_bufs[k]
-        params = self._params(h)
-        N.call("ps_trace_blend", ctypes.byref(params), stream)
+        self._issue(h)
         self.frames_done += 1
         return self.color, self.visibility
 

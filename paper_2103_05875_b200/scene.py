@@ -135,6 +135,7 @@ class DeviceScene:
         if self._light_evt[k] is not None:
             self._light_evt[k].synchronize()
         self._light_stage[k].numpy()[: len(arr)] = arr
+        self.light_host = arr
         self.lights.copy_(self._light_stage[k], non_blocking=True)
         evt = torch.cuda.Event()
         evt.record(torch.cuda.current_stream(self.device))

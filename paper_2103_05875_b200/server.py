@@ -85,6 +85,11 @@ class KindStream:
         self.sel_count = torch.empty(1, dtype=torch.int64, device=device)
         self._cur = 0
         self.timers = None  # optional dict of per-stage (start, end) event lists
+        # CUDA-graph replay (enable_graphs): {seq, frame_count, key} live on the
+        # device and advance inside the graph (ps_frame_advance)
+        self.graphs = None
+        self.frame_state = torch.zeros(3, dtype=torch.int64, device=device)
+        self._state_synced = False
 
     def _mark(self, name, stage):
         if self.timers is not None:
@@ -92,8 +97,49 @@ class KindStream:
             e.record()
             self.timers.setdefault(name, []).append((stage, e))
 
+    def enable_graphs(self, on: bool = True) -> None:
+        self.graphs = {} if on else None
+        self._state_synced = False
+
+    def _graphable(self) -> bool:
+        return (self.graphs is not None and self.frame_count >= 1 and not self.encode
+                and self.timers is None)
+
     def tick(self, rendered: ProbeAtlas, seq: int, pvs_bits=None) -> KindOutput:
+        if self._graphable():
+            return self._tick_graphed(rendered, seq, pvs_bits)
+        self._state_synced = False
+        return self._tick_eager(rendered, seq, pvs_bits)
+
+    def _tick_graphed(self, rendered: ProbeAtlas, seq: int, pvs_bits=None) -> KindOutput:
+        """Replay this kind's captured chain (one graph per atlas buffer /
+        plane parity); identical kernels to the eager chain, with seq and the
+        key-frame flag read from ``frame_state`` on the device."""
+        if not self._state_synced:
+            # state holds the previous frame's values; the graph advances it
+            self.frame_state.copy_(torch.tensor([seq - 1, self.frame_count - 1, 0],
+                                                dtype=torch.int64))
+            self._state_synced = True
+        key = (rendered.texels.data_ptr(), self._cur, D.ptr(pvs_bits))
+        g = self.graphs.get(key)
+        if g is None:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, capture_error_mode="thread_local"):
+                self._issue(rendered, seq, pvs_bits, graphed=True)
+            self.graphs[key] = g
+        g.replay()
+        return self._advance()
+
+    def _issue(self, rendered: ProbeAtlas, seq: int, pvs_bits, graphed: bool):
+        """Stream-ordered stage chain on the current stream; returns (entries,
+        count, current planes)."""
         tag = self.kind.value
+        seq_dev = key_dev = None
+        if graphed:
+            N.call("ps_frame_advance", self.frame_state.data_ptr(), self.gop_length,
+                   D.stream_ptr(self.device))
+            seq_dev = self.frame_state[0:1]
+            key_dev = self.frame_state[2:3].view(torch.int32)[:1]
         self._mark(f"{tag}.detect", 0)
         detect_changed_device(rendered, self.last_sent, self.volume, self.threshold,
                               bits=self.bits, with_ids=False, workspace_slot=f"detect.{tag}")
@@ -112,15 +158,31 @@ class KindStream:
                count.data_ptr(), self.layout.slot_count, self.layout.slots_per_row,
                self.update_texels.data_ptr(), self.update_texels.shape[1],
                self.last_sent.texels.data_ptr(), self.last_sent_seq.data_ptr(), int(seq),
-               D.stream_ptr(self.device))
+               D.ptr(seq_dev), D.stream_ptr(self.device))
         self._mark(f"{tag}.build", 1)
         key = self.frame_count % self.gop_length == 0
-        prev = None if key else self.planes[self._cur]
+        # graphed: the device flag decides key frames per replay
+        prev = self.planes[self._cur] if graphed or not key else None
         cur = self.planes[1 - self._cur]
         self._mark(f"{tag}.pack_delta", 0)
         pack_delta(self.update_texels, self.kind, prev, planes_out=cur, residual=self.residual,
-                   skip=self.skip)
+                   skip=self.skip, key_dev=key_dev)
         self._mark(f"{tag}.pack_delta", 1)
+        return entries, count, cur
+
+    def _advance(self, frame=None, frame_len=None, index=None, index_len=None) -> KindOutput:
+        key = self.frame_count % self.gop_length == 0
+        cur = self.planes[1 - self._cur]
+        self._cur = 1 - self._cur
+        self.frame_count += 1
+        return KindOutput(cur, self.residual, self.skip, self.layout._entries,
+                          self.layout._entry_count, key, frame, frame_len, index, index_len)
+
+    def _tick_eager(self, rendered: ProbeAtlas, seq: int, pvs_bits=None) -> KindOutput:
+        tag = self.kind.value
+        key = self.frame_count % self.gop_length == 0
+        prev = None if key else self.planes[self._cur]
+        entries, count, cur = self._issue(rendered, seq, pvs_bits, graphed=False)
         frame = frame_len = index = index_len = None
         if self.encode:  # §8(f)1: LPF1 bitstream, bit-exact with codec.encode_frame
             from .codec import encode_frame_device
@@ -130,10 +192,7 @@ class KindStream:
             frame, frame_len = encode_frame_device(cur, prev, self.stream_id, self.frame_count)
             index, index_len = encode_index_device(entries, count)  # §8(f)4
             self._mark(f"{tag}.encode", 1)
-        self._cur = 1 - self._cur
-        self.frame_count += 1
-        return KindOutput(cur, self.residual, self.skip, entries, count, key, frame, frame_len,
-                          index, index_len)
+        return self._advance(frame, frame_len, index, index_len)
 
 
 class ProbeStreamServer:
@@ -142,7 +201,8 @@ class ProbeStreamServer:
     def __init__(self, volume: ProbeVolume, scene, rays_per_probe: int = 256, device=None,
                  color_threshold: float = 0.0, visibility_threshold: float = 0.0,
                  slot_count=None, budget=None, gop_length: int = DEFAULT_GOP,
-                 overlap: bool = True, encode: bool = False, **probe_kwargs):
+                 overlap: bool = True, encode: bool = False, graphs: bool = False,
+                 **probe_kwargs):
         self.device = torch.device(device) if device is not None else D.device_of()
         self.volume = volume
         # overlap: the colour and visibility chains run on their own streams,
@@ -167,6 +227,15 @@ class ProbeStreamServer:
                                      stream_id=2)
         self.seq = 0
         self.timers = None
+        self.enable_graphs(graphs)
+
+    def enable_graphs(self, on: bool = True) -> None:
+        """Replay each frame as three captured CUDA graphs (trace + blend on
+        the main stream, one stage chain per kind on its side stream) instead
+        of ~130 individual launches; frame 0 always runs eagerly."""
+        self.graphs = bool(on)
+        for part in (self.updater, self.color, self.visibility):
+            part.enable_graphs(on)
 
     def enable_stage_timers(self, on: bool = True) -> None:
         self.timers = {} if on else None

@@ -17,6 +17,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c1")
     ap.add_argument("--frames", type=int, default=3)
+    ap.add_argument("--graphs", action="store_true", help="sharded side replays CUDA graphs")
+    ap.add_argument("--gop", type=int, default=30)
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -34,8 +36,8 @@ def main():
     dims, rays, scene_name = bench.CONFIGS[args.config]
     sc = bench.build_scene(scene_name)
     vol = S.volume_for(sc, dims)
-    kw = dict(irradiance_scale=2.0, shadows="map", shadow_map_size=128)
-    frame = DistributedFrame(vol, sc, rays, dev, rank, world, **kw)
+    kw = dict(irradiance_scale=2.0, shadows="map", shadow_map_size=128, gop_length=args.gop)
+    frame = DistributedFrame(vol, sc, rays, dev, rank, world, graphs=args.graphs, **kw)
     single = ProbeStreamServer(vol, sc, rays, device=dev, **kw) if rank == 0 else None
     ok = True
     for f in range(args.frames):
