@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define PS_ABI_VERSION 2
+#define PS_ABI_VERSION 3
 
 /* status codes */
 #define PS_OK 0
@@ -320,6 +320,10 @@ typedef struct ps_trace_params {
     const float *w_color;    /* (rays, 64) cosine weights, transposed       */
     const float *w_depth;    /* (rays, 256) cosine^sharpness weights        */
     const float *inv_wsum;   /* (64 + 256) reciprocal weight sums            */
+    /* optional tensor-core operand image of the weights written by
+     * ps_blend_weights ((rays/8) * 6144 floats); non-NULL with rays % 8 == 0
+     * selects the tcgen05 blend, NULL the CUDA-core blend */
+    const float *w_image;
     float hysteresis;        /* 0 on the first frame                        */
     float irradiance_scale;  /* colour unorm = irradiance / scale            */
     /* state (float, persistent across frames), indexed by p - probe_begin */
@@ -347,10 +351,12 @@ typedef struct ps_trace_params {
 
 /* Per-frame weights: from ray_dirs and the texel directions
  * (texdir: 64*4 colour then 256*4 depth floats), writes w_color, w_depth,
- * inv_wsum. */
+ * inv_wsum, and (w_image != NULL, rays % 8 == 0) the tensor-core operand
+ * image of ps_blend_weight_image_floats(rays) floats. */
 int ps_blend_weights(const float *ray_dirs, int32_t rays_per_probe, const float *texdir,
                      float sharpness, float *w_color, float *w_depth, float *inv_wsum,
-                     void *stream);
+                     float *w_image, void *stream);
+size_t ps_blend_weight_image_floats(int32_t rays_per_probe);
 
 int ps_trace_blend(const ps_trace_params *params, void *stream);
 

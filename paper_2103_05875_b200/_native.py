@@ -16,7 +16,7 @@ from pathlib import Path
 from .errors import LayoutMismatchError, NativeLibraryError, SlotOverflowError
 
 LIB_PATH = Path(os.environ.get("PROBESTREAM_LIB", Path(__file__).resolve().parent / "libprobestream.so"))
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 PS_OK = 0
 PS_ERR_VALUE = -1
@@ -56,7 +56,7 @@ class TraceParams(C.Structure):
         ("sky", _f32 * 3), ("max_distance", _f32), ("normal_bias", _f32),
         ("shadow_mode", _i32), ("shadow_map_size", _i32), ("shadow_maps", _vp),
         ("shadow_bias", _f32),
-        ("w_color", _vp), ("w_depth", _vp), ("inv_wsum", _vp),
+        ("w_color", _vp), ("w_depth", _vp), ("inv_wsum", _vp), ("w_image", _vp),
         ("hysteresis", _f32), ("irradiance_scale", _f32),
         ("irradiance", _vp), ("moments", _vp),
         ("color_atlas", _vp), ("vis_atlas", _vp),
@@ -111,7 +111,8 @@ _SIGNATURES = {
     "ps_import_tiles": (_int, [_int, _vp, _i64, _vp, _i32, _vp, _vp, _i64, _i64, _vp, _i64, _vp]),
     "ps_bvh_build": (_int, [_vp, _i64, _int, C.POINTER(BvhSizes), _vp, _vp]),
     "ps_bvh_build_wide": (_int, [_vp, _i64, _int, _int, C.POINTER(BvhSizes), _vp, _vp]),
-    "ps_blend_weights": (_int, [_vp, _i32, _vp, _f32, _vp, _vp, _vp, _vp]),
+    "ps_blend_weights": (_int, [_vp, _i32, _vp, _f32, _vp, _vp, _vp, _vp, _vp]),
+    "ps_blend_weight_image_floats": (_sz, [_i32]),
     "ps_trace_blend": (_int, [C.POINTER(TraceParams), _vp]),
 }
 

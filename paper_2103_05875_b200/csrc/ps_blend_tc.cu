@@ -1,0 +1,468 @@
+// Stage (2) on the 5th-generation tensor cores: the DDGI blend as dense
+// products issued with tcgen05.mma (kind::tf32, fp32 accumulators in TMEM).
+//
+// Per frame every probe blends its R rays into 64 colour texels and 256 depth
+// texels with weights that are shared by all probes (cosine / cosine^s of the
+// texel and ray directions).  For a CTA of P = 64 probes that is
+//
+//   D_depth[t, n] = sum_r Wd[r, t] * Bd[r, n]     t < 256, n = (d | d^2, probe)
+//   D_col  [t, n] = sum_r Wc[r, t] * Bc[r, n]     t < 64,  n = (r | g | b, probe)
+//
+// i.e. M = texels (two M=128 tiles for depth, one zero-padded M=128 tile for
+// colour), N = 128 / 192 probe channels, K = rays in steps of 8.  TMEM holds
+// all three accumulators (128 + 128 + 192 = 448 of 512 columns).
+//
+// Precision (parity bar: 1e-4 relative vs the fp32 oracle): fp32 operands
+// are split x = hi + lo with hi = x with its low 13 mantissa bits cleared
+// (exactly representable in tf32) and lo = x - hi (exact in fp32), and every
+// product is issued as A_hi*B_hi + A_hi*B_lo + A_lo*B_hi ("3xTF32"): the
+// dropped A_lo*B_lo term and the tf32 truncation of the lo parts are
+// <= 2^-21 relative, so the result is fp32-accurate.
+//
+// Pipeline per k-step (8 rays), 4 shared-memory stages of 44 KB:
+//   * A (weights, 6 operand images hi/lo, 24 KB) arrive by cp.async from a
+//     per-frame image the weights pass writes in the canonical K-major
+//     no-swizzle UMMA layout (so the copy is a straight 16-byte stream);
+//   * the ray records stream through a 4-slot cp.async ring (3 k-steps
+//     ahead); each thread converts its own 2 records to the B images (probe
+//     channels d, d^2, r, g, b) in the same layout, hi and lo;
+//   * one thread issues 9 MMAs (3 tiles x 3 terms) and commits them to the
+//     stage's mbarrier, which the producers wait on before reusing the stage.
+// The epilogue reads the accumulators with tcgen05.ld (one texel per TMEM
+// lane), applies the normalisation / hysteresis / quantisation of the SIMT
+// blend and writes the guard-banded atlas blocks.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+
+#include "ps_common.cuh"
+#include "ps_guard.cuh"
+
+namespace ps {
+namespace tc {
+
+constexpr int P = 64;         // probes per CTA
+constexpr int THREADS = 256;  // 8 warps
+constexpr int STAGES = 4;
+constexpr int PART = 128 * 8;                 // floats of one 128-row x 8-k operand image
+constexpr int A_FLOATS = 6 * PART;            // d0 hi, d1 hi, c hi, d0 lo, d1 lo, c lo
+constexpr int BD_ROWS = 2 * P;                // d (probe q) then d^2 (probe q)
+constexpr int BC_ROWS = 3 * P;                // r, g, b
+constexpr int BD = BD_ROWS * 8;               // floats of one depth B image
+constexpr int BC = BC_ROWS * 8;
+constexpr int STAGE = A_FLOATS + 2 * BD + 2 * BC;  // 11264 floats = 44 KB
+constexpr int RAW = P * 8 * 4;                      // raw records of one k-step (8 KB)
+constexpr int RING = 4;                             // raw ring slots (prefetch distance 3)
+constexpr size_t SMEM_BYTES = (size_t(STAGES) * STAGE + size_t(RING) * RAW) * 4 + 1024;
+constexpr uint32_t COL_D0 = 0, COL_D1 = 128, COL_C = 256, TMEM_COLS = 512;
+
+static_assert(P * 64 + P * 256 <= STAGES * STAGE, "epilogue staging must fit the stages");
+
+// canonical K-major, no-swizzle operand image: 8-row x 16-byte core matrices,
+// row groups 128 B apart (SBO), the two 4-wide k halves rows*16 B apart (LBO)
+__host__ __device__ constexpr int img_off(int rows, int m, int k) {
+    return (k >> 2) * rows * 4 + (m >> 3) * 32 + (m & 7) * 4 + (k & 3);
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ uint64_t smem_desc(const float *p, uint32_t rows) {
+    uint64_t d = uint64_t((smem_u32(p) >> 4) & 0x3FFFu);
+    d |= uint64_t((rows * 16u >> 4) & 0x3FFFu) << 16;  // leading byte offset (k halves)
+    d |= uint64_t((128u >> 4) & 0x3FFFu) << 32;        // stride byte offset (row groups)
+    d |= uint64_t(1) << 46;                            // descriptor version (sm_100)
+    return d;                                          // base 0, swizzle none
+}
+
+// instruction descriptor: D f32, A/B tf32, both K-major, M x N
+__host__ __device__ constexpr uint32_t idesc(int m, int n) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(n >> 3) << 17) | (uint32_t(m >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t id,
+                                         uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(id), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t *bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "LAB_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra DONE;\n\t"
+        "bra LAB_WAIT;\n\t"
+        "DONE:\n\t}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void fence_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// 16 consecutive accumulator columns of this warp's 32 TMEM lanes
+__device__ __forceinline__ void tmem_ld16(uint32_t addr, float (&v)[16]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15])
+        : "r"(addr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ float tf32_hi(float x) {
+    return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+}
+
+// weights pass: the per-frame A image, (R/8) k-steps x 6 operand images
+__global__ void weight_image_kernel(const float *w_color, const float *w_depth, int R,
+                                    float *img) {
+    const int total = (R / 8) * A_FLOATS;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        const int s = i / A_FLOATS, rem = i - s * A_FLOATS;
+        const int part = rem / PART, off = rem - part * PART;
+        // invert img_off(128, m, k)
+        const int kh = off / 512, in = off - kh * 512;
+        const int m = (in >> 5) * 8 + ((in & 31) >> 2);
+        const int k = kh * 4 + (in & 3);
+        const int r = s * 8 + k;
+        const int tile = part % 3;
+        float w = 0.f;
+        if (tile == 2)
+            w = m < 64 ? w_color[r * 64 + m] : 0.f;
+        else
+            w = w_depth[r * 256 + tile * 128 + m];
+        const float hi = tf32_hi(w);
+        img[i] = part < 3 ? hi : w - hi;
+    }
+}
+
+// this thread's share of a k-step: rays (8c + 2j, 8c + 2j + 1) of probe q,
+// staged raw (2 float4) in a ring slot of 8 KB by cp.async
+__device__ __forceinline__ void issue_raw(float *ring, const float4 *records, int R, int q,
+                                          int nq, int c, int j) {
+    if (q < nq) {
+        const float4 *src = records + size_t(q) * R + c * 8 + 2 * j;
+        float *dst = ring + (q * 8 + 2 * j) * 4;
+        cp_async16(dst, src);
+        cp_async16(dst + 4, src + 1);
+    }
+}
+
+__device__ __forceinline__ void put2(float *img, int rows, int m, int k, float x0, float x1) {
+    *reinterpret_cast<float2 *>(img + img_off(rows, m, k)) = make_float2(x0, x1);
+}
+
+// raw records of (q, rays 2j, 2j+1) -> B images (hi, lo) of the stage
+__device__ __forceinline__ void stage_b(float *st, const float *ring, int q, int nq, int j) {
+    float *bdh = st + A_FLOATS, *bdl = bdh + BD, *bch = bdl + BD, *bcl = bch + BC;
+    const int k = 2 * j;
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+    if (q < nq) {
+        const float4 *src = reinterpret_cast<const float4 *>(ring) + q * 8 + 2 * j;
+        a = src[0];
+        b = src[1];
+    }
+    const float x0[5] = {a.w, a.w * a.w, a.x, a.y, a.z};
+    const float x1[5] = {b.w, b.w * b.w, b.x, b.y, b.z};
+#pragma unroll
+    for (int ch = 0; ch < 5; ++ch) {
+        const float h0 = tf32_hi(x0[ch]), h1 = tf32_hi(x1[ch]);
+        if (ch < 2) {
+            put2(bdh, BD_ROWS, ch * P + q, k, h0, h1);
+            put2(bdl, BD_ROWS, ch * P + q, k, x0[ch] - h0, x1[ch] - h1);
+        } else {
+            put2(bch, BC_ROWS, (ch - 2) * P + q, k, h0, h1);
+            put2(bcl, BC_ROWS, (ch - 2) * P + q, k, x0[ch] - h0, x1[ch] - h1);
+        }
+    }
+}
+
+__device__ __forceinline__ void issue_a(float *st, const float *img, int c, int tid) {
+    const float *src = img + size_t(c) * A_FLOATS;
+#pragma unroll
+    for (int i = 0; i < A_FLOATS / 4 / THREADS; ++i) {
+        const int e = (i * THREADS + tid) * 4;
+        cp_async16(st + e, src + e);
+    }
+}
+
+__device__ __forceinline__ void issue_mma(float *st, uint32_t tmem, int c) {
+    const float *a = st;
+    const float *bdh = st + A_FLOATS, *bdl = bdh + BD, *bch = bdl + BD, *bcl = bch + BC;
+    const uint32_t acc = c > 0 ? 1u : 0u;
+    constexpr uint32_t ID_D = idesc(128, BD_ROWS), ID_C = idesc(128, BC_ROWS);
+    const uint64_t b_dh = smem_desc(bdh, BD_ROWS), b_dl = smem_desc(bdl, BD_ROWS);
+    const uint64_t b_ch = smem_desc(bch, BC_ROWS), b_cl = smem_desc(bcl, BC_ROWS);
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {  // depth tiles (texels 0-127, 128-255)
+        const uint64_t ah = smem_desc(a + t * PART, 128), al = smem_desc(a + (3 + t) * PART, 128);
+        const uint32_t d = tmem + (t ? COL_D1 : COL_D0);
+        mma_tf32(d, ah, b_dh, ID_D, acc);
+        mma_tf32(d, ah, b_dl, ID_D, 1u);
+        mma_tf32(d, al, b_dh, ID_D, 1u);
+    }
+    const uint64_t ah = smem_desc(a + 2 * PART, 128), al = smem_desc(a + 5 * PART, 128);
+    mma_tf32(tmem + COL_C, ah, b_ch, ID_C, acc);
+    mma_tf32(tmem + COL_C, ah, b_cl, ID_C, 1u);
+    mma_tf32(tmem + COL_C, al, b_ch, ID_C, 1u);
+}
+
+__global__ void __launch_bounds__(THREADS, 1) blend_tc_kernel(ps_trace_params prm) {
+    extern __shared__ unsigned char smem_raw[];
+    float *stages = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                              ~uintptr_t(1023));
+    __shared__ __align__(8) uint64_t bars[STAGES];
+    __shared__ uint32_t s_tmem;
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int R = prm.rays_per_probe, NK = R / 8;
+    const int64_t p0 = int64_t(prm.probe_begin) + int64_t(blockIdx.x) * P;
+    const int64_t left = int64_t(prm.probe_end) - p0;
+    const int nq = int(left < P ? left : P);
+    const int64_t pl0 = p0 - prm.probe_begin;
+    const float4 *records = reinterpret_cast<const float4 *>(prm.records) + pl0 * R;
+    const float *img = prm.w_image;
+
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(&s_tmem)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = s_tmem;
+
+    // ---- main loop: k-steps of 8 rays -------------------------------------------------------
+    // cp.async groups: G0 = {A0, raw0}, G1 = {A1, raw1}, G2 = {raw2}, then step c commits
+    // G(c+3) = {A(c+2), raw(c+3)}; waiting for all but the 2 newest groups at step c
+    // leaves A(c) (in G(c) or G(c+1)) and raw(c) (in G(c)) landed.
+    float *ring = stages + STAGES * STAGE;
+    const int q = tid >> 2, j = tid & 3;  // this thread's probe and ray pair in a k-step
+    issue_a(stages, img, 0, tid);
+    issue_raw(ring, records, R, q, nq, 0, j);
+    cp_async_commit();
+    if (NK > 1) {
+        issue_a(stages + STAGE, img, 1, tid);
+        issue_raw(ring + RAW, records, R, q, nq, 1, j);
+    }
+    cp_async_commit();
+    if (NK > 2) issue_raw(ring + 2 * RAW, records, R, q, nq, 2, j);
+    cp_async_commit();
+#pragma unroll 1
+    for (int c = 0; c < NK; ++c) {
+        float *st = stages + (c % STAGES) * STAGE;
+        if (c >= 2) mbar_wait(&bars[(c - 2) % STAGES], ((c - 2) / STAGES) & 1);
+        if (c + 2 < NK) issue_a(stages + ((c + 2) % STAGES) * STAGE, img, c + 2, tid);
+        if (c + 3 < NK) issue_raw(ring + ((c + 3) % RING) * RAW, records, R, q, nq, c + 3, j);
+        cp_async_commit();
+        cp_async_wait<2>();
+        stage_b(st, ring + (c % RING) * RAW, q, nq, j);  // own raw records: no barrier needed
+        fence_async_smem();
+        __syncthreads();
+        if (tid == 0) {
+            tc_fence_after();
+            issue_mma(st, tmem, c);
+            mma_commit(&bars[c % STAGES]);
+        }
+    }
+    mbar_wait(&bars[(NK - 1) % STAGES], ((NK - 1) / STAGES) & 1);  // every MMA has completed
+    cp_async_wait<0>();
+    tc_fence_after();
+
+    // ---- epilogue: TMEM -> state + quantised cores (staged in the freed stages) -----------
+    uint32_t *s_ccore = reinterpret_cast<uint32_t *>(stages);  // [P][64]
+    uint32_t *s_vcore = s_ccore + P * 64;                      // [P][256]
+    const float h = prm.hysteresis;
+    const float qs = prm.irradiance_scale > 0.f ? 1.0f / prm.irradiance_scale : 0.f;
+    const int sub = warp & 3, half = warp >> 2;
+    const uint32_t lane_base = tmem + (uint32_t(sub * 32) << 16);
+    {  // depth moments: warp half h owns tile h, one texel per lane
+        const int t = half * 128 + sub * 32 + lane;
+        const float inv = __ldg(prm.inv_wsum + 64 + t);
+        const uint32_t base = lane_base + (half ? COL_D1 : COL_D0);
+        float2 *mom = reinterpret_cast<float2 *>(prm.moments) + pl0 * 256 + t;
+        const bool need_old = inv == 0.f || h != 0.f;
+#pragma unroll 1
+        for (int q0 = 0; q0 < P; q0 += 16) {
+            float2 old[16];  // independent loads first: the state read is latency bound
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+                old[i] = (need_old && q0 + i < nq) ? __ldcs(mom + (q0 + i) * 256)
+                                                   : make_float2(0.f, 0.f);
+            float m1[16], m2[16];
+            tmem_ld16(base + q0, m1);
+            tmem_ld16(base + P + q0, m2);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const int qq = q0 + i;
+                if (qq >= nq) break;
+                float a = m1[i] * inv, b = m2[i] * inv;
+                if (inv == 0.f) {
+                    a = old[i].x;
+                    b = old[i].y;
+                } else if (h != 0.f) {
+                    a = fmaf(h, old[i].x - a, a);
+                    b = fmaf(h, old[i].y - b, b);
+                }
+                __stcs(mom + qq * 256, make_float2(a, b));
+                s_vcore[qq * 256 + t] = uint32_t(__half_as_ushort(__float2half_rn(a))) |
+                                        (uint32_t(__half_as_ushort(__float2half_rn(b))) << 16);
+            }
+        }
+    }
+    if (sub < 2) {  // colour: TMEM lanes 0-63 are the 64 texels; warp half h owns 32 probes
+        const int t = sub * 32 + lane;
+        const float inv = __ldg(prm.inv_wsum + t);
+        const uint32_t base = lane_base + COL_C;
+        const bool need_old = inv == 0.f || h != 0.f;
+#pragma unroll 1
+        for (int q0 = half * 32; q0 < half * 32 + 32; q0 += 16) {
+            float old[16][3];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const float *st = prm.irradiance + ((pl0 + q0 + i) * 64 + t) * 3;
+                const bool ld = need_old && q0 + i < nq;
+#pragma unroll
+                for (int ch = 0; ch < 3; ++ch) old[i][ch] = ld ? __ldcs(st + ch) : 0.f;
+            }
+            float cr[16], cg[16], cb[16];
+            tmem_ld16(base + q0, cr);
+            tmem_ld16(base + P + q0, cg);
+            tmem_ld16(base + 2 * P + q0, cb);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const int qq = q0 + i;
+                if (qq >= nq) break;
+                float *st = prm.irradiance + ((pl0 + qq) * 64 + t) * 3;
+                const float acc[3] = {cr[i], cg[i], cb[i]};
+                uint32_t texel = 0;
+#pragma unroll
+                for (int ch = 0; ch < 3; ++ch) {
+                    float v = acc[ch] * inv;
+                    if (inv == 0.f) v = old[i][ch];  // no ray sees this texel: keep the state
+                    else if (h != 0.f) v = fmaf(h, old[i][ch] - v, v);
+                    __stcs(st + ch, v);
+                    const float x = fminf(fmaxf(v * qs, 0.0f), 1.0f);
+                    texel |= __float2uint_rn(x * 1023.0f) << (10 * ch);
+                }
+                s_ccore[qq * 64 + t] = texel;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+
+    // ---- atlas blocks with guard bands -------------------------------------------------------
+    {
+        const int ppr = prm.probes_per_row_color;
+        const int W = ppr * 10;
+        const int pb = int(p0);
+        for (int idx = tid; idx < nq * 100; idx += THREADS) {
+            const int qq = idx / 100, k = idx - qq * 100;
+            const int r = k / 10, c = k - r * 10;
+            const int p = pb + qq;
+            const int by = p / ppr;
+            const int y0 = by * 10, x0 = (p - by * ppr) * 10;
+            prm.color_atlas[size_t(y0 + r) * W + x0 + c] = s_ccore[qq * 64 + guard_source(r, c, 10)];
+        }
+    }
+    {
+        const int ppr = prm.probes_per_row_vis;
+        const int W = ppr * 18;
+        const int pb = int(p0);
+        uint32_t *vis = reinterpret_cast<uint32_t *>(prm.vis_atlas);
+        for (int idx = tid; idx < nq * 324; idx += THREADS) {
+            const int qq = idx / 324, k = idx - qq * 324;
+            const int r = k / 18, c = k - r * 18;
+            const int p = pb + qq;
+            const int by = p / ppr;
+            const int y0 = by * 18, x0 = (p - by * ppr) * 18;
+            vis[size_t(y0 + r) * W + x0 + c] = s_vcore[qq * 256 + guard_source(r, c, 18)];
+        }
+    }
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                     "r"(TMEM_COLS));
+    }
+}
+
+}  // namespace tc
+
+size_t weight_image_floats(int rays_per_probe) {
+    return rays_per_probe % 8 == 0 ? size_t(rays_per_probe / 8) * tc::A_FLOATS : 0;
+}
+
+void launch_weight_image(const float *w_color, const float *w_depth, int R, float *img,
+                         cudaStream_t s) {
+    const int total = (R / 8) * tc::A_FLOATS;
+    tc::weight_image_kernel<<<unsigned(ceil_div(total, 256)), 256, 0, s>>>(w_color, w_depth, R, img);
+    check_launch("weight_image_kernel");
+}
+
+bool blend_tc_usable(const ps_trace_params &p) {
+    static const bool off = [] {
+        const char *e = getenv("PS_BLEND");
+        return e && e[0] == 's';  // PS_BLEND=simt forces the CUDA-core blend
+    }();
+    return !off && p.w_image && p.rays_per_probe % 8 == 0;
+}
+
+void launch_blend_tc(const ps_trace_params &p, int64_t nloc, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        check_cuda(cudaFuncSetAttribute(tc::blend_tc_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        int(tc::SMEM_BYTES)),
+                   "cudaFuncSetAttribute(blend_tc)");
+        attr = true;
+    }
+    tc::blend_tc_kernel<<<unsigned(ceil_div(nloc, tc::P)), tc::THREADS, tc::SMEM_BYTES, s>>>(p);
+    check_launch("blend_tc_kernel");
+}
+
+}  // namespace ps

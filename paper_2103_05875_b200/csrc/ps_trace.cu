@@ -33,8 +33,16 @@
 
 #include "ps_common.cuh"
 #include "ps_traverse.cuh"
+#include "ps_guard.cuh"
 
 namespace ps {
+
+// ps_blend_tc.cu
+size_t weight_image_floats(int rays_per_probe);
+void launch_weight_image(const float *w_color, const float *w_depth, int R, float *img,
+                         cudaStream_t s);
+bool blend_tc_usable(const ps_trace_params &p);
+void launch_blend_tc(const ps_trace_params &p, int64_t nloc, cudaStream_t s);
 namespace {
 
 constexpr int THREADS = 256;
@@ -142,24 +150,6 @@ __device__ Shade shade_hit(const ps_trace_params &p, const float4 *nodes, const 
     s.t = t;
     s.prim = prim;
     return s;
-}
-
-// guard band rule (packing.py:180-196): block (r, c) -> core index
-__device__ __forceinline__ int guard_source(int r, int c, int side) {
-    const int n = side - 2;
-    const bool top = r == 0, bot = r == side - 1, left = c == 0, right = c == side - 1;
-    int rr = r, cc = c;
-    if ((top || bot) && (left || right)) {
-        rr = top ? n : 1;
-        cc = left ? n : 1;
-    } else if (top || bot) {
-        rr = top ? 1 : n;
-        cc = side - 1 - c;
-    } else if (left || right) {
-        rr = side - 1 - r;
-        cc = left ? 1 : n;
-    }
-    return (rr - 1) * n + (cc - 1);
 }
 
 // ---- pass 0: cube distance maps traced from each light ------------------------------
@@ -722,9 +712,13 @@ using namespace ps;
 
 extern "C" {
 
+size_t ps_blend_weight_image_floats(int32_t rays_per_probe) {
+    return weight_image_floats(rays_per_probe);
+}
+
 int ps_blend_weights(const float *ray_dirs, int32_t rays_per_probe, const float *texdir,
                      float sharpness, float *w_color, float *w_depth, float *inv_wsum,
-                     void *stream) {
+                     float *w_image, void *stream) {
     PS_ABI_BEGIN
     if (rays_per_probe < 1) fail(PS_ERR_VALUE, "rays_per_probe must be >= 1");
     auto s = as_stream(stream);
@@ -735,6 +729,10 @@ int ps_blend_weights(const float *ray_dirs, int32_t rays_per_probe, const float 
     check_launch("weights_kernel");
     wsum_kernel<<<2, 256, 0, s>>>(rays_per_probe, w_color, w_depth, inv_wsum);
     check_launch("wsum_kernel");
+    if (w_image) {
+        if (rays_per_probe % 8) fail(PS_ERR_VALUE, "the weight image needs rays_per_probe % 8 == 0");
+        launch_weight_image(w_color, w_depth, rays_per_probe, w_image, s);
+    }
     PS_ABI_END
 }
 
@@ -787,7 +785,11 @@ int ps_trace_blend(const ps_trace_params *params, void *stream) {
         const int keep = p.reserve_sms > 0 && p.reserve_sms < sms / 2 ? p.reserve_sms : 0;
         launch_trace(p, variant, sms - keep, s);
     }
-    // pass 2: blend
+    // pass 2: blend -- tcgen05 tensor cores (ps_blend_tc.cu), or the CUDA-core kernel
+    if (blend_tc_usable(p)) {
+        launch_blend_tc(p, nloc, s);
+        return PS_OK;
+    }
     const size_t smem = blend_smem_bytes(p.rays_per_probe);
     static bool attr_set = false;
     if (!attr_set) {

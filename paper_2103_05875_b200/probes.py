@@ -172,6 +172,9 @@ class ProbeUpdater:
         self.w_color = torch.empty((R, 64), dtype=torch.float32, device=dev)
         self.w_depth = torch.empty((R, 256), dtype=torch.float32, device=dev)
         self.inv_wsum = torch.empty(320, dtype=torch.float32, device=dev)
+        # tensor-core blend operand image (rays % 8 == 0); None -> CUDA-core blend
+        nimg = N.lib().ps_blend_weight_image_floats(R)
+        self.w_image = torch.empty(nimg, dtype=torch.float32, device=dev) if nimg else None
         self.ray_dirs = torch.empty((R, 4), dtype=torch.float32, device=dev)
         # double-buffered pinned staging for the per-frame ray table
         self._pinned_dirs = [torch.empty((R, 4), dtype=torch.float32).pin_memory() for _ in range(2)]
@@ -219,6 +222,7 @@ class ProbeUpdater:
         p.reserve_sms = self.reserve_sms
         p.w_color, p.w_depth, p.inv_wsum = (self.w_color.data_ptr(), self.w_depth.data_ptr(),
                                             self.inv_wsum.data_ptr())
+        p.w_image = D.ptr(self.w_image)
         p.hysteresis = hysteresis
         p.irradiance_scale = self.irradiance_scale
         p.irradiance, p.moments = self.irradiance.data_ptr(), self.moments.data_ptr()
@@ -250,7 +254,7 @@ class ProbeUpdater:
         stream = D.stream_ptr(self.device)
         N.call("ps_blend_weights", self.ray_dirs.data_ptr(), self.rays_per_probe,
                self.texdir.data_ptr(), self.sharpness, self.w_color.data_ptr(),
-               self.w_depth.data_ptr(), self.inv_wsum.data_ptr(), stream)
+               self.w_depth.data_ptr(), self.inv_wsum.data_ptr(), D.ptr(self.w_image), stream)
         params = self._params(hysteresis)
         N.call("ps_trace_blend", ctypes.byref(params), stream)
 
