@@ -9,8 +9,9 @@
 //   D_col  [t, n] = sum_r Wc[r, t] * Bc[r, n]     t < 64,  n = (r | g | b, probe)
 //
 // i.e. M = texels (two M=128 tiles for depth, one zero-padded M=128 tile for
-// colour), N = 128 / 192 probe channels, K = rays in steps of 8.  TMEM holds
-// all three accumulators (128 + 128 + 192 = 448 of 512 columns).
+// colour), N = 64 / 96 probe channels, K = rays in steps of 8.  TMEM holds
+// all three accumulators (64 + 64 + 96 = 224 of a 256-column allocation), so
+// two CTAs share an SM and one's epilogue overlaps the other's MMAs.
 //
 // Precision (parity bar: 1e-4 relative vs the fp32 oracle): fp32 operands
 // are split x = hi + lo with hi = x with its low 13 mantissa bits cleared
@@ -19,18 +20,18 @@
 // dropped A_lo*B_lo term and the tf32 truncation of the lo parts are
 // <= 2^-21 relative, so the result is fp32-accurate.
 //
-// Pipeline per k-step (8 rays), 4 shared-memory stages of 44 KB:
-//   * A (weights, 6 operand images hi/lo, 24 KB) arrive by cp.async from a
-//     per-frame image the weights pass writes in the canonical K-major
-//     no-swizzle UMMA layout (so the copy is a straight 16-byte stream);
-//   * the ray records stream through a 4-slot cp.async ring (3 k-steps
-//     ahead); each thread converts its own 2 records to the B images (probe
-//     channels d, d^2, r, g, b) in the same layout, hi and lo;
-//   * one thread issues 9 MMAs (3 tiles x 3 terms) and commits them to the
-//     stage's mbarrier, which the producers wait on before reusing the stage.
+// Warp-specialised pipeline over k-steps of 8 rays, 3 shared-memory stages
+// of 34 KB, mbarriers between the roles:
+//   * warp 5 (one thread) streams the weights (6 operand images hi/lo,
+//     24 KB per k-step) with TMA bulk copies from a per-frame image the
+//     weights pass writes in the canonical K-major no-swizzle UMMA layout;
+//   * warps 0-3 convert the ray records (prefetched three k-steps ahead in
+//     registers) into the B images (channels d, d^2, r, g, b), hi and lo;
+//   * warp 4 (one thread) issues 9 MMAs per k-step (3 tiles x 3 terms) and
+//     commits them to the stage's "empty" barrier.
 // The epilogue reads the accumulators with tcgen05.ld (one texel per TMEM
-// lane), applies the normalisation / hysteresis / quantisation of the SIMT
-// blend and writes the guard-banded atlas blocks.
+// lane), applies the normalisation / hysteresis / quantisation of the
+// CUDA-core blend and writes the guard-banded atlas blocks.
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -42,25 +43,27 @@
 namespace ps {
 namespace tc {
 
-constexpr int P = 64;         // probes per CTA
-constexpr int THREADS = 256;  // 8 warps
-constexpr int STAGES = 4;
+constexpr int P = 32;         // probes per CTA (two CTAs per SM: one's epilogue overlaps
+                              // the other's MMAs)
+constexpr int THREADS = 256;  // warps 0-3 convert records, 4 issues MMAs, 5 loads weights
+constexpr int PRODUCERS = 128;
+constexpr int STAGES = 3;
 constexpr int PART = 128 * 8;                 // floats of one 128-row x 8-k operand image
 constexpr int A_FLOATS = 6 * PART;            // d0 hi, d1 hi, c hi, d0 lo, d1 lo, c lo
 constexpr int BD_ROWS = 2 * P;                // d (probe q) then d^2 (probe q)
 constexpr int BC_ROWS = 3 * P;                // r, g, b
 constexpr int BD = BD_ROWS * 8;               // floats of one depth B image
 constexpr int BC = BC_ROWS * 8;
-constexpr int STAGE = A_FLOATS + 2 * BD + 2 * BC;  // 11264 floats = 44 KB
-constexpr int RAW = P * 8 * 4;                      // raw records of one k-step (8 KB)
-constexpr int RING = 4;                             // raw ring slots (prefetch distance 3)
-constexpr size_t SMEM_BYTES = (size_t(STAGES) * STAGE + size_t(RING) * RAW) * 4 + 1024;
-constexpr uint32_t COL_D0 = 0, COL_D1 = 128, COL_C = 256, TMEM_COLS = 512;
+constexpr int STAGE = A_FLOATS + 2 * BD + 2 * BC;  // 8704 floats = 34 KB
+constexpr size_t SMEM_BYTES = size_t(STAGES) * STAGE * 4 + 1024;
+constexpr uint32_t COL_D0 = 0, COL_D1 = BD_ROWS, COL_C = 2 * BD_ROWS, TMEM_COLS = 256;
 
+static_assert(COL_C + BC_ROWS <= TMEM_COLS, "accumulators must fit the TMEM allocation");
 static_assert(P * 64 + P * 256 <= STAGES * STAGE, "epilogue staging must fit the stages");
 
 // canonical K-major, no-swizzle operand image: 8-row x 16-byte core matrices,
-// row groups 128 B apart (SBO), the two 4-wide k halves rows*16 B apart (LBO)
+// row groups 128 B apart (SBO), the two 4-wide k halves rows*16 B apart (LBO);
+// within a k half, row m starts at float 4m
 __host__ __device__ constexpr int img_off(int rows, int m, int k) {
     return (k >> 2) * rows * 4 + (m >> 3) * 32 + (m & 7) * 4 + (k & 3);
 }
@@ -111,15 +114,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "DONE:\n\t}\n" ::"r"(smem_u32(bar)),
         "r"(parity)
         : "memory");
-}
-
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
 __device__ __forceinline__ void fence_async_smem() {
@@ -174,15 +168,39 @@ __global__ void weight_image_kernel(const float *w_color, const float *w_depth, 
     }
 }
 
-// this thread's share of a k-step: rays (8c + 2j, 8c + 2j + 1) of probe q,
-// staged raw (2 float4) in a ring slot of 8 KB by cp.async
-__device__ __forceinline__ void issue_raw(float *ring, const float4 *records, int R, int q,
-                                          int nq, int c, int j) {
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+// TMA bulk copy global -> shared, completing `bytes` of the barrier's transaction count
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,
+                                         uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// one producer thread's share of a k-step: rays (8c + 2j, 8c + 2j + 1) of probe q
+struct Rec2 {
+    float4 a, b;
+};
+
+__device__ __forceinline__ void load_rec(Rec2 &v, const float4 *records, int R, int q, int nq,
+                                         int c, int j) {
     if (q < nq) {
-        const float4 *src = records + size_t(q) * R + c * 8 + 2 * j;
-        float *dst = ring + (q * 8 + 2 * j) * 4;
-        cp_async16(dst, src);
-        cp_async16(dst + 4, src + 1);
+        const float4 *p = records + size_t(q) * R + c * 8 + 2 * j;
+        v.a = __ldcs(p);
+        v.b = __ldcs(p + 1);
+    } else {
+        v.a = v.b = make_float4(0.f, 0.f, 0.f, 0.f);
     }
 }
 
@@ -190,18 +208,12 @@ __device__ __forceinline__ void put2(float *img, int rows, int m, int k, float x
     *reinterpret_cast<float2 *>(img + img_off(rows, m, k)) = make_float2(x0, x1);
 }
 
-// raw records of (q, rays 2j, 2j+1) -> B images (hi, lo) of the stage
-__device__ __forceinline__ void stage_b(float *st, const float *ring, int q, int nq, int j) {
+// records -> B images (hi, lo) of the stage: channels d, d^2 (depth), r, g, b
+__device__ __forceinline__ void stage_b(float *st, const Rec2 &v, int q, int j) {
     float *bdh = st + A_FLOATS, *bdl = bdh + BD, *bch = bdl + BD, *bcl = bch + BC;
     const int k = 2 * j;
-    float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
-    if (q < nq) {
-        const float4 *src = reinterpret_cast<const float4 *>(ring) + q * 8 + 2 * j;
-        a = src[0];
-        b = src[1];
-    }
-    const float x0[5] = {a.w, a.w * a.w, a.x, a.y, a.z};
-    const float x1[5] = {b.w, b.w * b.w, b.x, b.y, b.z};
+    const float x0[5] = {v.a.w, v.a.w * v.a.w, v.a.x, v.a.y, v.a.z};
+    const float x1[5] = {v.b.w, v.b.w * v.b.w, v.b.x, v.b.y, v.b.z};
 #pragma unroll
     for (int ch = 0; ch < 5; ++ch) {
         const float h0 = tf32_hi(x0[ch]), h1 = tf32_hi(x1[ch]);
@@ -215,16 +227,7 @@ __device__ __forceinline__ void stage_b(float *st, const float *ring, int q, int
     }
 }
 
-__device__ __forceinline__ void issue_a(float *st, const float *img, int c, int tid) {
-    const float *src = img + size_t(c) * A_FLOATS;
-#pragma unroll
-    for (int i = 0; i < A_FLOATS / 4 / THREADS; ++i) {
-        const int e = (i * THREADS + tid) * 4;
-        cp_async16(st + e, src + e);
-    }
-}
-
-__device__ __forceinline__ void issue_mma(float *st, uint32_t tmem, int c) {
+__device__ __forceinline__ void issue_mma(const float *st, uint32_t tmem, int c) {
     const float *a = st;
     const float *bdh = st + A_FLOATS, *bdl = bdh + BD, *bch = bdl + BD, *bcl = bch + BC;
     const uint32_t acc = c > 0 ? 1u : 0u;
@@ -245,11 +248,11 @@ __device__ __forceinline__ void issue_mma(float *st, uint32_t tmem, int c) {
     mma_tf32(tmem + COL_C, al, b_ch, ID_C, 1u);
 }
 
-__global__ void __launch_bounds__(THREADS, 1) blend_tc_kernel(ps_trace_params prm) {
+__global__ void __launch_bounds__(THREADS, 2) blend_tc_kernel(ps_trace_params prm) {
     extern __shared__ unsigned char smem_raw[];
     float *stages = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~uintptr_t(1023));
-    __shared__ __align__(8) uint64_t bars[STAGES];
+    __shared__ __align__(8) uint64_t a_full[STAGES], b_full[STAGES], empty[STAGES], done;
     __shared__ uint32_t s_tmem;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -258,11 +261,14 @@ __global__ void __launch_bounds__(THREADS, 1) blend_tc_kernel(ps_trace_params pr
     const int64_t left = int64_t(prm.probe_end) - p0;
     const int nq = int(left < P ? left : P);
     const int64_t pl0 = p0 - prm.probe_begin;
-    const float4 *records = reinterpret_cast<const float4 *>(prm.records) + pl0 * R;
-    const float *img = prm.w_image;
 
     if (tid == 0) {
-        for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&a_full[s], 1);
+            mbar_init(&b_full[s], PRODUCERS);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(&done, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0) {
@@ -276,41 +282,60 @@ __global__ void __launch_bounds__(THREADS, 1) blend_tc_kernel(ps_trace_params pr
     tc_fence_after();
     const uint32_t tmem = s_tmem;
 
-    // ---- main loop: k-steps of 8 rays -------------------------------------------------------
-    // cp.async groups: G0 = {A0, raw0}, G1 = {A1, raw1}, G2 = {raw2}, then step c commits
-    // G(c+3) = {A(c+2), raw(c+3)}; waiting for all but the 2 newest groups at step c
-    // leaves A(c) (in G(c) or G(c+1)) and raw(c) (in G(c)) landed.
-    float *ring = stages + STAGES * STAGE;
-    const int q = tid >> 2, j = tid & 3;  // this thread's probe and ray pair in a k-step
-    issue_a(stages, img, 0, tid);
-    issue_raw(ring, records, R, q, nq, 0, j);
-    cp_async_commit();
-    if (NK > 1) {
-        issue_a(stages + STAGE, img, 1, tid);
-        issue_raw(ring + RAW, records, R, q, nq, 1, j);
-    }
-    cp_async_commit();
-    if (NK > 2) issue_raw(ring + 2 * RAW, records, R, q, nq, 2, j);
-    cp_async_commit();
+    // ---- main loop: k-steps of 8 rays, warp-specialised ------------------------------------
+    // stage s, use u = c / STAGES: a_full / b_full complete phase u when the weights /
+    // probe channels of k-step c are in place; empty completes phase u when the MMAs of
+    // k-step c have drained the stage.
+    if (warp < PRODUCERS / 32) {
+        const float4 *records = reinterpret_cast<const float4 *>(prm.records) + pl0 * R;
+        const int q = tid >> 2, j = tid & 3;
+        Rec2 r0, r1, r2;  // records prefetched three k-steps ahead
+        load_rec(r0, records, R, q, nq, 0, j);
+        if (NK > 1) load_rec(r1, records, R, q, nq, 1, j);
+        if (NK > 2) load_rec(r2, records, R, q, nq, 2, j);
+        auto produce = [&](int c, Rec2 &rv) {
+            const int s = c % STAGES, u = c / STAGES;
+            if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
+            stage_b(stages + s * STAGE, rv, q, j);
+            fence_async_smem();  // generic-proxy stores -> visible to the tensor core
+            mbar_arrive(&b_full[s]);
+            if (c + 3 < NK) load_rec(rv, records, R, q, nq, c + 3, j);
+        };
 #pragma unroll 1
-    for (int c = 0; c < NK; ++c) {
-        float *st = stages + (c % STAGES) * STAGE;
-        if (c >= 2) mbar_wait(&bars[(c - 2) % STAGES], ((c - 2) / STAGES) & 1);
-        if (c + 2 < NK) issue_a(stages + ((c + 2) % STAGES) * STAGE, img, c + 2, tid);
-        if (c + 3 < NK) issue_raw(ring + ((c + 3) % RING) * RAW, records, R, q, nq, c + 3, j);
-        cp_async_commit();
-        cp_async_wait<2>();
-        stage_b(st, ring + (c % RING) * RAW, q, nq, j);  // own raw records: no barrier needed
-        fence_async_smem();
-        __syncthreads();
-        if (tid == 0) {
-            tc_fence_after();
-            issue_mma(st, tmem, c);
-            mma_commit(&bars[c % STAGES]);
+        for (int c = 0; c < NK; c += 3) {
+            produce(c, r0);
+            if (c + 1 < NK) produce(c + 1, r1);
+            if (c + 2 < NK) produce(c + 2, r2);
         }
+    } else if (warp == 4) {
+        if (lane == 0) {
+#pragma unroll 1
+            for (int c = 0; c < NK; ++c) {
+                const int s = c % STAGES, u = c / STAGES;
+                mbar_wait(&a_full[s], u & 1);
+                mbar_wait(&b_full[s], u & 1);
+                tc_fence_after();
+                issue_mma(stages + s * STAGE, tmem, c);
+                mma_commit(&empty[s]);
+            }
+            mma_commit(&done);  // arrives once every MMA of the CTA has completed
+        }
+        __syncwarp();
+    } else if (warp == 5) {
+        if (lane == 0) {
+#pragma unroll 1
+            for (int c = 0; c < NK; ++c) {
+                const int s = c % STAGES, u = c / STAGES;
+                if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
+                mbar_expect_tx(&a_full[s], A_FLOATS * 4);
+                bulk_g2s(stages + s * STAGE, prm.w_image + size_t(c) * A_FLOATS, A_FLOATS * 4,
+                         &a_full[s]);
+            }
+        }
+        __syncwarp();
     }
-    mbar_wait(&bars[(NK - 1) % STAGES], ((NK - 1) / STAGES) & 1);  // every MMA has completed
-    cp_async_wait<0>();
+    // (a parity wait on a stage barrier could alias a phase two behind: use `done`)
+    mbar_wait(&done, 0);
     tc_fence_after();
 
     // ---- epilogue: TMEM -> state + quantised cores (staged in the freed stages) -----------
@@ -354,43 +379,42 @@ __global__ void __launch_bounds__(THREADS, 1) blend_tc_kernel(ps_trace_params pr
             }
         }
     }
-    if (sub < 2) {  // colour: TMEM lanes 0-63 are the 64 texels; warp half h owns 32 probes
+    if (sub < 2) {  // colour: TMEM lanes 0-63 are the 64 texels; warp half h owns P/2 probes
         const int t = sub * 32 + lane;
         const float inv = __ldg(prm.inv_wsum + t);
         const uint32_t base = lane_base + COL_C;
         const bool need_old = inv == 0.f || h != 0.f;
-#pragma unroll 1
-        for (int q0 = half * 32; q0 < half * 32 + 32; q0 += 16) {
-            float old[16][3];
+        const int q0 = half * (P / 2);
+        static_assert(P / 2 == 16, "one 16-column TMEM load per channel");
+        float old[16][3];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const float *st = prm.irradiance + ((pl0 + q0 + i) * 64 + t) * 3;
-                const bool ld = need_old && q0 + i < nq;
+        for (int i = 0; i < 16; ++i) {
+            const float *st = prm.irradiance + ((pl0 + q0 + i) * 64 + t) * 3;
+            const bool ld = need_old && q0 + i < nq;
 #pragma unroll
-                for (int ch = 0; ch < 3; ++ch) old[i][ch] = ld ? __ldcs(st + ch) : 0.f;
+            for (int ch = 0; ch < 3; ++ch) old[i][ch] = ld ? __ldcs(st + ch) : 0.f;
+        }
+        float cr[16], cg[16], cb[16];
+        tmem_ld16(base + q0, cr);
+        tmem_ld16(base + P + q0, cg);
+        tmem_ld16(base + 2 * P + q0, cb);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int qq = q0 + i;
+            if (qq >= nq) break;
+            float *st = prm.irradiance + ((pl0 + qq) * 64 + t) * 3;
+            const float acc[3] = {cr[i], cg[i], cb[i]};
+            uint32_t texel = 0;
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) {
+                float v = acc[ch] * inv;
+                if (inv == 0.f) v = old[i][ch];  // no ray sees this texel: keep the state
+                else if (h != 0.f) v = fmaf(h, old[i][ch] - v, v);
+                __stcs(st + ch, v);
+                const float x = fminf(fmaxf(v * qs, 0.0f), 1.0f);
+                texel |= __float2uint_rn(x * 1023.0f) << (10 * ch);
             }
-            float cr[16], cg[16], cb[16];
-            tmem_ld16(base + q0, cr);
-            tmem_ld16(base + P + q0, cg);
-            tmem_ld16(base + 2 * P + q0, cb);
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const int qq = q0 + i;
-                if (qq >= nq) break;
-                float *st = prm.irradiance + ((pl0 + qq) * 64 + t) * 3;
-                const float acc[3] = {cr[i], cg[i], cb[i]};
-                uint32_t texel = 0;
-#pragma unroll
-                for (int ch = 0; ch < 3; ++ch) {
-                    float v = acc[ch] * inv;
-                    if (inv == 0.f) v = old[i][ch];  // no ray sees this texel: keep the state
-                    else if (h != 0.f) v = fmaf(h, old[i][ch] - v, v);
-                    __stcs(st + ch, v);
-                    const float x = fminf(fmaxf(v * qs, 0.0f), 1.0f);
-                    texel |= __float2uint_rn(x * 1023.0f) << (10 * ch);
-                }
-                s_ccore[qq * 64 + t] = texel;
-            }
+            s_ccore[qq * 64 + t] = texel;
         }
     }
     tc_fence_before();
