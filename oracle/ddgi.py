@@ -228,19 +228,53 @@ def shade(tris, albedo, emission, lights, sky, origins, dirs, t, prim, max_dista
 # --- blend (float32) ----------------------------------------------------------------------
 
 
+def tf32_trunc(x: np.ndarray) -> np.ndarray:
+    """float32 with the low 13 mantissa bits cleared (a tf32 number)."""
+    x = np.ascontiguousarray(x, np.float32)
+    return (x.view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32)
+
+
 def blend_weights(dirs32: np.ndarray, sharpness: float):
-    """(Wc (64,R), Wd (256,R), inv_c (64,), inv_d (256,)) in float32."""
+    """(Wc (64,R), Wd (256,R), inv_c (64,), inv_d (256,)) in float32.
+
+    The weights are tf32 numbers by definition (low 13 mantissa bits
+    cleared), so the device blend can run exactly on tf32 tensor cores with
+    only the probe channels split hi + lo."""
     tc = texel_directions(8).astype(np.float32)
     td = texel_directions(16).astype(np.float32)
     d = np.asarray(dirs32, np.float32)[:, :3]
-    wc = np.maximum(tc @ d.T, np.float32(0))
-    wd = np.power(np.maximum(td @ d.T, np.float32(0)), np.float32(sharpness))
+    wc = tf32_trunc(np.maximum(tc @ d.T, np.float32(0)))
+    wd = tf32_trunc(np.power(np.maximum(td @ d.T, np.float32(0)), np.float32(sharpness)))
     inv = []
     for w in (wc, wd):
         s = w.sum(axis=1, dtype=np.float32)
         with np.errstate(divide="ignore"):
             inv.append(np.where(s > 0, np.float32(1) / s, np.float32(0)).astype(np.float32))
     return wc, wd, inv[0], inv[1]
+
+
+def weights_from(wc: np.ndarray, wd: np.ndarray):
+    """The blend_weights tuple for given (64,R) / (256,R) float32 weights."""
+    inv = []
+    for w in (wc, wd):
+        s = w.sum(axis=1, dtype=np.float32)
+        with np.errstate(divide="ignore"):
+            inv.append(np.where(s > 0, np.float32(1) / s, np.float32(0)).astype(np.float32))
+    return wc, wd, inv[0], inv[1]
+
+
+def check_device_weights(w_color_dev: np.ndarray, w_depth_dev: np.ndarray, dirs32, sharpness):
+    """Device weight tables ((R,64), (R,256)) against blend_weights: equal to
+    within one tf32 ulp (the fp32 cosine / pow may round differently before
+    the truncation).  Returns the weights tuple built from the device tables,
+    so the blend itself is checked on identical weights."""
+    wc_o, wd_o, _, _ = blend_weights(dirs32, sharpness)
+    wc, wd = np.ascontiguousarray(w_color_dev.T), np.ascontiguousarray(w_depth_dev.T)
+    for a, b in ((wc, wc_o), (wd, wd_o)):
+        assert np.array_equal(a, tf32_trunc(a)), "device weights are not tf32 numbers"
+        np.testing.assert_allclose(a, b, rtol=2.0 ** -9, atol=1e-30)
+        assert np.mean(a != b) < 1e-2
+    return weights_from(wc, wd)
 
 
 def blend(rgb32, depth32, weights, prev_irr, prev_mom, hysteresis):

@@ -13,21 +13,23 @@
 // all three accumulators (64 + 64 + 96 = 224 of a 256-column allocation), so
 // two CTAs share an SM and one's epilogue overlaps the other's MMAs.
 //
-// Precision (parity bar: 1e-4 relative vs the fp32 oracle): fp32 operands
-// are split x = hi + lo with hi = x with its low 13 mantissa bits cleared
-// (exactly representable in tf32) and lo = x - hi (exact in fp32), and every
-// product is issued as A_hi*B_hi + A_hi*B_lo + A_lo*B_hi ("3xTF32"): the
-// dropped A_lo*B_lo term and the tf32 truncation of the lo parts are
-// <= 2^-21 relative, so the result is fp32-accurate.
+// Precision (parity bar: 1e-4 relative vs the fp32 oracle): the weights are
+// tf32 numbers by definition (the weights pass clears their low 13 mantissa
+// bits; oracle/ddgi.py does the same), and each fp32 probe channel is split
+// x = hi + lo, hi = x with its low 13 mantissa bits cleared (exact in tf32),
+// lo = x - hi (exact in fp32).  Every product is issued as W*B_hi + W*B_lo:
+// only the tf32 truncation of lo is lost (<= 2^-21 relative), so the result
+// is fp32-accurate with two MMAs per tile.
 //
 // Warp-specialised pipeline over k-steps of 8 rays, 3 shared-memory stages
-// of 34 KB, mbarriers between the roles:
-//   * warp 5 (one thread) streams the weights (6 operand images hi/lo,
-//     24 KB per k-step) with TMA bulk copies from a per-frame image the
-//     weights pass writes in the canonical K-major no-swizzle UMMA layout;
-//   * warps 0-3 convert the ray records (prefetched three k-steps ahead in
-//     registers) into the B images (channels d, d^2, r, g, b), hi and lo;
-//   * warp 4 (one thread) issues 9 MMAs per k-step (3 tiles x 3 terms) and
+// of 22 KB, mbarriers between the roles:
+//   * warp 5 (one thread) streams the weights (3 operand images, 12 KB per
+//     k-step) with TMA bulk copies from a per-frame image the weights pass
+//     writes in the canonical K-major no-swizzle UMMA layout;
+//   * warps 0-3 stream their ray records through a cp.async ring (7 k-steps
+//     ahead) and convert them into the B images (channels d, d^2, r, g, b),
+//     hi and lo;
+//   * warp 4 (one thread) issues 6 MMAs per k-step (3 tiles x 2 terms) and
 //     commits them to the stage's "empty" barrier.
 // The epilogue reads the accumulators with tcgen05.ld (one texel per TMEM
 // lane), applies the normalisation / hysteresis / quantisation of the
@@ -49,13 +51,16 @@ constexpr int THREADS = 256;  // warps 0-3 convert records, 4 issues MMAs, 5 loa
 constexpr int PRODUCERS = 128;
 constexpr int STAGES = 3;
 constexpr int PART = 128 * 8;                 // floats of one 128-row x 8-k operand image
-constexpr int A_FLOATS = 6 * PART;            // d0 hi, d1 hi, c hi, d0 lo, d1 lo, c lo
+constexpr int A_FLOATS = 3 * PART;            // depth tile 0, depth tile 1, colour
 constexpr int BD_ROWS = 2 * P;                // d (probe q) then d^2 (probe q)
 constexpr int BC_ROWS = 3 * P;                // r, g, b
 constexpr int BD = BD_ROWS * 8;               // floats of one depth B image
 constexpr int BC = BC_ROWS * 8;
-constexpr int STAGE = A_FLOATS + 2 * BD + 2 * BC;  // 8704 floats = 34 KB
-constexpr size_t SMEM_BYTES = size_t(STAGES) * STAGE * 4 + 1024;
+constexpr int STAGE = A_FLOATS + 2 * BD + 2 * BC;  // 5632 floats = 22 KB
+constexpr uint32_t A_LOAD_BYTES = (2 * PART + 2 * 256) * 4;  // colour rows 64-127 stay zero
+constexpr int RAW = P * 8 * 4;  // floats of one k-step's raw ray records (4 KB)
+constexpr int RING = 8;         // raw record ring: records stream RING - 1 k-steps ahead
+constexpr size_t SMEM_BYTES = (size_t(STAGES) * STAGE + size_t(RING) * RAW) * 4 + 1024;
 constexpr uint32_t COL_D0 = 0, COL_D1 = BD_ROWS, COL_C = 2 * BD_ROWS, TMEM_COLS = 256;
 
 static_assert(COL_C + BC_ROWS <= TMEM_COLS, "accumulators must fit the TMEM allocation");
@@ -116,6 +121,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         : "memory");
 }
 
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 __device__ __forceinline__ void fence_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -145,7 +159,8 @@ __device__ __forceinline__ float tf32_hi(float x) {
     return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
 }
 
-// weights pass: the per-frame A image, (R/8) k-steps x 6 operand images
+// weights pass: the per-frame A image, (R/8) k-steps x 3 operand images of the
+// (already tf32) weights
 __global__ void weight_image_kernel(const float *w_color, const float *w_depth, int R,
                                     float *img) {
     const int total = (R / 8) * A_FLOATS;
@@ -157,14 +172,12 @@ __global__ void weight_image_kernel(const float *w_color, const float *w_depth, 
         const int m = (in >> 5) * 8 + ((in & 31) >> 2);
         const int k = kh * 4 + (in & 3);
         const int r = s * 8 + k;
-        const int tile = part % 3;
         float w = 0.f;
-        if (tile == 2)
+        if (part == 2)
             w = m < 64 ? w_color[r * 64 + m] : 0.f;
         else
-            w = w_depth[r * 256 + tile * 128 + m];
-        const float hi = tf32_hi(w);
-        img[i] = part < 3 ? hi : w - hi;
+            w = w_depth[r * 256 + part * 128 + m];
+        img[i] = w;
     }
 }
 
@@ -188,20 +201,32 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
         : "memory");
 }
 
-// one producer thread's share of a k-step: rays (8c + 2j, 8c + 2j + 1) of probe q
+// one producer thread's share of a k-step: rays (8c + 2j, 8c + 2j + 1) of probe q,
+// copied raw (2 float4) into its ring slot
+__device__ __forceinline__ void issue_raw(float *slot, const float4 *records, int R, int q,
+                                          int nq, int c, int j) {
+    if (q < nq) {
+        const float4 *src = records + size_t(q) * R + c * 8 + 2 * j;
+        float *dst = slot + (q * 8 + 2 * j) * 4;
+        cp_async16(dst, src);
+        cp_async16(dst + 4, src + 1);
+    }
+}
+
 struct Rec2 {
     float4 a, b;
 };
 
-__device__ __forceinline__ void load_rec(Rec2 &v, const float4 *records, int R, int q, int nq,
-                                         int c, int j) {
+__device__ __forceinline__ Rec2 read_raw(const float *slot, int q, int nq, int j) {
+    Rec2 v;
     if (q < nq) {
-        const float4 *p = records + size_t(q) * R + c * 8 + 2 * j;
-        v.a = __ldcs(p);
-        v.b = __ldcs(p + 1);
+        const float4 *src = reinterpret_cast<const float4 *>(slot) + q * 8 + 2 * j;
+        v.a = src[0];
+        v.b = src[1];
     } else {
         v.a = v.b = make_float4(0.f, 0.f, 0.f, 0.f);
     }
+    return v;
 }
 
 __device__ __forceinline__ void put2(float *img, int rows, int m, int k, float x0, float x1) {
@@ -236,16 +261,14 @@ __device__ __forceinline__ void issue_mma(const float *st, uint32_t tmem, int c)
     const uint64_t b_ch = smem_desc(bch, BC_ROWS), b_cl = smem_desc(bcl, BC_ROWS);
 #pragma unroll
     for (int t = 0; t < 2; ++t) {  // depth tiles (texels 0-127, 128-255)
-        const uint64_t ah = smem_desc(a + t * PART, 128), al = smem_desc(a + (3 + t) * PART, 128);
+        const uint64_t aw = smem_desc(a + t * PART, 128);
         const uint32_t d = tmem + (t ? COL_D1 : COL_D0);
-        mma_tf32(d, ah, b_dh, ID_D, acc);
-        mma_tf32(d, ah, b_dl, ID_D, 1u);
-        mma_tf32(d, al, b_dh, ID_D, 1u);
+        mma_tf32(d, aw, b_dh, ID_D, acc);
+        mma_tf32(d, aw, b_dl, ID_D, 1u);
     }
-    const uint64_t ah = smem_desc(a + 2 * PART, 128), al = smem_desc(a + 5 * PART, 128);
-    mma_tf32(tmem + COL_C, ah, b_ch, ID_C, acc);
-    mma_tf32(tmem + COL_C, ah, b_cl, ID_C, 1u);
-    mma_tf32(tmem + COL_C, al, b_ch, ID_C, 1u);
+    const uint64_t aw = smem_desc(a + 2 * PART, 128);
+    mma_tf32(tmem + COL_C, aw, b_ch, ID_C, acc);
+    mma_tf32(tmem + COL_C, aw, b_cl, ID_C, 1u);
 }
 
 __global__ void __launch_bounds__(THREADS, 2) blend_tc_kernel(ps_trace_params prm) {
@@ -277,6 +300,13 @@ __global__ void __launch_bounds__(THREADS, 2) blend_tc_kernel(ps_trace_params pr
                      "r"(TMEM_COLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
+    for (int i = tid; i < STAGES * 2 * 64; i += THREADS) {  // colour A rows 64-127: zero
+        const int st = i / 128, r = i % 128;
+        float4 *z = reinterpret_cast<float4 *>(stages + st * STAGE + 2 * PART + 256 +
+                                               (r >> 6) * 512) + (r & 63);
+        *z = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    fence_async_smem();
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -287,26 +317,30 @@ __global__ void __launch_bounds__(THREADS, 2) blend_tc_kernel(ps_trace_params pr
     // probe channels of k-step c are in place; empty completes phase u when the MMAs of
     // k-step c have drained the stage.
     if (warp < PRODUCERS / 32) {
+        // each thread streams its own 32 B of every k-step through the raw ring (no
+        // cross-thread hand-off), RING - 1 k-steps ahead of its conversion
         const float4 *records = reinterpret_cast<const float4 *>(prm.records) + pl0 * R;
+        float *ring = stages + STAGES * STAGE;
         const int q = tid >> 2, j = tid & 3;
-        Rec2 r0, r1, r2;  // records prefetched three k-steps ahead
-        load_rec(r0, records, R, q, nq, 0, j);
-        if (NK > 1) load_rec(r1, records, R, q, nq, 1, j);
-        if (NK > 2) load_rec(r2, records, R, q, nq, 2, j);
-        auto produce = [&](int c, Rec2 &rv) {
+#pragma unroll
+        for (int c = 0; c < RING - 1; ++c) {
+            if (c < NK) issue_raw(ring + c * RAW, records, R, q, nq, c, j);
+            cp_async_commit();
+        }
+#pragma unroll 1
+        for (int c = 0; c < NK; ++c) {
             const int s = c % STAGES, u = c / STAGES;
+            if (c + RING - 1 < NK)
+                issue_raw(ring + ((c + RING - 1) % RING) * RAW, records, R, q, nq, c + RING - 1, j);
+            cp_async_commit();
+            cp_async_wait<RING - 1>();  // k-step c's records have landed
+            const Rec2 rv = read_raw(ring + (c % RING) * RAW, q, nq, j);
             if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
             stage_b(stages + s * STAGE, rv, q, j);
             fence_async_smem();  // generic-proxy stores -> visible to the tensor core
             mbar_arrive(&b_full[s]);
-            if (c + 3 < NK) load_rec(rv, records, R, q, nq, c + 3, j);
-        };
-#pragma unroll 1
-        for (int c = 0; c < NK; c += 3) {
-            produce(c, r0);
-            if (c + 1 < NK) produce(c + 1, r1);
-            if (c + 2 < NK) produce(c + 2, r2);
         }
+        cp_async_wait<0>();
     } else if (warp == 4) {
         if (lane == 0) {
 #pragma unroll 1
@@ -327,9 +361,14 @@ __global__ void __launch_bounds__(THREADS, 2) blend_tc_kernel(ps_trace_params pr
             for (int c = 0; c < NK; ++c) {
                 const int s = c % STAGES, u = c / STAGES;
                 if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
-                mbar_expect_tx(&a_full[s], A_FLOATS * 4);
-                bulk_g2s(stages + s * STAGE, prm.w_image + size_t(c) * A_FLOATS, A_FLOATS * 4,
-                         &a_full[s]);
+                // depth tiles (8 KB) + the 64 live rows of each k half of the colour tile
+                // (its rows 64-127 are zero in every stage since the prologue)
+                float *dst = stages + s * STAGE;
+                const float *src = prm.w_image + size_t(c) * A_FLOATS;
+                mbar_expect_tx(&a_full[s], A_LOAD_BYTES);
+                bulk_g2s(dst, src, 2 * PART * 4, &a_full[s]);
+                bulk_g2s(dst + 2 * PART, src + 2 * PART, 256 * 4, &a_full[s]);
+                bulk_g2s(dst + 2 * PART + 512, src + 2 * PART + 512, 256 * 4, &a_full[s]);
             }
         }
         __syncwarp();

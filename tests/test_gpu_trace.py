@@ -93,7 +93,8 @@ def _check_trace(upd, sc, frame, max_mismatch=2e-3):
 
 def _check_blend(upd, prev_irr, prev_mom, h):
     rgb, depth, *_ = _records(upd)
-    w = ddgi.blend_weights(upd.ray_dirs.cpu().numpy(), upd.sharpness)
+    w = ddgi.check_device_weights(upd.w_color.cpu().numpy(), upd.w_depth.cpu().numpy(),
+                                  upd.ray_dirs.cpu().numpy(), upd.sharpness)
     irr, mom = ddgi.blend(rgb, depth, w, prev_irr, prev_mom, h)
     g_irr = upd.irradiance.cpu().numpy()
     g_mom = upd.moments.cpu().numpy()
