@@ -212,6 +212,13 @@ def run_ours(args, rank, world, local):
     # ---- per-stage device times + launch count (untimed instrumented frames) ---------
     base = args.warmup + 2 * args.steps + 1
     stages = server.stage_times(3, base, frame_lights)
+    rank_trace = [stages.get("trace_blend", 0.0)]
+    if world > 1:
+        t = torch.tensor([rank_trace[0]], device=dev, dtype=torch.float64)
+        allt = torch.zeros(world, device=dev, dtype=torch.float64)
+        dist.all_gather_into_tensor(allt, t)
+        rank_trace = [round(v, 4) for v in allt.cpu().tolist()]
+    slabs = getattr(server.impl, "ranges", None)
     launches_per_step, kernel_names = server.count_launches(base + 3, frame_lights)
     encode = server.encode_times() if world == 1 else {}
 
@@ -251,6 +258,8 @@ def run_ours(args, rank, world, local):
             if hasattr(server.impl, "updater") else "map",
             "l2": "per-frame working set (atlases, float state, planes) > 126 MB L2; no flush",
             "parallelism": f"z-slab x{world}",
+            "slabs": ([[int(b), int(e)] for b, e in slabs] if slabs and world > 1 else None),
+            "rank_trace_blend_ms": rank_trace if world > 1 else None,
             "launch": "eager" if args.eager else "CUDA graphs (trace+blend, one chain per kind)",
         },
         "grays_per_s": round(rays_total / (ms_max / 1e3) / 1e9, 4),

@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define PS_ABI_VERSION 3
+#define PS_ABI_VERSION 4
 
 /* status codes */
 #define PS_OK 0
@@ -316,6 +316,12 @@ typedef struct ps_trace_params {
     int32_t shadow_map_size; /* cube face side S (PS_SHADOW_MAP)              */
     float *shadow_maps;      /* light_count * 6 * S * S distances (scratch)   */
     float shadow_bias;       /* relative slack of the map depth compare       */
+    /* map texels [shadow_texel_begin, shadow_texel_end) of the flattened
+     * (light, face, j, i) maps are traced (end 0 = all): ranks of a sharded
+     * frame each trace a slice and all-gather the maps */
+    int64_t shadow_texel_begin, shadow_texel_end;
+    /* passes to run: bit 0 shadow maps, bit 1 probe rays, bit 2 blend; 0 = all */
+    int32_t passes;
     /* blend */
     const float *w_color;    /* (rays, 64) cosine weights, transposed       */
     const float *w_depth;    /* (rays, 256) cosine^sharpness weights        */

@@ -16,7 +16,7 @@ from pathlib import Path
 from .errors import LayoutMismatchError, NativeLibraryError, SlotOverflowError
 
 LIB_PATH = Path(os.environ.get("PROBESTREAM_LIB", Path(__file__).resolve().parent / "libprobestream.so"))
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 PS_OK = 0
 PS_ERR_VALUE = -1
@@ -56,6 +56,7 @@ class TraceParams(C.Structure):
         ("sky", _f32 * 3), ("max_distance", _f32), ("normal_bias", _f32),
         ("shadow_mode", _i32), ("shadow_map_size", _i32), ("shadow_maps", _vp),
         ("shadow_bias", _f32),
+        ("shadow_texel_begin", _i64), ("shadow_texel_end", _i64), ("passes", _i32),
         ("w_color", _vp), ("w_depth", _vp), ("inv_wsum", _vp), ("w_image", _vp),
         ("hysteresis", _f32), ("irradiance_scale", _f32),
         ("irradiance", _vp), ("moments", _vp),

@@ -160,11 +160,13 @@ template <int WIDTH>
 __global__ void __launch_bounds__(256) shadow_map_kernel(ps_trace_params prm) {
     const int S = prm.shadow_map_size;
     const int64_t per_light = int64_t(6) * S * S;
-    const int64_t total = per_light * prm.light_count;
+    const int64_t all = per_light * prm.light_count;
+    const int64_t total = prm.shadow_texel_end > 0 && prm.shadow_texel_end < all
+                              ? prm.shadow_texel_end : all;
     const float4 *nodes = reinterpret_cast<const float4 *>(prm.nodes);
     const float4 *tris = reinterpret_cast<const float4 *>(prm.tris);
-    for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
-         idx += int64_t(gridDim.x) * blockDim.x) {
+    for (int64_t idx = prm.shadow_texel_begin + blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+         idx < total; idx += int64_t(gridDim.x) * blockDim.x) {
         const int l = int(idx / per_light);
         const int rem = int(idx - int64_t(l) * per_light);
         const int f = rem / (S * S);
@@ -191,8 +193,13 @@ __global__ void __launch_bounds__(256) shadow_map_kernel(ps_trace_params prm) {
 // the coherence-ordered set) from a global counter, traces + shades them and
 // writes {rgb, depth}.  Dynamic claiming keeps every SM busy regardless of the
 // large per-direction cost differences.
-template <int SHADOW, int LEAFV, int MINB, int PROBE_PARALLEL, int WIDTH>
-__global__ void __launch_bounds__(THREADS, MINB) trace_kernel(ps_trace_params prm) {
+// TPB = 1024 is the "SM-sized" launch used when SMs are reserved for
+// concurrent streams: one CTA fills an SM (64 registers x 1024 threads), so a
+// grid of sms - reserve CTAs leaves whole SMs free (a grid of 256-thread CTAs
+// would be spread over every SM and leave only fragments, too small for NCCL's
+// kernels).  The kernel is per-warp, so the block size is free.
+template <int SHADOW, int LEAFV, int MINB, int PROBE_PARALLEL, int WIDTH, int TPB = THREADS>
+__global__ void __launch_bounds__(TPB, TPB == THREADS ? MINB : 1) trace_kernel(ps_trace_params prm) {
     const float4 *nodes = reinterpret_cast<const float4 *>(prm.nodes);
     const float4 *tris = reinterpret_cast<const float4 *>(prm.tris);
     const float4 *dirs = reinterpret_cast<const float4 *>(prm.ray_dirs);
@@ -662,7 +669,11 @@ int resident_blocks(K kernel, int threads, size_t smem) {
 }
 
 template <int SHADOW, int LEAFV, int MINB, int PP, int WIDTH>
-void launch_trace_t(const ps_trace_params &p, int sms, cudaStream_t s) {
+void launch_trace_t(const ps_trace_params &p, int sms, cudaStream_t s, bool sm_sized) {
+    if (sm_sized) {
+        trace_kernel<SHADOW, LEAFV, MINB, PP, WIDTH, 1024><<<sms, 1024, 0, s>>>(p);
+        return;
+    }
     const int per_sm = resident_blocks(trace_kernel<SHADOW, LEAFV, MINB, PP, WIDTH>, THREADS, 0);
     trace_kernel<SHADOW, LEAFV, MINB, PP, WIDTH><<<sms * per_sm, THREADS, 0, s>>>(p);
 }
@@ -674,39 +685,39 @@ void launch_trace_ww(const ps_trace_params &p, int sms, cudaStream_t s) {
 }
 
 template <int SHADOW>
-void launch_trace_s(const ps_trace_params &p, int variant, int sms, cudaStream_t s) {
+void launch_trace_s(const ps_trace_params &p, int variant, int sms, cudaStream_t s, bool big) {
     if (p.bvh_width == 5) {
         switch (variant) {
-            case 11: launch_trace_t<SHADOW, 1, 4, 0, 5>(p, sms, s); break;
-            default: launch_trace_t<SHADOW, 1, 1, 0, 5>(p, sms, s); break;
+            case 11: launch_trace_t<SHADOW, 1, 4, 0, 5>(p, sms, s, big); break;
+            default: launch_trace_t<SHADOW, 1, 1, 0, 5>(p, sms, s, big); break;
         }
         return;
     }
     if (p.bvh_width == 4) {
         switch (variant) {
-            case 0: launch_trace_t<SHADOW, 0, 1, 0, 4>(p, sms, s); break;
-            case 10: launch_trace_t<SHADOW, 0, 4, 0, 4>(p, sms, s); break;
-            case 11: launch_trace_t<SHADOW, 1, 4, 0, 4>(p, sms, s); break;
-            case 30: launch_trace_t<SHADOW, 1, 1, 1, 4>(p, sms, s); break;
-            default: launch_trace_t<SHADOW, 1, 1, 0, 4>(p, sms, s); break;
+            case 0: launch_trace_t<SHADOW, 0, 1, 0, 4>(p, sms, s, big); break;
+            case 10: launch_trace_t<SHADOW, 0, 4, 0, 4>(p, sms, s, big); break;
+            case 11: launch_trace_t<SHADOW, 1, 4, 0, 4>(p, sms, s, big); break;
+            case 30: launch_trace_t<SHADOW, 1, 1, 1, 4>(p, sms, s, big); break;
+            default: launch_trace_t<SHADOW, 1, 1, 0, 4>(p, sms, s, big); break;
         }
         return;
     }
     switch (variant) {
         case 20: launch_trace_ww<SHADOW, 1>(p, sms, s); break;
         case 22: launch_trace_ww<SHADOW, 4>(p, sms, s); break;
-        case 30: launch_trace_t<SHADOW, 1, 1, 1, 2>(p, sms, s); break;
-        case 0: launch_trace_t<SHADOW, 0, 1, 0, 2>(p, sms, s); break;
-        case 10: launch_trace_t<SHADOW, 0, 4, 0, 2>(p, sms, s); break;
-        default: launch_trace_t<SHADOW, 1, 1, 0, 2>(p, sms, s); break;
+        case 30: launch_trace_t<SHADOW, 1, 1, 1, 2>(p, sms, s, big); break;
+        case 0: launch_trace_t<SHADOW, 0, 1, 0, 2>(p, sms, s, big); break;
+        case 10: launch_trace_t<SHADOW, 0, 4, 0, 2>(p, sms, s, big); break;
+        default: launch_trace_t<SHADOW, 1, 1, 0, 2>(p, sms, s, big); break;
     }
 }
 
-void launch_trace(const ps_trace_params &p, int variant, int sms, cudaStream_t s) {
+void launch_trace(const ps_trace_params &p, int variant, int sms, cudaStream_t s, bool big) {
     switch (p.shadow_mode) {
-        case PS_SHADOW_NONE: launch_trace_s<PS_SHADOW_NONE>(p, variant, sms, s); break;
-        case PS_SHADOW_RAYS: launch_trace_s<PS_SHADOW_RAYS>(p, variant, sms, s); break;
-        default: launch_trace_s<PS_SHADOW_MAP>(p, variant, sms, s); break;
+        case PS_SHADOW_NONE: launch_trace_s<PS_SHADOW_NONE>(p, variant, sms, s, big); break;
+        case PS_SHADOW_RAYS: launch_trace_s<PS_SHADOW_RAYS>(p, variant, sms, s, big); break;
+        default: launch_trace_s<PS_SHADOW_MAP>(p, variant, sms, s, big); break;
     }
     check_launch("trace_kernel");
 }
@@ -764,13 +775,19 @@ int ps_trace_blend(const ps_trace_params *params, void *stream) {
         fail(PS_ERR_VALUE, "shadow map size / buffer missing");
     if (!p.records || !p.work_counter) fail(PS_ERR_VALUE, "records / work_counter scratch missing");
     const int64_t nloc = p.probe_end - p.probe_begin;
-    if (nloc == 0) return PS_OK;
     auto s = as_stream(stream);
     const int sms = sm_count();
+    const int passes = p.passes ? p.passes : 7;
+    if (p.shadow_texel_begin < 0 || p.shadow_texel_end < 0 ||
+        (p.shadow_texel_end > 0 && p.shadow_texel_end < p.shadow_texel_begin))
+        fail(PS_ERR_VALUE, "bad shadow texel range");
     // pass 0: shadow maps
-    if (p.shadow_mode == PS_SHADOW_MAP && p.light_count > 0) {
-        const int64_t texels = int64_t(p.light_count) * 6 * p.shadow_map_size * p.shadow_map_size;
-        const unsigned blocks = unsigned(std::min<int64_t>(ceil_div(texels, 256), int64_t(sms) * 32));
+    if ((passes & 1) && p.shadow_mode == PS_SHADOW_MAP && p.light_count > 0) {
+        const int64_t all = int64_t(p.light_count) * 6 * p.shadow_map_size * p.shadow_map_size;
+        const int64_t end = p.shadow_texel_end > 0 && p.shadow_texel_end < all ? p.shadow_texel_end : all;
+        const int64_t texels = end > p.shadow_texel_begin ? end - p.shadow_texel_begin : 0;
+        const unsigned blocks = unsigned(std::max<int64_t>(
+            1, std::min<int64_t>(ceil_div(texels, 256), int64_t(sms) * 32)));
         if (p.bvh_width == 5)
             shadow_map_kernel<5><<<blocks, 256, 0, s>>>(p);
         else if (p.bvh_width == 4)
@@ -779,9 +796,10 @@ int ps_trace_blend(const ps_trace_params *params, void *stream) {
             shadow_map_kernel<2><<<blocks, 256, 0, s>>>(p);
         check_launch("shadow_map_kernel");
     }
+    if (nloc == 0) return PS_OK;
     // pass 1: persistent trace with dynamic chunk claiming
-    check_cuda(cudaMemsetAsync(p.work_counter, 0, sizeof(uint32_t), s), "memset counter");
-    {
+    if (passes & 2) {
+        check_cuda(cudaMemsetAsync(p.work_counter, 0, sizeof(uint32_t), s), "memset counter");
         // PS_TRACE_VARIANT (tuning knob): leaf fetch 0 = sequential, 1 = pairs,
         // 2 = four in flight; +10 = cap registers for 4 resident CTAs per SM
         static const int variant = [] {
@@ -789,8 +807,9 @@ int ps_trace_blend(const ps_trace_params *params, void *stream) {
             return e ? atoi(e) : 1;
         }();
         const int keep = p.reserve_sms > 0 && p.reserve_sms < sms / 2 ? p.reserve_sms : 0;
-        launch_trace(p, variant, sms - keep, s);
+        launch_trace(p, variant, sms - keep, s, keep > 0);
     }
+    if (!(passes & 4)) return PS_OK;
     // pass 2: blend -- tcgen05 tensor cores (ps_blend_tc.cu), or the CUDA-core kernel
     if (blend_tc_usable(p)) {
         launch_blend_tc(p, nloc, s);

@@ -25,6 +25,8 @@ The encoder rank's outputs are bit-identical to the single-GPU pipeline's
 
 from __future__ import annotations
 
+import os
+
 import torch
 import torch.distributed as dist
 
@@ -33,9 +35,15 @@ from . import _native as N
 from .delta import pack_delta, skip_shape
 from .packing import UpdateAtlasLayout, widened_width
 from .probes import ProbeUpdater
+from .scene import DeviceScene
 from .selection import detect_changed_device, select_device
 from .server import DEFAULT_GOP, RESERVE_SMS, KindOutput
 from .volume import AtlasKind, ProbeAtlas
+
+
+def _env_flag(name: str, default: bool) -> bool:
+    v = os.environ.get(name)
+    return default if v is None else v not in ("0", "false", "no", "")
 
 
 def slab_range(volume, rank: int, world: int):
@@ -43,6 +51,71 @@ def slab_range(volume, rank: int, world: int):
     nx, ny, nz = volume.dims
     plane = nx * ny
     return (nz * rank) // world * plane, (nz * (rank + 1)) // world * plane
+
+
+def ranges_from_cost(n_units: int, unit: int, world: int, unit_cost) -> list:
+    """Contiguous probe ranges of whole units (rows of nx probes) with
+    near-equal summed cost; every rank gets at least one unit."""
+    cost = [max(float(c), 1e-12) for c in unit_cost]
+    total = sum(cost)
+    cuts, acc, k = [0], 0.0, 0
+    for r in range(1, world):
+        target = total * r / world
+        while k < n_units and acc + cost[k] / 2 < target and n_units - k > world - r:
+            acc += cost[k]
+            k += 1
+        if k < cuts[-1] + 1:
+            acc += sum(cost[k:cuts[-1] + 1])
+            k = cuts[-1] + 1
+        cuts.append(k)
+    cuts.append(n_units)
+    return [(cuts[r] * unit, cuts[r + 1] * unit) for r in range(world)]
+
+
+def balanced_ranges(volume, scene, rays_per_probe, device, rank, world, sub: int = 8,
+                    group=None, **probe_kwargs):
+    """Cost-balanced slabs: every rank times the trace of ``sub`` pieces of
+    its equal z-slab (CUDA events, no shadow pass), the timings are
+    all-gathered and every rank cuts the probe rows (nx probes each) at equal
+    cumulative cost -- identical ranges on every rank, so the sharded output
+    stays bit-identical to one GPU.  Inner slabs of an interior scene cost
+    ~9 % more than outer ones, more than a whole z-plane of granularity."""
+    nx, ny, nz = volume.dims
+    b, e = slab_range(volume, rank, world)
+    r0, r1 = b // nx, e // nx
+    kw = {k: v for k, v in probe_kwargs.items() if k not in ("shadows", "reserve_sms")}
+    upd = ProbeUpdater(volume, scene, rays_per_probe=rays_per_probe, device=device,
+                       probe_range=(b, e), shadows="none", **kw)
+    upd.update(0)  # warm-up (weights, first-touch)
+    nsub = max(1, min(sub, r1 - r0))
+    bounds = [r0 + (r1 - r0) * i // nsub for i in range(nsub + 1)]
+    local = torch.zeros(sub, dtype=torch.float64, device=device)
+    for i in range(nsub):
+        upd.probe_begin, upd.probe_end = bounds[i] * nx, bounds[i + 1] * nx
+        best = None
+        for rep in range(2):
+            a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            upd.update(1 + rep)
+            z.record()
+            z.synchronize()
+            t = a.elapsed_time(z)
+            best = t if best is None else min(best, t)
+        local[i] = best / max(1, bounds[i + 1] - bounds[i])  # ms per row
+    del upd
+    allc = torch.zeros(world * sub, dtype=torch.float64, device=device)
+    dist.all_gather_into_tensor(allc, local, group=group)
+    allc = allc.cpu().tolist()
+    row_cost = [0.0] * (ny * nz)
+    for r in range(world):
+        rb, re_ = slab_range(volume, r, world)
+        q0, q1 = rb // nx, re_ // nx
+        n = max(1, min(sub, q1 - q0))
+        bb = [q0 + (q1 - q0) * i // n for i in range(n + 1)]
+        for i in range(n):
+            for q in range(bb[i], bb[i + 1]):
+                row_cost[q] = allc[r * sub + i]
+    return ranges_from_cost(ny * nz, nx, world, row_cost)
 
 
 def exchange_bitmap(bits: torch.Tensor, group=None) -> None:
@@ -231,9 +304,21 @@ class DistributedFrame:
     def __init__(self, volume, scene, rays_per_probe, device, rank, world, encoder=0,
                  color_threshold=0.0, visibility_threshold=0.0, slot_count=None, budget=None,
                  gop_length=DEFAULT_GOP, overlap: bool = True, graphs: bool = False,
-                 **probe_kwargs):
+                 balance: bool = _env_flag("PS_BALANCE", False),
+                 shard_shadows: bool = _env_flag("PS_SHADOW_SHARD", False), **probe_kwargs):
         self.volume, self.device, self.rank, self.world = volume, device, rank, world
-        self.ranges = [slab_range(volume, r, world) for r in range(world)]
+        # balance / shard_shadows (off by default, PS_BALANCE / PS_SHADOW_SHARD):
+        # measured at N=4 on C4 both lose -- the per-frame shadow all-gather couples
+        # the ranks' traces (a fast rank can no longer run a frame ahead), and cost
+        # balancing hands the encoder rank, which also imports and packs the whole
+        # update, more probes -- 2.99 / 2.91 ms vs 2.80 ms per frame
+        if not isinstance(scene, DeviceScene):
+            scene = scene.device(device)  # one BVH build, shared with the calibration
+        if balance and world > 1:
+            self.ranges = balanced_ranges(volume, scene, rays_per_probe, device, rank, world,
+                                          **probe_kwargs)
+        else:
+            self.ranges = [slab_range(volume, r, world) for r in range(world)]
         # overlap: both kind chains (with their NCCL exchanges) run on side
         # streams concurrently with the next frame's trace, as on one GPU
         self.overlap = overlap
@@ -241,6 +326,9 @@ class DistributedFrame:
                                     probe_range=self.ranges[rank],
                                     atlas_buffers=2 if overlap else 1,
                                     reserve_sms=probe_kwargs.pop("reserve_sms", RESERVE_SMS) if overlap else 0, **probe_kwargs)
+        # shadow maps: each rank traces 1/world of the texels, all-gathered
+        if shard_shadows:
+            self.updater.shadow_split = (rank, world, None)
         self.streams = {"color": torch.cuda.Stream(device, priority=-1),
                         "visibility": torch.cuda.Stream(device, priority=-1)}
         self._buf_done = [[], []]

@@ -195,11 +195,28 @@ class ProbeUpdater:
         self.graphs = None
         self._graph_evt = [None, None]
         self._pinned_lights = None
+        # sharded shadow maps (set by the sharded frame): (rank, world, group);
+        # each rank traces a slice of the map texels and the slices are
+        # all-gathered before the probe rays are traced
+        self.shadow_split = None
 
     def enable_graphs(self, on: bool = True) -> None:
         self.graphs = {} if on else None
 
-    def _params(self, hysteresis: float) -> N.TraceParams:
+    def _shadow_slice(self):
+        """(begin, end, chunk) of this rank's map texels, or None when unsharded."""
+        if (self.shadow_split is None or self.shadow_mode != N.PS_SHADOW_MAP
+                or self.dscene.light_count == 0):
+            return None
+        rank, world = self.shadow_split[:2]
+        S = self.shadow_map_size
+        total = self.dscene.light_count * 6 * S * S
+        chunk = -(-total // world)
+        if chunk * world > self.shadow_maps.numel():
+            return None  # no room for the padded gather: every rank traces all texels
+        return rank * chunk, min((rank + 1) * chunk, total), chunk
+
+    def _params(self, hysteresis: float, passes: int = 0, texels=None) -> N.TraceParams:
         v, s = self.volume, self.dscene
         p = N.TraceParams()
         p.nx, p.ny, p.nz = v.dims
@@ -219,6 +236,9 @@ class ProbeUpdater:
         p.shadow_map_size = self.shadow_map_size
         p.shadow_maps = self.shadow_maps.data_ptr() if self.shadow_maps is not None else None
         p.shadow_bias = self.shadow_bias
+        p.passes = passes
+        if texels is not None:
+            p.shadow_texel_begin, p.shadow_texel_end = texels
         p.records = self.records.data_ptr()
         p.work_counter = self.work_counter.data_ptr()
         p.reserve_sms = self.reserve_sms
@@ -253,12 +273,40 @@ class ProbeUpdater:
 
     def _issue(self, hysteresis: float) -> None:
         """Weights + shadow maps + trace + blend on the current stream."""
+        sl = self._shadow_slice()
+        self._issue_pre(hysteresis, sl)
+        if sl is not None:
+            self._gather_shadow(sl)
+            self._issue_post(hysteresis)
+
+    def _issue_pre(self, hysteresis: float, sl) -> None:
+        """Weights, then everything (unsharded) or this rank's shadow-map slice."""
         stream = D.stream_ptr(self.device)
         N.call("ps_blend_weights", self.ray_dirs.data_ptr(), self.rays_per_probe,
                self.texdir.data_ptr(), self.sharpness, self.w_color.data_ptr(),
                self.w_depth.data_ptr(), self.inv_wsum.data_ptr(), D.ptr(self.w_image), stream)
-        params = self._params(hysteresis)
+        if sl is None:
+            params = self._params(hysteresis)
+        else:
+            b, e, _ = sl
+            if e <= b:
+                return  # empty slice: this rank only receives
+            params = self._params(hysteresis, passes=1, texels=(b, e))
         N.call("ps_trace_blend", ctypes.byref(params), stream)
+
+    def _issue_post(self, hysteresis: float) -> None:
+        params = self._params(hysteresis, passes=6)
+        N.call("ps_trace_blend", ctypes.byref(params), D.stream_ptr(self.device))
+
+    def _gather_shadow(self, sl) -> None:
+        """In-place all-gather of the ranks' map slices (NCCL, current stream)."""
+        import torch.distributed as dist
+
+        rank, world, group = self.shadow_split
+        _, _, chunk = sl
+        flat = self.shadow_maps.view(-1)
+        dist.all_gather_into_tensor(flat[:chunk * world], flat[rank * chunk:(rank + 1) * chunk],
+                                    group=group)
 
     def _update_graphed(self, frame: int, lights):
         k = self.frames_done & 1
@@ -278,16 +326,25 @@ class ProbeUpdater:
         self._pinned_dirs[k].numpy()[...] = frame_ray_directions(self.rays_per_probe, self.seed, frame)
         kb = self.frames_done % len(self._color_bufs)
         self.color, self.visibility = self._color_bufs[kb], self._vis_bufs[kb]
+        sl = self._shadow_slice()
         key = (k, kb, s.light_count)
         g = self.graphs.get(key)
         if g is None:
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, capture_error_mode="thread_local"):
+            # unsharded: one graph; sharded shadow maps: graph (inputs, weights, map
+            # slice) -> eager NCCL all-gather -> graph (trace, blend)
+            g = [torch.cuda.CUDAGraph()] + ([torch.cuda.CUDAGraph()] if sl is not None else [])
+            with torch.cuda.graph(g[0], capture_error_mode="thread_local"):
                 self.ray_dirs.copy_(self._pinned_dirs[k], non_blocking=True)
                 s.lights.copy_(self._pinned_lights[k], non_blocking=True)
-                self._issue(self.hysteresis)
+                self._issue_pre(self.hysteresis, sl)
+            if sl is not None:
+                with torch.cuda.graph(g[1], capture_error_mode="thread_local"):
+                    self._issue_post(self.hysteresis)
             self.graphs[key] = g
-        g.replay()
+        g[0].replay()
+        if len(g) > 1:
+            self._gather_shadow(sl)
+            g[1].replay()
         evt = torch.cuda.Event()
         evt.record(torch.cuda.current_stream(self.device))
         self._graph_evt[k] = evt

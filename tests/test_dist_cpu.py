@@ -126,3 +126,26 @@ def test_sharded_stages_emulation_matches_single():
         sy, sx = cache2.slot_yx(slot)
         tex[sy:sy + 16, sx:sx + 16] = payloads[r, p - ranges[r][0]]
     assert np.array_equal(tex, want_tex)
+
+
+def test_cost_balanced_ranges():
+    """ranges_from_cost: whole planes, contiguous, cover the volume, every rank
+    at least one plane, and near-equal cost (calibration input of
+    balanced_ranges, which every rank evaluates identically)."""
+    from paper_2103_05875_b200.distributed import ranges_from_cost
+
+    plane = 64 * 32
+    for world in (1, 2, 3, 4, 8):
+        r = ranges_from_cost(64, plane, world, [1.0] * 64)
+        assert r[0][0] == 0 and r[-1][1] == 64 * plane
+        assert all(a[1] == b[0] for a, b in zip(r, r[1:]))
+        sizes = [(e - b) // plane for b, e in r]
+        assert max(sizes) - min(sizes) <= 1 and min(sizes) >= 1
+    cost = [1.0] * 32 + [3.0] * 32  # the far half is 3x more expensive
+    r = ranges_from_cost(64, plane, 4, cost)
+    sums = [sum(cost[b // plane:e // plane]) for b, e in r]
+    assert max(sums) - min(sums) <= 3.0 + 1e-9
+    r = ranges_from_cost(8, plane, 8, [100.0] + [1.0] * 7)
+    assert [(e - b) // plane for b, e in r] == [1] * 8
+    r = ranges_from_cost(8, plane, 4, [1.0] * 7 + [100.0])
+    assert r[-1] == (7 * plane, 8 * plane) and min(e - b for b, e in r) >= plane

@@ -18,14 +18,19 @@ def main():
     h = rows[hi]
     ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
     tot, cnt = defaultdict(float), defaultdict(int)
+    # setup launches (allocations' fills, BVH upload, ...) precede the first
+    # frame's first kernel; only frames are counted
+    body = rows[hi + 1:]
+    first = next((i for i, r in enumerate(body) if "weights_kernel" in r[ki]), 0)
     scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
-    for r in rows[hi + 1:]:
+    for r in body[first:]:
         name = r[ki].replace("(anonymous namespace)::", "").replace("<unnamed>::", "")
         name = re.sub(r"<.*", "", name.replace("void ", "").split("(")[0])
         tot[name] += float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
         cnt[name] += 1
     T = sum(tot.values())
-    print(f"ncu launch list ({args.csv}), {args.frames} frames, serialised cold-cache launches\n")
+    print(f"ncu launch list ({args.csv}), {args.frames} frames from the first frame's first "
+          "kernel, serialised cold-cache launches\n")
     print("| kernel | launches | total us | us / frame | share |")
     print("|---|---|---|---|---|")
     for k, v in sorted(tot.items(), key=lambda kv: -kv[1]):
