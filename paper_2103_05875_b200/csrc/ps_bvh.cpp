@@ -17,8 +17,10 @@
 // the same construction the Moller-Trumbore test of the reference uses
 // (selection.py:124-126).
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <stdexcept>
@@ -63,13 +65,66 @@ struct BuildNode {
     int first = 0, count = 0;   // primitive range (leaf)
 };
 
+// Early split clipping (Ernst & Greiner 2007): a triangle whose box is large
+// next to the scene is referenced by the tight boxes of its pieces clipped at
+// the box midplanes, so a few huge triangles (the hall's gallery slabs span
+// the whole nave) no longer inflate every node above them.  The pieces keep
+// the whole triangle's record (a duplicate in each leaf): hits are tested
+// against the full triangle, so any piece box the ray enters finds it.
+using Poly = std::vector<std::array<double, 3>>;
+
+Poly clip_half(const Poly &in, int axis, double plane, bool keep_below) {
+    Poly out;
+    const size_t n = in.size();
+    for (size_t i = 0; i < n; ++i) {
+        const auto &a = in[i], &b = in[(i + 1) % n];
+        const double da = keep_below ? plane - a[axis] : a[axis] - plane;
+        const double db = keep_below ? plane - b[axis] : b[axis] - plane;
+        if (da >= 0) out.push_back(a);
+        if ((da >= 0) != (db >= 0)) {
+            const double t = da / (da - db);
+            std::array<double, 3> p;
+            for (int k = 0; k < 3; ++k) p[k] = a[k] + t * (b[k] - a[k]);
+            p[axis] = plane;
+            out.push_back(p);
+        }
+    }
+    return out;
+}
+
+void split_refs(int tri, const Poly &poly, const Aabb &box, double limit, int depth,
+                std::vector<Aabb> &boxes, std::vector<int> &tris) {
+    int axis = 0;
+    for (int k = 1; k < 3; ++k)
+        if (box.hi[k] - box.lo[k] > box.hi[axis] - box.lo[axis]) axis = k;
+    if (box.hi[axis] - box.lo[axis] <= limit || depth == 0 || poly.size() < 3) {
+        boxes.push_back(box);
+        tris.push_back(tri);
+        return;
+    }
+    const double mid = 0.5 * (box.lo[axis] + box.hi[axis]);
+    for (int side = 0; side < 2; ++side) {
+        const Poly part = clip_half(poly, axis, mid, side == 0);
+        if (part.size() < 3) continue;
+        Aabb pb;
+        for (const auto &q : part) pb.grow(q.data());
+        for (int k = 0; k < 3; ++k) {  // never outside the parent box
+            pb.lo[k] = std::max(pb.lo[k], box.lo[k]);
+            pb.hi[k] = std::min(pb.hi[k], box.hi[k]);
+        }
+        split_refs(tri, part, pb, limit, depth - 1, boxes, tris);
+    }
+}
+
 struct Builder {
     const double *v;
-    std::vector<Aabb> tri_box;
-    std::vector<double> centroid;
+    std::vector<Aabb> tri_box;    // per reference
+    std::vector<double> centroid; // per reference
+    std::vector<int> ref_tri;     // reference -> triangle
     std::vector<int> order;
     std::vector<BuildNode> nodes;
     int leaf_size;
+    double traversal_cost = 1.2;  // SAH: one node visit vs one triangle test
     static constexpr int BINS = 32;
 
     int build(int first, int count) {
@@ -125,7 +180,7 @@ struct Builder {
         const double parent_area = nodes[id].box.area();
         const double leaf_cost = parent_area * count;
         // traversal cost ~ 1 box pair per node vs 1 triangle per primitive
-        const double split_cost = 1.2 * parent_area + best_cost;
+        const double split_cost = traversal_cost * parent_area + best_cost;
         if (best_axis < 0) {
             if (count <= leaf_size) return id;
             // coincident centroids: split the range in half by index
@@ -232,15 +287,32 @@ static int bvh_build_impl(const double *vertices, int64_t tri_count, int leaf_si
         Builder b;
         b.v = vertices;
         b.leaf_size = leaf_size;
-        const int n = int(tri_count);
-        b.tri_box.resize(n);
+        if (const char *ct = std::getenv("PS_BVH_CT")) b.traversal_cost = std::atof(ct);  // tuning knob
+        const int ntri = int(tri_count);
+        Aabb scene_box;
+        for (int t = 0; t < ntri; ++t)
+            for (int k = 0; k < 3; ++k) scene_box.grow(vertices + 9 * size_t(t) + 3 * k);
+        double diag = 0.0;
+        for (int k = 0; k < 3; ++k) diag += (scene_box.hi[k] - scene_box.lo[k]) * (scene_box.hi[k] - scene_box.lo[k]);
+        // split references longer than diag / PS_BVH_SPLIT (tuning knob; default 0 = off:
+        // on the C4 hall 24 / 48 / 96 / 192 traced in 7.95 / 8.00 / 8.15 / 8.36 ms vs 7.90
+        // unsplit -- its few long triangles are thin slabs the binned SAH already isolates)
+        const char *env = std::getenv("PS_BVH_SPLIT");
+        const double div = env ? std::atof(env) : 0.0;
+        const double limit = div > 0 ? std::sqrt(diag) / div : std::numeric_limits<double>::infinity();
+        for (int t = 0; t < ntri; ++t) {
+            const double *p = vertices + 9 * size_t(t);
+            Aabb tb;
+            for (int k = 0; k < 3; ++k) tb.grow(p + 3 * k);
+            Poly poly{{p[0], p[1], p[2]}, {p[3], p[4], p[5]}, {p[6], p[7], p[8]}};
+            split_refs(t, poly, tb, limit, 8, b.tri_box, b.ref_tri);
+        }
+        const int n = int(b.ref_tri.size());
         b.centroid.resize(3 * size_t(n));
         b.order.resize(n);
-        for (int t = 0; t < n; ++t) {
-            const double *p = vertices + 9 * size_t(t);
-            for (int k = 0; k < 3; ++k) b.tri_box[t].grow(p + 3 * k);
-            for (int a = 0; a < 3; ++a) b.centroid[3 * t + a] = (p[a] + p[3 + a] + p[6 + a]) / 3.0;
-            b.order[t] = t;
+        for (int r = 0; r < n; ++r) {
+            for (int a = 0; a < 3; ++a) b.centroid[3 * r + a] = 0.5 * (b.tri_box[r].lo[a] + b.tri_box[r].hi[a]);
+            b.order[r] = r;
         }
         b.nodes.reserve(2 * size_t(n));
         b.build(0, n);
@@ -362,7 +434,7 @@ static int bvh_build_impl(const double *vertices, int64_t tri_count, int leaf_si
         for (int id : leaves) {
             const BuildNode &bn = b.nodes[id];
             for (int i = bn.first; i < bn.first + bn.count; ++i) {
-                const int t = b.order[i];
+                const int t = b.ref_tri[b.order[i]];
                 const double *p = vertices + 9 * size_t(t);
                 float *r = tris_out + 12 * s;
                 r[0] = float(p[0]); r[1] = float(p[1]); r[2] = float(p[2]);
