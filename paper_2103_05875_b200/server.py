@@ -33,8 +33,10 @@ from .volume import AtlasKind, ProbeAtlas, ProbeVolume
 
 DEFAULT_GOP = 30  # codec.py:46
 # SMs the persistent tracer leaves to the previous frame's stage chains when
-# they overlap (high-priority side streams); tunable via PS_RESERVE_SMS
-RESERVE_SMS = int(__import__("os").environ.get("PS_RESERVE_SMS", "8"))
+# they overlap (high-priority side streams); tunable via PS_RESERVE_SMS.
+# Measured at C4 (ms/frame, reserve 2 / 4 / 8): N=1 8.31 / 8.26 / 8.38,
+# N=2 - / 4.79 / 4.88, N=4 - / 2.73 / 2.77
+RESERVE_SMS = int(__import__("os").environ.get("PS_RESERVE_SMS", "4"))
 
 
 @dataclass
