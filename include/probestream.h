@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define PS_ABI_VERSION 4
+#define PS_ABI_VERSION 5
 
 /* status codes */
 #define PS_OK 0
@@ -179,12 +179,14 @@ int ps_pvs(const float *nodes, int32_t bvh_width, const float *tris, const doubl
  * candidates = changed & pvs & active (bitmaps; pvs_bits NULL = all), ordered
  * by staleness (current_seq - last_sent_seq[p]) descending then id
  * ascending, truncated with python slice semantics when has_budget.
+ * ordered = 0 without a budget returns the same set in ascending id order
+ * (no sort): what the slot assignment consumes, which orders by id itself.
  * ------------------------------------------------------------------------- */
 size_t ps_select_workspace_bytes(int64_t probe_count);
 int ps_select(const uint32_t *changed_bits, const uint32_t *pvs_bits, const uint8_t *active,
               const int64_t *last_sent_seq, int64_t current_seq, int64_t probe_count,
-              int has_budget, int64_t budget, int64_t *out_ids, int64_t *out_count,
-              void *workspace, size_t workspace_bytes, void *stream);
+              int has_budget, int64_t budget, int ordered, int64_t *out_ids,
+              int64_t *out_count, void *workspace, size_t workspace_bytes, void *stream);
 
 /* ---------------------------------------------------------------------------
  * Stage (4): update-atlas slot cache (packing.py:243-317) and build

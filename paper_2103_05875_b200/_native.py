@@ -16,7 +16,7 @@ from pathlib import Path
 from .errors import LayoutMismatchError, NativeLibraryError, SlotOverflowError
 
 LIB_PATH = Path(os.environ.get("PROBESTREAM_LIB", Path(__file__).resolve().parent / "libprobestream.so"))
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 PS_OK = 0
 PS_ERR_VALUE = -1
@@ -97,7 +97,8 @@ _SIGNATURES = {
     "ps_pvs": (_int, [_vp, _i32, _vp, _vp, _vp, _i64, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp,
                       _vp, _vp, _vp, _sz, _vp]),
     "ps_select_workspace_bytes": (_sz, [_i64]),
-    "ps_select": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _int, _i64, _vp, _vp, _vp, _sz, _vp]),
+    "ps_select": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _int, _i64, _int, _vp, _vp, _vp, _sz,
+                         _vp]),
     "ps_assign_workspace_bytes": (_sz, [_i64, _i64]),
     "ps_assign_slots": (_int, [_vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp,
                                _vp, _vp, _sz, _vp]),

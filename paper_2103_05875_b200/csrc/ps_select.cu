@@ -475,8 +475,8 @@ size_t ps_select_workspace_bytes(int64_t probe_count) {
 
 int ps_select(const uint32_t *changed_bits, const uint32_t *pvs_bits, const uint8_t *active,
               const int64_t *last_sent_seq, int64_t current_seq, int64_t probe_count,
-              int has_budget, int64_t budget, int64_t *out_ids, int64_t *out_count,
-              void *workspace, size_t workspace_bytes, void *stream) {
+              int has_budget, int64_t budget, int ordered, int64_t *out_ids,
+              int64_t *out_count, void *workspace, size_t workspace_bytes, void *stream) {
     PS_ABI_BEGIN
     (void)current_seq;  // staleness order is invariant to the common offset
     if (probe_count < 1) fail(PS_ERR_VALUE, "probe_count must be >= 1");
@@ -488,6 +488,12 @@ int ps_select(const uint32_t *changed_bits, const uint32_t *pvs_bits, const uint
     candidate_kernel<<<grid_for(ceil_div(n, 32)), 256, 0, s>>>(changed_bits, pvs_bits, active, n,
                                                                 w.cand);
     check_launch("candidate_kernel");
+    if (!ordered && !has_budget) {
+        // the whole candidate set is selected and the caller only needs the set (the
+        // slot assignment orders by id anyway): ascending ids, no staleness sort
+        compact_bits(w.cand, n, out_ids, nullptr, out_count, w.cmp, w.cmp_bytes, s);
+        return PS_OK;
+    }
     compact_bits(w.cand, n, w.ids, nullptr, w.count, w.cmp, w.cmp_bytes, s);
     select_keys_kernel<<<grid_for(n), 256, 0, s>>>(w.ids, w.count, last_sent_seq, n, w.keys_in,
                                                    w.vals_in);

@@ -132,9 +132,12 @@ def bits_to_ids(bits, probe_count: int):
 
 
 def select_device(changed_bits, pvs_bits, volume, last_sent_seq, current_seq: int,
-                  budget=None, *, out_ids=None, out_count=None, workspace_slot="select"):
+                  budget=None, *, out_ids=None, out_count=None, workspace_slot="select",
+                  ordered: bool = True):
     """Stream-ordered selection over bitmaps; pvs_bits None means every probe.
-    Returns (ids int64[N], count int64[1]) with the first count ids valid."""
+    Returns (ids int64[N], count int64[1]) with the first count ids valid, in
+    staleness order (``ordered``) or, without a budget, ascending id order --
+    the same set, for callers that only need the set."""
     dev = changed_bits.device
     n = volume.probe_count
     seq = D.to_device(last_sent_seq, torch.int64, dev)
@@ -148,7 +151,7 @@ def select_device(changed_bits, pvs_bits, volume, last_sent_seq, current_seq: in
     has_budget = budget is not None
     N.call("ps_select", changed_bits.data_ptr(), D.ptr(pvs_bits),
            volume.active_device(dev).data_ptr(), seq.data_ptr(), int(current_seq), n,
-           int(has_budget), int(budget) if has_budget else 0, out_ids.data_ptr(),
+           int(has_budget), int(budget) if has_budget else 0, int(bool(ordered)), out_ids.data_ptr(),
            out_count.data_ptr(), ws.data_ptr(), ws.numel(), D.stream_ptr(dev))
     return out_ids, out_count
 

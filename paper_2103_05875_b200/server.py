@@ -149,7 +149,7 @@ class KindStream:
         self._mark(f"{tag}.select", 0)
         select_device(self.bits, pvs_bits, self.volume, self.last_sent_seq, seq, self.budget,
                       out_ids=self.sel_ids, out_count=self.sel_count,
-                      workspace_slot=f"select.{tag}")
+                      workspace_slot=f"select.{tag}", ordered=False)
         self._mark(f"{tag}.select", 1)
         self._mark(f"{tag}.assign", 0)
         entries, count = self.layout.assign_device(self.sel_ids, self.sel_count)

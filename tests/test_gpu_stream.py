@@ -261,6 +261,23 @@ def test_select_full_size(ps):
         assert got == want
 
 
+def test_select_unordered_is_the_same_set(ps):
+    """ordered=False (the server chain's fast path, no budget) returns exactly
+    the selected set in ascending id order."""
+    pkg, _, selection, _ = ps
+    n = 131072
+    rng = np.random.default_rng(10)
+    active = rng.random(n) < 0.8
+    vol = pkg.ProbeVolume((64, 32, 64), active=active)
+    changed = rng.choice(n, size=n // 3, replace=False)
+    seq = torch.from_numpy(rng.integers(-100, 100, size=n)).to(DEV)
+    bits, _ = selection.ids_to_bits(changed, n, torch.device(DEV))
+    ids, cnt = selection.select_device(bits, None, vol, seq, 200, None, ordered=False)
+    k = int(cnt.item())
+    want = so.select_for_client(changed, np.arange(n), active, seq.cpu().numpy(), 200, None)
+    assert ids[:k].cpu().tolist() == sorted(want)
+
+
 # --- slot cache + build ---------------------------------------------------------------
 
 
