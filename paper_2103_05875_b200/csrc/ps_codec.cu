@@ -282,6 +282,7 @@ __global__ void __launch_bounds__(WARPS * 32) encode_emit_kernel(EncArgs a) {
 // ---- container + CRC32 ----------------------------------------------------------------
 
 __device__ __forceinline__ uint32_t multmodp(uint32_t a, uint32_t b) {
+    if (a == 0) return 0;  // the loop below needs a set bit to terminate
     uint32_t m = 1u << 31, p = 0;
     while (true) {
         if (a & m) {
@@ -291,6 +292,18 @@ __device__ __forceinline__ uint32_t multmodp(uint32_t a, uint32_t b) {
         m >>= 1;
         b = (b & 1) ? (b >> 1) ^ CRC_POLY : b >> 1;
     }
+    return p;
+}
+
+// X8[k] = x^(8 * 2^k) mod P (reflected, zlib's representation), k < 48
+__constant__ uint32_t c_X8[48] = {
+    0x00800000u, 0x00008000u, 0xedb88320u, 0xb1e6b092u, 0xa06a2517u, 0xed627daeu, 0x88d14467u, 0xd7bbfe6au, 0xec447f11u, 0x8e7ea170u, 0x6427800eu, 0x4d47bae0u, 0x09fe548fu, 0x83852d0fu, 0x30362f1au, 0x7b5a9cc3u, 0x31fec169u, 0x9fec022au, 0x6c8dedc4u, 0x15d6874du, 0x5fde7a4eu, 0xbad90e37u, 0x2e4e5eefu, 0x4eaba214u, 0xa8a472c0u, 0x429a969eu, 0x148d302au, 0xc40ba6d0u, 0xc4e22c3cu, 0x40000000u, 0x20000000u, 0x08000000u, 0x00800000u, 0x00008000u, 0xedb88320u, 0xb1e6b092u, 0xa06a2517u, 0xed627daeu, 0x88d14467u, 0xd7bbfe6au, 0xec447f11u, 0x8e7ea170u, 0x6427800eu, 0x4d47bae0u, 0x09fe548fu, 0x83852d0fu, 0x30362f1au, 0x7b5a9cc3u};
+
+// x^(8n) mod P
+__device__ __forceinline__ uint32_t x8n(uint64_t n) {
+    uint32_t p = 1u << 31;
+    for (int k = 0; n; ++k, n >>= 1)
+        if (n & 1) p = multmodp(c_X8[k], p);
     return p;
 }
 
@@ -315,10 +328,11 @@ __global__ void header_kernel(uint8_t *out, const uint64_t *offsets, const uint3
     *frame_len = HDR + payload + 4;
 }
 
-// CRC32 of 4 KB chunks, one thread per chunk: 16-byte loads, slicing-by-4
+// CRC32 of 4 KB chunks, one thread per chunk: 16-byte loads, slicing-by-16
+// (16 independent table lookups per word; only the final XOR is serial)
 __global__ void __launch_bounds__(128) crc_chunk_kernel(const uint8_t *data, const uint64_t *frame_len,
                                                        uint32_t *crcs, int64_t max_chunks) {
-    __shared__ uint32_t T[4][256];
+    __shared__ uint32_t T[16][256];
     for (int i = threadIdx.x; i < 256; i += blockDim.x) {
         uint32_t c = uint32_t(i);
         for (int k = 0; k < 8; ++k) c = (c & 1) ? CRC_POLY ^ (c >> 1) : c >> 1;
@@ -327,7 +341,7 @@ __global__ void __launch_bounds__(128) crc_chunk_kernel(const uint8_t *data, con
     __syncthreads();
     for (int i = threadIdx.x; i < 256; i += blockDim.x) {
         uint32_t c = T[0][i];
-        for (int k = 1; k < 4; ++k) {
+        for (int k = 1; k < 16; ++k) {
             c = (c >> 8) ^ T[0][c & 0xFFu];
             T[k][i] = c;
         }
@@ -344,76 +358,52 @@ __global__ void __launch_bounds__(128) crc_chunk_kernel(const uint8_t *data, con
         const uint4 *v = reinterpret_cast<const uint4 *>(data + b0);  // chunk starts are 16-B aligned
         for (; i + 16 <= b1; i += 16, ++v) {
             const uint4 q = __ldg(v);
-            const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                crc ^= w4[k];
-                crc = T[3][crc & 0xFFu] ^ T[2][(crc >> 8) & 0xFFu] ^ T[1][(crc >> 16) & 0xFFu] ^
-                      T[0][crc >> 24];
-            }
+            const uint32_t w0 = q.x ^ crc;
+            crc = T[15][w0 & 0xFFu] ^ T[14][(w0 >> 8) & 0xFFu] ^ T[13][(w0 >> 16) & 0xFFu] ^
+                  T[12][w0 >> 24] ^ T[11][q.y & 0xFFu] ^ T[10][(q.y >> 8) & 0xFFu] ^
+                  T[9][(q.y >> 16) & 0xFFu] ^ T[8][q.y >> 24] ^ T[7][q.z & 0xFFu] ^
+                  T[6][(q.z >> 8) & 0xFFu] ^ T[5][(q.z >> 16) & 0xFFu] ^ T[4][q.z >> 24] ^
+                  T[3][q.w & 0xFFu] ^ T[2][(q.w >> 8) & 0xFFu] ^ T[1][(q.w >> 16) & 0xFFu] ^
+                  T[0][q.w >> 24];
         }
         for (; i < b1; ++i) crc = T[0][(crc ^ data[i]) & 0xFFu] ^ (crc >> 8);
         crcs[c] = crc ^ 0xFFFFFFFFu;
     }
 }
 
-// x^(8n) mod P from a table X8[k] = x^(8 * 2^k)
-__device__ __forceinline__ uint32_t x8n_table(const uint32_t *X8, uint64_t n) {
-    uint32_t p = 1u << 31;
-    for (int k = 0; n; ++k, n >>= 1)
-        if (n & 1) p = multmodp(X8[k], p);
-    return p;
-}
-
-// one CTA: 1024 threads fold contiguous runs of equal 4 KB chunks with a
-// constant shift, then a 10-level tree combines the 1024 partial CRCs
-// (crc(A|B) = crc(A) * x^(8|B|) ^ crc(B), the zlib crc32_combine rule)
-__global__ void __launch_bounds__(1024) crc_combine_kernel(uint8_t *out, const uint64_t *frame_len,
-                                                          const uint32_t *crcs) {
-    __shared__ uint32_t X8[48];
-    __shared__ uint32_t part[1024];
-    __shared__ uint64_t plen[1024];
-    if (threadIdx.x == 0) {
-        uint32_t x = 1u << 23;  // x^8
-        for (int k = 0; k < 48; ++k) {
-            X8[k] = x;
-            x = multmodp(x, x);
-        }
-    }
-    __syncthreads();
+// crc(whole) = XOR_c crc(chunk c) * x^(8 * bytes after chunk c): every chunk
+// is shifted independently (the product is associative), XOR-reduced per
+// block and folded into one word with atomicXor
+__global__ void __launch_bounds__(256) crc_shift_kernel(const uint64_t *frame_len,
+                                                        const uint32_t *crcs, int64_t max_chunks,
+                                                        uint32_t *acc) {
     const uint64_t len = *frame_len - 4;
     const int64_t chunks = int64_t((len + CRC_CHUNK - 1) / CRC_CHUNK);
-    const int64_t per = (chunks + 1023) / 1024;
-    const int64_t c0 = threadIdx.x * per, c1 = c0 + per < chunks ? c0 + per : chunks;
-    const uint32_t shift_full = X8[12];  // x^(8 * 4096)
-    uint32_t crc = 0;
-    uint64_t bytes = 0;
-    for (int64_t c = c0; c < c1; ++c) {
-        const uint64_t clen = (c == chunks - 1) ? len - uint64_t(c) * CRC_CHUNK : CRC_CHUNK;
-        const uint32_t sh = (clen == CRC_CHUNK) ? shift_full : x8n_table(X8, clen);
-        crc = (bytes ? multmodp(sh, crc) : 0u) ^ crcs[c];
-        bytes += clen;
+    uint32_t v = 0;
+    for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < chunks && c < max_chunks;
+         c += int64_t(gridDim.x) * blockDim.x) {
+        const uint64_t end = uint64_t(c + 1) * CRC_CHUNK < len ? uint64_t(c + 1) * CRC_CHUNK : len;
+        v ^= multmodp(x8n(len - end), crcs[c]);
     }
-    part[threadIdx.x] = crc;
-    plen[threadIdx.x] = bytes;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v ^= __shfl_xor_sync(0xffffffffu, v, o);
+    __shared__ uint32_t part[8];
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = v;
     __syncthreads();
-    for (int stride = 1; stride < 1024; stride <<= 1) {
-        const int t = threadIdx.x;
-        if ((t % (2 * stride)) == 0 && plen[t + stride]) {
-            const uint64_t rl = plen[t + stride];
-            part[t] = (plen[t] ? multmodp(x8n_table(X8, rl), part[t]) : 0u) ^ part[t + stride];
-            plen[t] += rl;
-        }
-        __syncthreads();
-    }
     if (threadIdx.x == 0) {
-        const uint32_t acc = part[0];
-        for (int k = 0; k < 4; ++k) out[len + k] = uint8_t(acc >> (8 * k));
+        uint32_t r = 0;
+        for (int w = 0; w < int(blockDim.x >> 5); ++w) r ^= part[w];
+        if (r) atomicXor(acc, r);
     }
+}
+
+__global__ void crc_store_kernel(uint8_t *out, const uint64_t *frame_len, const uint32_t *acc) {
+    const uint64_t len = *frame_len - 4;
+    for (int k = 0; k < 4; ++k) out[len + k] = uint8_t(*acc >> (8 * k));
 }
 
 struct EncWs {
-    uint32_t *sizes, *lens, *crcs;
+    uint32_t *sizes, *lens, *crcs, *crc_acc;
     uint8_t *modes;
     uint64_t *offsets, *frame_len;
     void *scan_tmp;
@@ -432,6 +422,7 @@ EncWs carve_enc(void *ws, size_t bytes, int64_t nblocks, int64_t capacity) {
     w.frame_len = c.take<uint64_t>(1);
     w.max_chunks = ceil_div(capacity, CRC_CHUNK);
     w.crcs = c.take<uint32_t>(size_t(w.max_chunks));
+    w.crc_acc = c.take<uint32_t>(1);
     w.scan_bytes = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, w.scan_bytes, (const uint32_t *)nullptr,
                                   (uint64_t *)nullptr, int(nblocks));
@@ -504,8 +495,12 @@ int ps_encode_frame(int elem_bytes, const void *planes, const void *reference, i
     const unsigned cgrid = unsigned(std::max<int64_t>(1, std::min<int64_t>(ceil_div(ws.max_chunks, 128), 4096)));
     crc_chunk_kernel<<<cgrid, 128, 0, s>>>(out, ws.frame_len, ws.crcs, ws.max_chunks);
     check_launch("crc_chunk_kernel");
-    crc_combine_kernel<<<1, 1024, 0, s>>>(out, ws.frame_len, ws.crcs);
-    check_launch("crc_combine_kernel");
+    check_cuda(cudaMemsetAsync(ws.crc_acc, 0, sizeof(uint32_t), s), "memset crc");
+    const unsigned sgrid = unsigned(std::max<int64_t>(1, std::min<int64_t>(ceil_div(ws.max_chunks, 256), 1024)));
+    crc_shift_kernel<<<sgrid, 256, 0, s>>>(ws.frame_len, ws.crcs, ws.max_chunks, ws.crc_acc);
+    check_launch("crc_shift_kernel");
+    crc_store_kernel<<<1, 1, 0, s>>>(out, ws.frame_len, ws.crc_acc);
+    check_launch("crc_store_kernel");
     check_cuda(cudaMemcpyAsync(frame_len, ws.frame_len, sizeof(int64_t), cudaMemcpyDeviceToDevice, s),
                "copy frame length");
     PS_ABI_END
