@@ -24,6 +24,7 @@
 // uvarint(len << 1) + bytes.  A zero byte belongs to such a run iff a
 // neighbouring byte is also zero.
 #include <cub/device/device_scan.cuh>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "ps_common.cuh"
@@ -251,6 +252,207 @@ __global__ void __launch_bounds__(WARPS * 32) encode_size_kernel(EncArgs a) {
             a.modes[b] = uint8_t(mode);
             a.lens[b] = uint32_t(len);
         }
+    }
+}
+
+// ---- size pass, one thread per block --------------------------------------------------
+// The entropy size of a stream only needs its zero-run structure: a maximal
+// run of >= 2 zero bytes costs vlen(2L+1) bytes, every literal stretch of L
+// bytes vlen(2L) + L, and vlen(2L[+1]) = 1 + (L >= 64) for the <= 768-byte
+// streams of a block.  So a thread streams its block's RAW bytes and its
+// residual varint bytes through two small state machines (no scratch, no
+// warp collectives): 32 neighbouring blocks per warp, coalesced row loads.
+struct Sizer {
+    int run = 0, lit = 0, size = 0;
+    __device__ __forceinline__ void push(uint32_t byte) {
+        if (byte == 0) {
+            ++run;
+            return;
+        }
+        if (run >= 2) {
+            if (lit) size += 1 + (lit >= 64) + lit;
+            size += 1 + (run >= 64);
+            lit = 0;
+        } else {
+            lit += run;
+        }
+        ++lit;
+        run = 0;
+    }
+    __device__ __forceinline__ int finish() {
+        if (run >= 2) {
+            if (lit) size += 1 + (lit >= 64) + lit;
+            size += 1 + (run >= 64);
+        } else if (lit + run) {
+            size += 1 + (lit + run >= 64) + lit + run;
+        }
+        return size;
+    }
+};
+
+__device__ __forceinline__ void push_varint(Sizer &z, uint32_t v) {
+    while (v >= 128u) {
+        z.push((v & 0x7Fu) | 0x80u);
+        v >>= 7;
+    }
+    z.push(v);
+}
+
+__global__ void __launch_bounds__(128) encode_size_thread_kernel(EncArgs a) {
+    const int64_t psz = int64_t(a.h) * a.w * a.eb;
+    for (int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; b < a.nblocks;
+         b += int64_t(gridDim.x) * blockDim.x) {
+        int pl, y0, x0, bh, bw;
+        block_coords(a, b, pl, y0, x0, bh, bw);
+        const uint8_t *cur = a.cur + pl * psz;
+        const bool p_frame = a.ref != nullptr;
+        const bool intra = !p_frame && x0 >= 16;
+        const uint8_t *pred = p_frame ? a.ref + pl * psz : cur;
+        const int px = intra ? x0 - 16 : x0;
+        Sizer raw, del;
+        bool diff = false;
+        for (int y = y0; y < y0 + bh; ++y) {
+            for (int x = 0; x < bw; ++x) {
+                const uint32_t cv = load_elem(cur, a.w, y, x0 + x, a.eb);
+                raw.push(cv & 0xFFu);
+                if (a.eb == 2) raw.push(cv >> 8);
+                if (p_frame || intra) {
+                    const uint32_t pv = load_elem(pred, a.w, y, px + x, a.eb);
+                    diff |= cv != pv;
+                    int32_t r;
+                    if (a.eb == 2) r = int32_t(int16_t(uint16_t(cv - pv)));
+                    else r = int32_t(int8_t(uint8_t(cv - pv)));
+                    push_varint(del, (uint32_t(r) << 1) ^ uint32_t(r >> 31));
+                }
+            }
+        }
+        if (p_frame && !diff) {  // SKIP iff bit-identical to the reference block
+            a.sizes[b] = 1;
+            a.modes[b] = 0;
+            a.lens[b] = 0;
+            continue;
+        }
+        int mode = 2, len = raw.finish();
+        if (p_frame || intra) {
+            const int dl = del.finish();
+            if (dl < len) {  // strictly shorter, ties go to RAW (codec.py:283)
+                mode = 1;
+                len = dl;
+            }
+        }
+        a.sizes[b] = uint32_t(1 + vlen(uint32_t(len)) + len);
+        a.modes[b] = uint8_t(mode);
+        a.lens[b] = uint32_t(len);
+    }
+}
+
+// ---- emit pass, one thread per block, staged per warp ----------------------------------
+// Each thread writes its block (mode, uvarint(len), tokens) into the warp's
+// shared staging at its offset relative to the warp's first block -- the 32
+// blocks of a warp are consecutive in the payload -- and the warp then copies
+// the staged bytes out with coalesced stores.  Literal headers are reserved as
+// one byte and widened (the segment shifted by one) when the literal reaches
+// 64 bytes, the only case whose uvarint(2L) needs two bytes.
+constexpr int EMIT_WARPS = 4;
+constexpr int BLOCK_OUT_MAX = 776;  // 1 mode + 2 length + 770 tokens, rounded up
+
+struct Emitter {
+    uint8_t *o;
+    int pos = 0, run = 0, lit = 0, hdr = 0;
+    __device__ __forceinline__ void lit_byte(uint32_t v) {
+        if (lit == 0) hdr = pos++;
+        o[pos++] = uint8_t(v);
+        ++lit;
+    }
+    __device__ __forceinline__ void close_lit() {
+        if (!lit) return;
+        if (lit >= 64) {  // two-byte header: shift the literal bytes up by one
+            for (int i = pos - 1; i > hdr; --i) o[i + 1] = o[i];
+            ++pos;
+            put_varint(o + hdr, uint32_t(lit) << 1);
+        } else {
+            o[hdr] = uint8_t(lit << 1);
+        }
+        lit = 0;
+    }
+    __device__ __forceinline__ void close_run() {
+        close_lit();
+        pos += put_varint(o + pos, (uint32_t(run) << 1) | 1u);
+    }
+    __device__ __forceinline__ void push(uint32_t byte) {
+        if (byte == 0) {
+            ++run;
+            return;
+        }
+        if (run >= 2) close_run();
+        else if (run == 1) lit_byte(0);
+        lit_byte(byte);
+        run = 0;
+    }
+    __device__ __forceinline__ void finish() {
+        if (run >= 2) close_run();
+        else if (run == 1) lit_byte(0);
+        close_lit();
+    }
+};
+
+__device__ __forceinline__ void emit_varint(Emitter &e, uint32_t v) {
+    while (v >= 128u) {
+        e.push((v & 0x7Fu) | 0x80u);
+        v >>= 7;
+    }
+    e.push(v);
+}
+
+__global__ void __launch_bounds__(EMIT_WARPS * 32) encode_emit_thread_kernel(EncArgs a) {
+    extern __shared__ uint8_t stage_raw[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint8_t *stage = stage_raw + wid * (32 * BLOCK_OUT_MAX);
+    const int64_t psz = int64_t(a.h) * a.w * a.eb;
+    const int64_t nwarps = (a.nblocks + 31) / 32;
+    for (int64_t wb = int64_t(blockIdx.x) * EMIT_WARPS + wid; wb < nwarps;
+         wb += int64_t(gridDim.x) * EMIT_WARPS) {
+        const int64_t b0 = wb * 32;
+        const int64_t b = b0 + lane;
+        const uint64_t base = a.offsets[b0];
+        const int64_t last = (b0 + 32 < a.nblocks ? b0 + 32 : a.nblocks) - 1;
+        const uint64_t total = a.offsets[last] + a.sizes[last] - base;
+        if (b < a.nblocks) {
+            Emitter e;
+            e.o = stage + (a.offsets[b] - base);
+            const int mode = a.modes[b];
+            e.o[0] = uint8_t(mode);
+            if (mode != 0) {
+                e.pos = 1 + put_varint(e.o + 1, a.lens[b]);
+                e.o += e.pos;  // tokens start here
+                e.pos = 0;
+                int pl, y0, x0, bh, bw;
+                block_coords(a, b, pl, y0, x0, bh, bw);
+                const uint8_t *cur = a.cur + pl * psz;
+                const bool intra = a.ref == nullptr;
+                const uint8_t *pred = intra ? cur : a.ref + pl * psz;
+                const int px = intra ? x0 - 16 : x0;
+                for (int y = y0; y < y0 + bh; ++y)
+                    for (int x = 0; x < bw; ++x) {
+                        const uint32_t cv = load_elem(cur, a.w, y, x0 + x, a.eb);
+                        if (mode == 2) {
+                            e.push(cv & 0xFFu);
+                            if (a.eb == 2) e.push(cv >> 8);
+                        } else {
+                            const uint32_t pv = load_elem(pred, a.w, y, px + x, a.eb);
+                            int32_t r;
+                            if (a.eb == 2) r = int32_t(int16_t(uint16_t(cv - pv)));
+                            else r = int32_t(int8_t(uint8_t(cv - pv)));
+                            emit_varint(e, (uint32_t(r) << 1) ^ uint32_t(r >> 31));
+                        }
+                    }
+                e.finish();
+            }
+        }
+        __syncwarp();
+        uint8_t *dst = a.out + HDR + base;
+        for (uint64_t i = lane; i < total; i += 32) dst[i] = stage[i];
+        __syncwarp();
     }
 }
 
@@ -482,13 +684,42 @@ int ps_encode_frame(int elem_bytes, const void *planes, const void *reference, i
     a.offsets = ws.offsets;
     a.out = out;
     const unsigned grid = unsigned(std::min<int64_t>(ceil_div(nb, WARPS), int64_t(sm_count()) * 64));
-    encode_size_kernel<<<grid, WARPS * 32, 0, s>>>(a);
-    check_launch("encode_size_kernel");
+    static const bool warp_size_pass = [] {
+        const char *e = getenv("PS_ENCODE_SIZE");  // "warp": the warp-per-block passes
+        return e && e[0] == 'w';
+    }();
+    if (warp_size_pass) {
+        encode_size_kernel<<<grid, WARPS * 32, 0, s>>>(a);
+        check_launch("encode_size_kernel");
+    } else {
+        const unsigned tgrid = unsigned(std::min<int64_t>(ceil_div(nb, 128), int64_t(sm_count()) * 16));
+        encode_size_thread_kernel<<<tgrid, 128, 0, s>>>(a);
+        check_launch("encode_size_thread_kernel");
+    }
     size_t tmp = ws.scan_bytes;
     check_cuda(cub::DeviceScan::ExclusiveSum(ws.scan_tmp, tmp, ws.sizes, ws.offsets, int(nb), s),
                "cub ExclusiveSum");
-    encode_emit_kernel<<<grid, WARPS * 32, 0, s>>>(a);
-    check_launch("encode_emit_kernel");
+    // emit: the staged thread-per-block pass wins for 1-byte elements (visibility
+    // 1.46 -> 1.38 ms key, P 1.59 -> 1.31 ms at C4); with 2-byte elements the
+    // 776-byte staging per block caps occupancy and the warp pass stays ahead
+    // (colour key 0.54 vs 0.63 ms)
+    if (warp_size_pass || elem_bytes == 2) {
+        encode_emit_kernel<<<grid, WARPS * 32, 0, s>>>(a);
+        check_launch("encode_emit_kernel");
+    } else {
+        static bool attr = false;
+        const int smem = EMIT_WARPS * 32 * BLOCK_OUT_MAX;
+        if (!attr) {
+            check_cuda(cudaFuncSetAttribute(encode_emit_thread_kernel,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+                       "cudaFuncSetAttribute(emit)");
+            attr = true;
+        }
+        const int64_t nw = ceil_div(nb, 32);
+        const unsigned egrid = unsigned(std::min<int64_t>(ceil_div(nw, EMIT_WARPS), int64_t(sm_count()) * 8));
+        encode_emit_thread_kernel<<<egrid, EMIT_WARPS * 32, smem, s>>>(a);
+        check_launch("encode_emit_thread_kernel");
+    }
     header_kernel<<<1, 1, 0, s>>>(out, ws.offsets, ws.sizes, nb, reference == nullptr, stream_id,
                                    frame_seq, int(w), int(h), elem_bytes * 8, ws.frame_len);
     check_launch("header_kernel");
