@@ -92,6 +92,7 @@ class KindStream:
         self.graphs = None
         self.frame_state = torch.zeros(3, dtype=torch.int64, device=device)
         self._state_synced = False
+        self._wire = None  # LPF1 frame / index buffers (encode=True), two frame parities
 
     def _mark(self, name, stage):
         if self.timers is not None:
@@ -191,8 +192,22 @@ class KindStream:
             from .index_buffer import encode_index_device
 
             self._mark(f"{tag}.encode", 0)
-            frame, frame_len = encode_frame_device(cur, prev, self.stream_id, self.frame_count)
-            index, index_len = encode_index_device(entries, count)  # §8(f)4
+            # wire buffers ping-pong by frame parity, so a frame's bytes stay valid
+            # while the next frame is encoded (a caller may read them a frame late)
+            k = self.frame_count & 1
+            if self._wire is None:
+                cap = N.lib().ps_encode_frame_capacity(cur.shape[1], cur.shape[2],
+                                                      cur.element_size())
+                icap = 1 + 20 * max(int(entries.shape[0]), 1)
+                self._wire = [(torch.empty(cap, dtype=torch.uint8, device=self.device),
+                               torch.zeros(1, dtype=torch.int64, device=self.device),
+                               torch.empty(icap, dtype=torch.uint8, device=self.device),
+                               torch.zeros(1, dtype=torch.int64, device=self.device))
+                              for _ in range(2)]
+            fb, fl, ib, il = self._wire[k]
+            frame, frame_len = encode_frame_device(cur, prev, self.stream_id, self.frame_count,
+                                                   out=fb, frame_len=fl)
+            index, index_len = encode_index_device(entries, count, out=ib, out_len=il)  # §8(f)4
             self._mark(f"{tag}.encode", 1)
         return self._advance(frame, frame_len, index, index_len)
 

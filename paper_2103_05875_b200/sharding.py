@@ -94,7 +94,10 @@ class SlabServer:
     def run_e2e_encoded(self, steps: int, first_frame: int, lights_for) -> dict:
         """End to end including §8(f)1/4: every frame is encoded to LPF1 on the
         device and the wire bytes (frames + index buffers) are read back to
-        pinned host memory -- what a server sends to its client."""
+        pinned host memory -- what a server sends to its client.  Read-back
+        runs one frame behind: after issuing frame f the host waits for frame
+        f-1's lengths (its stage chains finish while frame f traces) and queues
+        the D2H of its bytes, so the pipeline never drains."""
         impl = self.impl
         if not hasattr(impl, "color") or not hasattr(impl.color, "encode"):
             return {}
@@ -105,29 +108,50 @@ class SlabServer:
             impl.tick(first_frame, lights_for(first_frame))  # buffers + warm
             torch.cuda.synchronize(self.device)
             host = {ks.kind.value: torch.empty(256 << 20, dtype=torch.uint8).pin_memory() for ks in kinds}
-            d2h = 0
+            lens = {ks.kind.value: torch.zeros((2, 2), dtype=torch.int64).pin_memory() for ks in kinds}
+            d2h = [0]
+
+            def issue_lens(outs, par):
+                evs = []
+                for ks, o in zip(kinds, outs):
+                    st = self._out_stream(ks.kind.value)
+                    with torch.cuda.stream(st):
+                        lens[ks.kind.value][par, 0:1].copy_(o.frame_len, non_blocking=True)
+                        lens[ks.kind.value][par, 1:2].copy_(o.index_len, non_blocking=True)
+                        ev = torch.cuda.Event()
+                        ev.record(st)
+                    evs.append(ev)
+                return evs
+
+            def drain(outs, evs, par):
+                for ks, o, ev in zip(kinds, outs, evs):
+                    ev.synchronize()
+                    n, ni = int(lens[ks.kind.value][par, 0]), int(lens[ks.kind.value][par, 1])
+                    hb = host[ks.kind.value]
+                    with torch.cuda.stream(self._out_stream(ks.kind.value)):
+                        hb[:n].copy_(o.frame[:n], non_blocking=True)
+                        hb[n:n + ni].copy_(o.index[:ni], non_blocking=True)
+                    d2h[0] += n + ni + 16
+
             stream = torch.cuda.current_stream(self.device)
             start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize(self.device)
             start.record(stream)
+            prev = None
             for k in range(steps):
                 f = first_frame + 1 + k
                 outs = impl.tick(f, lights_for(f))
-                for ks, o in zip(kinds, outs):
-                    st = self._out_stream(ks.kind.value)
-                    st.synchronize()  # frame / index lengths are needed on the host
-                    n, ni = int(o.frame_len.item()), int(o.index_len.item())
-                    hb = host[ks.kind.value]
-                    with torch.cuda.stream(st):
-                        hb[:n].copy_(o.frame[:n], non_blocking=True)
-                        hb[n:n + ni].copy_(o.index[:ni], non_blocking=True)
-                    d2h += n + ni + 16
+                evs = issue_lens(outs, k & 1)
+                if prev is not None:
+                    drain(*prev)
+                prev = (outs, evs, k & 1)
+            drain(*prev)
             self.join()
             end.record(stream)
             torch.cuda.synchronize(self.device)
             return {"ms_per_step": start.elapsed_time(end) / steps,
                     "h2d_bytes_per_step": impl.h2d_bytes_per_frame(),
-                    "d2h_bytes_per_step": d2h // steps}
+                    "d2h_bytes_per_step": d2h[0] // steps}
         finally:
             for ks in kinds:
                 ks.encode = False
