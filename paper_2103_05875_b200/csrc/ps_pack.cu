@@ -218,6 +218,160 @@ __global__ void __launch_bounds__(TILE_X *TILE_Y)
     }
 }
 
+// Visibility planes whose rows are not 16-byte aligned (plane width
+// ceil(4w/3) % 16 != 0, e.g. a 4,096-texel update atlas): same work as
+// pack_delta_kernel, but the 16-byte plane segments are funnel-shifted onto
+// the aligned 16-byte words of the row.  Thread j writes the aligned word that
+// holds its segment's tail and the next segment's head (taken from lane j+1
+// with a 16-wide shuffle); only the first / last thread of a tile row and the
+// row ends fall back to byte stores.  Previous planes are read as the two
+// aligned words around each segment.
+__device__ __forceinline__ void funnel16(const uint32_t lo[4], const uint32_t hi[4], int s,
+                                         uint32_t out[4]) {
+    // bytes [s, s + 16) of lo || hi, 0 <= s <= 16
+    const uint32_t c[9] = {lo[0], lo[1], lo[2], lo[3], hi[0], hi[1], hi[2], hi[3], 0u};
+    const int q = s >> 2, r = (s & 3) * 8;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        uint32_t a0 = c[i], a1 = c[i + 1];
+#pragma unroll
+        for (int k = 1; k <= 4; ++k) {
+            a0 = q == k ? c[i + k] : a0;
+            a1 = q == k ? c[i + k + 1 < 9 ? i + k + 1 : 8] : a1;
+        }
+        out[i] = r ? __funnelshift_r(a0, a1, r) : a0;
+    }
+}
+
+// bytes [lo, hi) of the 16-byte value x to the 16-byte aligned address base,
+// as a few naturally aligned 8 / 4 / 2 / 1-byte stores
+__device__ __forceinline__ void store_range(uint8_t *base, const uint32_t x[4], int lo, int hi) {
+    while (lo < hi) {
+        const int q = lo >> 2;
+        const uint32_t wq = q == 0 ? x[0] : q == 1 ? x[1] : q == 2 ? x[2] : x[3];
+        if ((lo & 7) == 0 && lo + 8 <= hi) {
+            *reinterpret_cast<uint2 *>(base + lo) = make_uint2(wq, q == 0 ? x[1] : x[3]);
+            lo += 8;
+        } else if ((lo & 3) == 0 && lo + 4 <= hi) {
+            *reinterpret_cast<uint32_t *>(base + lo) = wq;
+            lo += 4;
+        } else if ((lo & 1) == 0 && lo + 2 <= hi) {
+            *reinterpret_cast<uint16_t *>(base + lo) = uint16_t(wq >> (8 * (lo & 3)));
+            lo += 2;
+        } else {
+            base[lo] = uint8_t(wq >> (8 * (lo & 3)));
+            lo += 1;
+        }
+    }
+}
+
+// one 16-byte segment at row offset x0_b of the row starting at `row` (any
+// alignment); valid_b = row bytes from the segment start on.  Every lane of
+// the 16-wide group calls this (inactive lanes with valid_b <= 0).
+__device__ __forceinline__ void store_seg_unaligned(uint8_t *row, int64_t x0_b, int64_t valid_b,
+                                                    int tx, const uint32_t w[4]) {
+    const int m = int(reinterpret_cast<uintptr_t>(row) & 15u);  // x0_b is a multiple of 16
+    uint32_t nxt[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) nxt[i] = __shfl_down_sync(0xffffffffu, w[i], 1, 16);
+    if (valid_b <= 0) return;
+    uint8_t *seg = row + x0_b;
+    if (m == 0) {
+        if (valid_b >= 16)
+            *reinterpret_cast<uint4 *>(seg) = make_uint4(w[0], w[1], w[2], w[3]);
+        else
+            store_range(seg, w, 0, int(valid_b));
+        return;
+    }
+    const uint32_t zero[4] = {0u, 0u, 0u, 0u};
+    // head: segment bytes [0, 16 - m) = word j bytes [m, 16), written by the previous
+    // lane unless this is the tile row's first lane
+    if (tx == 0) {
+        uint32_t x[4];
+        funnel16(zero, w, 16 - m, x);
+        store_range(seg - m, x, m, m + int(valid_b < 16 - m ? valid_b : 16 - m));
+    }
+    if (valid_b <= 16 - m) return;  // the segment ends inside word j
+    // word j + 1: our tail (m bytes) then the next segment's head (16 - m bytes)
+    uint8_t *word = seg + (16 - m);  // 16-byte aligned
+    const int64_t in_row = valid_b - (16 - m);  // row bytes from `word` on (ours + later)
+    uint32_t x[4];
+    funnel16(w, nxt, 16 - m, x);
+    if (tx < 15 && in_row >= 16) {
+        *reinterpret_cast<uint4 *>(word) = make_uint4(x[0], x[1], x[2], x[3]);
+        return;
+    }
+    const int64_t lim = tx < 15 ? 16 : m;  // the last lane only owns its own tail
+    store_range(word, x, 0, int(in_row < lim ? in_row : lim));
+}
+
+__global__ void __launch_bounds__(TILE_X *TILE_Y)
+    pack_delta_vis_unaligned_kernel(PackArgs a) {
+    if (a.key_dev && *a.key_dev) a.prev = nullptr;
+    __shared__ uint32_t dirty[3][TILE_X];
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int64_t seg = int64_t(blockIdx.x) * TILE_X + tx;
+    const int64_t by = blockIdx.y;
+    const int64_t r = by * TILE_Y + ty;
+    if (ty == 0)
+        for (int e = 0; e < 3; ++e) dirty[e][tx] = 0u;
+    __syncthreads();
+    const bool active = seg < a.nseg && r < a.h;
+    uint32_t cur[3][8];
+    if (active) {
+        load_segment<PS_KIND_VISIBILITY>(a, r, seg, cur);
+    } else {
+#pragma unroll
+        for (int e = 0; e < 3; ++e)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) cur[e][i] = 0u;
+    }
+    const int64_t x0_b = seg * SEG;
+    const int64_t valid_b = active ? a.pw - seg * SEG : 0;
+    const int64_t plane_b = a.h * a.pw;
+    const int64_t row_b = (r < a.h ? r : 0) * a.pw;
+#pragma unroll
+    for (int e = 0; e < 3; ++e) {
+        if (a.prev) {
+            uint32_t pv[4] = {0u, 0u, 0u, 0u};
+            if (active) {
+                const uint8_t *p = a.prev + e * plane_b + row_b + x0_b;
+                const int m = int(reinterpret_cast<uintptr_t>(p) & 15u);
+                const uint8_t *al = p - m;
+                const int64_t left = (a.prev + 3 * plane_b) - al;  // bytes to the buffer end
+                if (left >= 32) {
+                    const uint4 l0 = __ldg(reinterpret_cast<const uint4 *>(al));
+                    const uint4 l1 = __ldg(reinterpret_cast<const uint4 *>(al) + 1);
+                    const uint32_t lo[4] = {l0.x, l0.y, l0.z, l0.w}, hi[4] = {l1.x, l1.y, l1.z, l1.w};
+                    funnel16(lo, hi, m, pv);
+                } else {
+                    for (int b = 0; b < 16 && b < valid_b; ++b)
+                        pv[b >> 2] |= uint32_t(p[b]) << (8 * (b & 3));
+                }
+                if (valid_b < 16) {  // bytes past the row end count as zero, as in the cur planes
+                    for (int b = int(valid_b); b < 16; ++b) pv[b >> 2] &= ~(0xFFu << (8 * (b & 3)));
+                }
+            }
+            uint32_t any = 0, res[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                any |= cur[e][i] ^ pv[i];
+                res[i] = __vsub4(cur[e][i], pv[i]);
+            }
+            if (a.residual)
+                store_seg_unaligned(a.residual + e * plane_b + row_b, x0_b, valid_b, tx, res);
+            if (active && any) atomicOr(&dirty[e][tx], 1u);
+        }
+        store_seg_unaligned(a.cur + e * plane_b + row_b, x0_b, valid_b, tx, cur[e]);
+    }
+    __syncthreads();
+    if (a.skip && ty < 3 && seg < a.nseg) {
+        const int64_t nby = (a.h + TILE_Y - 1) / TILE_Y;
+        uint8_t sk = a.prev ? uint8_t(dirty[ty][tx] == 0u) : uint8_t(0);
+        a.skip[(int64_t(ty) * nby + by) * a.nseg + seg] = sk;
+    }
+}
+
 // Generic temporal delta over already-packed planes (elements of 1 or 2 B).
 template <int EB>
 __global__ void __launch_bounds__(TILE_X *TILE_Y)
@@ -309,8 +463,13 @@ int launch_pack_delta(int kind, const void *texels, int64_t h, int64_t w, int64_
     dim3 block(TILE_X, TILE_Y);
     dim3 grid(unsigned(ceil_div(a.nseg, TILE_X)), unsigned(ceil_div(h, TILE_Y)));
     if (grid.y > 65535u) fail(PS_ERR_VALUE, "plane too tall");
+    const bool rows_misaligned = kind == PS_KIND_VISIBILITY && !a.vec_out && a.vec_in &&
+                                 aligned16(planes_cur) && (!planes_prev || aligned16(planes_prev)) &&
+                                 (!residual || aligned16(residual));
     if (kind == PS_KIND_COLOR)
         pack_delta_kernel<PS_KIND_COLOR><<<grid, block, 0, stream>>>(a);
+    else if (rows_misaligned)
+        pack_delta_vis_unaligned_kernel<<<grid, block, 0, stream>>>(a);
     else
         pack_delta_kernel<PS_KIND_VISIBILITY><<<grid, block, 0, stream>>>(a);
     check_launch("pack_delta_kernel");

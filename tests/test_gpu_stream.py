@@ -117,7 +117,7 @@ def test_delta_golden(ps, golden, tag):
 
 
 @pytest.mark.parametrize("kind", ["color", "visibility"])
-@pytest.mark.parametrize("slots", [1, 5, 17, 363, 1000])
+@pytest.mark.parametrize("slots", [1, 5, 17, 363, 1000, 4096, 16384])
 def test_pack_delta_matches_pack_then_delta(ps, kind, slots):
     pkg, packing, _, delta = ps
     rng = np.random.default_rng(slots)
