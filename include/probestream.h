@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define PS_ABI_VERSION 5
+#define PS_ABI_VERSION 6
 
 /* status codes */
 #define PS_OK 0
@@ -235,6 +235,41 @@ int ps_import_tiles(int kind, const void *payloads, int64_t payload_stride,
                     const int64_t *rank_begin, int32_t world, const int64_t *entries,
                     const int64_t *entry_count, int64_t max_entries, int64_t slots_per_row,
                     void *update_texels, int64_t update_row_stride, void *stream);
+
+/* Peer-memory exchanges of the slab-sharded frame (csrc/ps_peer.cu, new:
+ * the reference has no multi-GPU path).
+ *   ps_detect_changed_bcast: as ps_detect_changed_range, but every changed
+ *     word is ORed (system-scope atomics) into each of the ndst bitmaps in
+ *     dst_bits (a device array of device pointers, peers' mapped bitmaps
+ *     included); the caller zeroes the bitmaps between frames.
+ *   ps_export_tiles_peer: copies the cores of the selected probes inside
+ *     [probe_begin, probe_end) into the slots of dst_update_texels (the
+ *     encoder rank's update atlas, mapped from another process), commits
+ *     them into last_sent and stamps last_sent_seq for every entry.
+ *   ps_peer_signal: stores (value or *value_dev) + add into each *flags[i]
+ *     with system-scope release semantics after a system fence;
+ *     ps_peer_wait: spins until every flags[i] >= that value (acquire).
+ *   ps_ipc_export / ps_ipc_open: CUDA IPC handle (ps_ipc_handle_bytes bytes)
+ *     and offset for any device pointer; opening maps it in this process
+ *     (cached per allocation). */
+int ps_detect_changed_bcast(int kind, const void *rendered, const void *last_sent,
+                            int64_t probe_count, int64_t probes_per_row, int64_t block_rows,
+                            int64_t probe_begin, int64_t probe_end, const uint8_t *active,
+                            double threshold, int threshold_is_f64, uint32_t *const *dst_bits,
+                            int ndst, void *stream);
+int ps_export_tiles_peer(int kind, const void *source, int64_t probe_count,
+                         int64_t probes_per_row, const int64_t *entries,
+                         const int64_t *entry_count, int64_t max_entries, int64_t probe_begin,
+                         int64_t probe_end, int64_t slots_per_row, void *dst_update_texels,
+                         int64_t dst_row_stride, void *last_sent, int64_t *last_sent_seq,
+                         int64_t current_seq, const int64_t *current_seq_dev, void *stream);
+int ps_peer_signal(int64_t *const *flags, int32_t nflags, int64_t value,
+                   const int64_t *value_dev, int64_t add, void *stream);
+int ps_peer_wait(const int64_t *flags, int32_t nflags, int64_t value, const int64_t *value_dev,
+                 int64_t add, void *stream);
+size_t ps_ipc_handle_bytes(void);
+int ps_ipc_export(const void *ptr, uint8_t *handle, int64_t *offset);
+int ps_ipc_open(const uint8_t *handle, int64_t offset, void **ptr);
 
 /* Device-resident per-stream frame counters for CUDA-graph replay (no host
  * scalar is baked into a captured frame).  state = int64[3]

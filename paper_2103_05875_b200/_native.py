@@ -16,7 +16,7 @@ from pathlib import Path
 from .errors import LayoutMismatchError, NativeLibraryError, SlotOverflowError
 
 LIB_PATH = Path(os.environ.get("PROBESTREAM_LIB", Path(__file__).resolve().parent / "libprobestream.so"))
-ABI_VERSION = 5
+ABI_VERSION = 6
 
 PS_OK = 0
 PS_ERR_VALUE = -1
@@ -108,6 +108,15 @@ _SIGNATURES = {
     "ps_index_workspace_bytes": (_sz, [_i64]),
     "ps_encode_index": (_int, [_vp, _vp, _i64, _vp, _vp, _vp, _sz, _vp]),
     "ps_frame_advance": (_int, [_vp, _i64, _vp]),
+    "ps_detect_changed_bcast": (_int, [_int, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _f64,
+                                       _int, _vp, _int, _vp]),
+    "ps_export_tiles_peer": (_int, [_int, _vp, _i64, _i64, _vp, _vp, _i64, _i64, _i64, _i64, _vp,
+                                    _i64, _vp, _vp, _i64, _vp, _vp]),
+    "ps_peer_signal": (_int, [_vp, _i32, _i64, _vp, _i64, _vp]),
+    "ps_peer_wait": (_int, [_vp, _i32, _i64, _vp, _i64, _vp]),
+    "ps_ipc_handle_bytes": (_sz, []),
+    "ps_ipc_export": (_int, [_vp, _vp, _vp]),
+    "ps_ipc_open": (_int, [_vp, _i64, _vp]),
     "ps_export_tiles": (_int, [_int, _vp, _i64, _i64, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp,
                                _i64, _vp, _vp]),
     "ps_import_tiles": (_int, [_int, _vp, _i64, _vp, _i32, _vp, _vp, _i64, _i64, _vp, _i64, _vp]),

@@ -36,6 +36,8 @@ struct DetectArgs {
     int64_t band0;           // first block row of the range
     const uint8_t *active;   // bool[probe_count] or nullptr (all active)
     uint32_t *bits;          // changed bitmap (zeroed by the launcher)
+    uint32_t *const *dst;    // or: publish into these bitmaps (peer memory allowed)
+    int ndst;
     int color_cut;           // COLOR_CUT: changed iff max channel delta >= cut
     float thr32;
     double thr64;
@@ -104,13 +106,30 @@ __global__ void __launch_bounds__(DET_THREADS) detect_kernel(DetectArgs a) {
     }
     __syncthreads();
     // publish: one thread per probe touched by this CTA
-    for (int i = threadIdx.x; i < nprobe; i += DET_THREADS) {
+    if (!a.dst) {
+        for (int i = threadIdx.x; i < nprobe; i += DET_THREADS) {
+            const int64_t bc = bc0 + i;
+            if (bc >= a.ppr) continue;
+            const int64_t p = band * a.ppr + bc;
+            if (p < a.probe_begin || p >= a.probe_end || !probe_hit[i]) continue;
+            if (a.active && !a.active[p]) continue;
+            atomicOr(&a.bits[p >> 5], 1u << (p & 31));
+        }
+        return;
+    }
+    // broadcast: the lanes of a bitmap word OR their bits (warp match + reduce) and
+    // one lane ORs the word into every destination, peers' bitmaps over NVLink
+    for (int i0 = 0; i0 < nprobe; i0 += DET_THREADS) {
+        const int i = i0 + threadIdx.x;
         const int64_t bc = bc0 + i;
-        if (bc >= a.ppr) continue;
         const int64_t p = band * a.ppr + bc;
-        if (p < a.probe_begin || p >= a.probe_end || !probe_hit[i]) continue;
-        if (a.active && !a.active[p]) continue;
-        atomicOr(&a.bits[p >> 5], 1u << (p & 31));
+        const bool ok = i < nprobe && bc < a.ppr && p >= a.probe_begin && p < a.probe_end &&
+                        probe_hit[i] && (!a.active || a.active[p]);
+        const int64_t word = ok ? (p >> 5) : -1;
+        const unsigned grp = __match_any_sync(0xffffffffu, word);
+        const uint32_t v = __reduce_or_sync(grp, ok ? 1u << (p & 31) : 0u);
+        if (ok && (threadIdx.x & 31) == __ffs(grp) - 1)
+            for (int d = 0; d < a.ndst; ++d) atomicOr_system(a.dst[d] + word, v);
     }
 }
 
@@ -235,33 +254,20 @@ void ids_to_bits(const int64_t *ids, const int64_t *n_dev, int64_t n_host, int64
 
 using namespace ps;
 
-extern "C" {
-
-size_t ps_detect_workspace_bytes(int64_t probe_count) {
-    return compact_workspace_bytes(std::max<int64_t>(probe_count, 1));
-}
-
-size_t ps_compact_workspace_bytes(int64_t probe_count) {
-    return compact_workspace_bytes(std::max<int64_t>(probe_count, 1));
-}
-
-int ps_detect_changed_range(int kind, const void *rendered, const void *last_sent,
-                            int64_t probe_count, int64_t probes_per_row, int64_t block_rows,
-                            int64_t probe_begin, int64_t probe_end, const uint8_t *active,
-                            double threshold, int threshold_is_f64, uint32_t *changed_bits,
-                            int64_t *out_ids, int64_t *out_count, void *workspace,
-                            size_t workspace_bytes, void *stream) {
-    PS_ABI_BEGIN
+static void detect_range_impl(int kind, const void *rendered, const void *last_sent,
+                              int64_t probe_count, int64_t probes_per_row, int64_t block_rows,
+                              int64_t probe_begin, int64_t probe_end, const uint8_t *active,
+                              double threshold, int threshold_is_f64, uint32_t *changed_bits,
+                              uint32_t *const *dst, int ndst, cudaStream_t s) {
     if (probe_begin < 0 || probe_end > probe_count || probe_begin > probe_end)
         fail(PS_ERR_INDEX, "probe range outside the volume");
     if (kind != PS_KIND_COLOR && kind != PS_KIND_VISIBILITY) fail(PS_ERR_VALUE, "bad kind");
     if (probe_count < 1) fail(PS_ERR_VALUE, "probe_count must be >= 1");
     if (probes_per_row < 1 || block_rows != ceil_div(probe_count, probes_per_row))
         fail(PS_ERR_LAYOUT, "atlas layout does not match probe count");
-    auto s = as_stream(stream);
     const int side = (kind == PS_KIND_COLOR) ? 10 : 18;
     const int64_t words = ceil_div(probe_count, 32);
-    check_cuda(cudaMemsetAsync(changed_bits, 0, size_t(words) * 4, s), "memset bits");
+    if (!dst) check_cuda(cudaMemsetAsync(changed_bits, 0, size_t(words) * 4, s), "memset bits");
 
     DetectArgs a;
     a.a = static_cast<const uint2 *>(rendered);
@@ -275,6 +281,8 @@ int ps_detect_changed_range(int kind, const void *rendered, const void *last_sen
     a.band0 = probe_begin / probes_per_row;
     a.active = active;
     a.bits = changed_bits;
+    a.dst = dst;
+    a.ndst = ndst;
     a.color_cut = 1;
     a.thr32 = 0.f;
     a.thr64 = 0.0;
@@ -313,6 +321,42 @@ int ps_detect_changed_range(int kind, const void *rendered, const void *last_sen
 #undef PS_DET
     check_launch("detect_kernel");
     }
+}
+
+extern "C" {
+
+size_t ps_detect_workspace_bytes(int64_t probe_count) {
+    return compact_workspace_bytes(std::max<int64_t>(probe_count, 1));
+}
+
+size_t ps_compact_workspace_bytes(int64_t probe_count) {
+    return compact_workspace_bytes(std::max<int64_t>(probe_count, 1));
+}
+
+int ps_detect_changed_bcast(int kind, const void *rendered, const void *last_sent,
+                            int64_t probe_count, int64_t probes_per_row, int64_t block_rows,
+                            int64_t probe_begin, int64_t probe_end, const uint8_t *active,
+                            double threshold, int threshold_is_f64, uint32_t *const *dst_bits,
+                            int ndst, void *stream) {
+    PS_ABI_BEGIN
+    if (!dst_bits || ndst < 1) fail(PS_ERR_VALUE, "need at least one destination bitmap");
+    detect_range_impl(kind, rendered, last_sent, probe_count, probes_per_row, block_rows,
+                      probe_begin, probe_end, active, threshold, threshold_is_f64, nullptr,
+                      dst_bits, ndst, as_stream(stream));
+    PS_ABI_END
+}
+
+int ps_detect_changed_range(int kind, const void *rendered, const void *last_sent,
+                            int64_t probe_count, int64_t probes_per_row, int64_t block_rows,
+                            int64_t probe_begin, int64_t probe_end, const uint8_t *active,
+                            double threshold, int threshold_is_f64, uint32_t *changed_bits,
+                            int64_t *out_ids, int64_t *out_count, void *workspace,
+                            size_t workspace_bytes, void *stream) {
+    PS_ABI_BEGIN
+    auto s = as_stream(stream);
+    detect_range_impl(kind, rendered, last_sent, probe_count, probes_per_row, block_rows,
+                      probe_begin, probe_end, active, threshold, threshold_is_f64, changed_bits,
+                      nullptr, 0, s);
     if (out_ids || out_count)
         compact_bits(changed_bits, probe_count, out_ids, nullptr, out_count, workspace,
                      workspace_bytes, s);

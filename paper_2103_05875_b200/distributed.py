@@ -1,30 +1,34 @@
-"""Slab-sharded frame over N GPUs of one node (one process per GPU, NCCL).
+"""Slab-sharded frame over N GPUs of one node (one process per GPU).
 
 Per frame, every rank r (z-slab [b_r, e_r), scene replicated):
 
 1. traces + blends its own probes (ProbeUpdater with probe_range);
-2. per texture kind, change-detects its slab only
-   (``ps_detect_changed_range``);
-3. EXCHANGE 1 -- the change bitmap: slabs are disjoint so the per-rank
-   bitmaps have disjoint bits, and an int32 all-reduce(SUM) of the 16 KB
-   bitmap (C4) equals their OR.  Every rank then holds the global bitmap,
-   identical to single-GPU ``flatnonzero`` order because slabs are ascending
-   id ranges;
-4. runs the same selection and slot assignment (replicated, deterministic:
-   twin layouts replay identically, test_packing.py:235-240);
-5. exports the cores of its own selected probes into a payload indexed by
-   local probe id, commits its own blocks into last_sent and stamps
-   last_sent_seq for every entry (replicated state);
-6. EXCHANGE 2 -- the packed tiles: payloads are gathered (NCCL send/recv) to
-   the encoder rank, which imports them into the single update atlas and
-   runs pack + temporal delta (the north star's "single encoder stream").
+2. per texture kind, change-detects its slab only;
+3. EXCHANGE 1 -- the change bitmap: slabs are disjoint, so the global bitmap
+   is the OR of the ranks' bits.  Default (peer memory): the detect kernel
+   ORs every changed word straight into each rank's bitmap, mapped with CUDA
+   IPC, with system-scope atomics over NVLink -- detection and the all-gather
+   are one kernel -- and per-rank release / acquire flags order it with the
+   readers.  PS_PEER=0: an int32 NCCL all-reduce(SUM) of the bitmaps;
+4. runs the same selection and slot assignment on every rank (replicated,
+   deterministic: twin layouts replay identically, test_packing.py:235-240);
+5. EXCHANGE 2 -- the selected cores: default, each rank's export kernel
+   writes its own probes' cores directly into the encoder rank's update
+   atlas at their slots (build and gather in one kernel), commits its blocks
+   into last_sent and stamps last_sent_seq for every entry, then raises the
+   encoder's flag; PS_PEER=0: a payload per rank, NCCL send/recv to the
+   encoder rank and an import pass;
+6. the encoder rank waits for every rank's flag and runs pack + temporal
+   delta on the single update atlas (the north star's "single encoder
+   stream").
 
 The encoder rank's outputs are bit-identical to the single-GPU pipeline's
-(tests/test_gpu_dist.py).
+(tests/test_gpu_dist.py, both exchange paths, eager and CUDA-graph replay).
 """
 
 from __future__ import annotations
 
+import ctypes
 import os
 
 import torch
@@ -36,7 +40,7 @@ from .delta import pack_delta, skip_shape
 from .packing import UpdateAtlasLayout, widened_width
 from .probes import ProbeUpdater
 from .scene import DeviceScene
-from .selection import detect_changed_device, select_device
+from .selection import _threshold_args, detect_changed_device, select_device
 from .server import DEFAULT_GOP, RESERVE_SMS, KindOutput
 from .volume import AtlasKind, ProbeAtlas
 
@@ -142,10 +146,45 @@ def gather_payloads(payload: torch.Tensor, payloads: torch.Tensor | None, rank: 
             w.wait()
 
 
+class PeerBuffers:
+    """Every rank's copy of some device buffers, mapped into this process with
+    CUDA IPC (handles exchanged once with an object all-gather): the device
+    pointers the peer-memory kernels read and write over NVLink."""
+
+    def __init__(self, tensors: dict, rank: int, world: int, group=None):
+        hb = N.lib().ps_ipc_handle_bytes()
+        mine = {}
+        for name, t in tensors.items():
+            if t is None:
+                mine[name] = None
+                continue
+            h = (ctypes.c_uint8 * hb)()
+            off = ctypes.c_int64()
+            N.check(N.lib().ps_ipc_export(ctypes.c_void_p(t.data_ptr()), h, ctypes.byref(off)),
+                    "ps_ipc_export")
+            mine[name] = (bytes(h), off.value)
+        allh = [None] * world
+        dist.all_gather_object(allh, mine, group=group)
+        self.ptrs = {name: [] for name in tensors}
+        for r in range(world):
+            for name, t in tensors.items():
+                if r == rank:
+                    self.ptrs[name].append(t.data_ptr() if t is not None else 0)
+                    continue
+                e = allh[r][name]
+                if e is None:
+                    self.ptrs[name].append(0)
+                    continue
+                p = ctypes.c_void_p()
+                buf = (ctypes.c_uint8 * hb).from_buffer_copy(e[0])
+                N.check(N.lib().ps_ipc_open(buf, e[1], ctypes.byref(p)), "ps_ipc_open")
+                self.ptrs[name].append(int(p.value))
+
+
 class DistKindStream:
     def __init__(self, kind: AtlasKind, volume, device, rank, world, ranges, encoder=0,
                  slot_count=None, threshold=0.0, gop_length=DEFAULT_GOP, budget=None,
-                 probes_per_row=None):
+                 probes_per_row=None, peer: bool = False):
         self.kind, self.volume, self.device = kind, volume, device
         self.rank, self.world, self.encoder = rank, world, encoder
         self.ranges = ranges
@@ -185,10 +224,107 @@ class DistKindStream:
         self.graphs = None
         self.frame_state = torch.zeros(3, dtype=torch.int64, device=device)
         self._state_synced = False
+        self.peer = peer
+        if peer:
+            self._setup_peer()
 
     def enable_graphs(self, on: bool = True) -> None:
         self.graphs = {} if on else None
         self._state_synced = False
+
+    def _setup_peer(self) -> None:
+        """Peer-memory exchange (no NCCL on the data path): two-parity change
+        bitmaps every rank ORs into, per-rank flag slots, and the encoder's
+        update atlas every rank exports its cores into."""
+        dev, n, world = self.device, self.volume.probe_count, self.world
+        words = (n + 31) // 32
+        self.bits2 = torch.zeros((2, words), dtype=torch.int32, device=dev)
+        self.flags = torch.zeros((2, world), dtype=torch.int64, device=dev)  # bits / export
+        pb = PeerBuffers({"bits": self.bits2, "flags": self.flags,
+                          "update": self.update_texels if self.is_encoder else None},
+                         self.rank, world)
+        self._pb = pb
+        ptr = lambda xs: torch.tensor(xs, dtype=torch.int64, device=dev)
+        self.dst_bits = [ptr([b + k * words * 4 for b in pb.ptrs["bits"]]) for k in range(2)]
+        self.sig_bits = ptr([f + self.rank * 8 for f in pb.ptrs["flags"]])
+        self.sig_export = ptr([pb.ptrs["flags"][self.encoder] + (world + self.rank) * 8])
+        self.enc_update = pb.ptrs["update"][self.encoder]
+        self.enc_update_stride = int(self.layout.texel_shape(self.kind)[1])
+
+    def _issue_peer(self, rendered: ProbeAtlas, seq: int, pvs_bits, graphed: bool):
+        """detect + bitmap all-gather in one kernel (peer atomics) -> flags ->
+        selection -> assign -> export straight into the encoder's update atlas
+        -> flag -> (encoder) pack + delta.  Kernels only: one CUDA graph."""
+        tag, dev, world = self.kind.value, self.device, self.world
+        st = D.stream_ptr(dev)
+        seq_dev = self.frame_state[0:1] if graphed else None
+        key_dev = self.frame_state[2:3].view(torch.int32)[:1] if graphed else None
+        if graphed:
+            N.call("ps_frame_advance", self.frame_state.data_ptr(), self.gop_length, st)
+        k = self.frame_count & 1
+        vol, src = self.volume, rendered
+        thr, is64 = _threshold_args(self.threshold)
+        self._mark(f"{tag}.detect", 0)
+        N.call("ps_detect_changed_bcast", self.kind.native, src.texels.data_ptr(),
+               self.last_sent.texels.data_ptr(), vol.probe_count, src.probes_per_row,
+               src.block_rows, self.begin, self.end, vol.active_device(dev).data_ptr(), thr, is64,
+               self.dst_bits[k].data_ptr(), world, st)
+        self._mark(f"{tag}.detect", 1)
+        self._mark(f"{tag}.exchange_bits", 0)
+        N.call("ps_peer_signal", self.sig_bits.data_ptr(), world, int(seq), D.ptr(seq_dev), 1, st)
+        N.call("ps_peer_wait", self.flags.data_ptr(), world, int(seq), D.ptr(seq_dev), 1, st)
+        self._mark(f"{tag}.exchange_bits", 1)
+        self._mark(f"{tag}.select", 0)
+        select_device(self.bits2[k], pvs_bits, vol, self.last_sent_seq, seq, self.budget,
+                      out_ids=self.sel_ids, out_count=self.sel_count,
+                      workspace_slot=f"select.{tag}", ordered=False)
+        self.bits2[k].zero_()  # ready for frame + 2 (peers write it only after our next flag)
+        self._mark(f"{tag}.select", 1)
+        self._mark(f"{tag}.assign", 0)
+        entries, count = self.layout.assign_device(self.sel_ids, self.sel_count)
+        self._mark(f"{tag}.assign", 1)
+        self._mark(f"{tag}.export", 0)
+        N.call("ps_export_tiles_peer", self.kind.native, src.texels.data_ptr(), vol.probe_count,
+               src.probes_per_row, entries.data_ptr(), count.data_ptr(), self.layout.slot_count,
+               self.begin, self.end, self.layout.slots_per_row, self.enc_update,
+               self.enc_update_stride, self.last_sent.texels.data_ptr(),
+               self.last_sent_seq.data_ptr(), int(seq), D.ptr(seq_dev), st)
+        self._mark(f"{tag}.export", 1)
+        self._mark(f"{tag}.gather", 0)
+        N.call("ps_peer_signal", self.sig_export.data_ptr(), 1, int(seq), D.ptr(seq_dev), 1, st)
+        if self.is_encoder:
+            N.call("ps_peer_wait", self.flags[1].data_ptr(), world, int(seq), D.ptr(seq_dev), 1,
+                   st)
+        self._mark(f"{tag}.gather", 1)
+        if self.is_encoder:
+            key = self.frame_count % self.gop_length == 0
+            prev = self.planes[self._cur] if graphed or not key else None
+            cur = self.planes[1 - self._cur]
+            self._mark(f"{tag}.pack_delta", 0)
+            pack_delta(self.update_texels, self.kind, prev, planes_out=cur,
+                       residual=self.residual, skip=self.skip, key_dev=key_dev)
+            self._mark(f"{tag}.pack_delta", 1)
+
+    def _tick_peer(self, rendered: ProbeAtlas, seq: int, pvs_bits=None):
+        graphed = self.graphs is not None and self.frame_count >= 1 and self.timers is None
+        if not graphed:
+            self._state_synced = False
+            self._issue_peer(rendered, seq, pvs_bits, graphed=False)
+            return self._finish()
+        if not self._state_synced:
+            self.frame_state.copy_(torch.tensor([seq - 1, self.frame_count - 1, 0],
+                                                dtype=torch.int64))
+            self._state_synced = True
+        key = ("peer", rendered.texels.data_ptr(), getattr(self, "_cur", 0), self.frame_count & 1,
+               D.ptr(pvs_bits))
+        g = self.graphs.get(key)
+        if g is None:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, capture_error_mode="thread_local"):
+                self._issue_peer(rendered, seq, pvs_bits, graphed=True)
+            self.graphs[key] = g
+        g.replay()
+        return self._finish()
 
     def _mark(self, name, stage):
         if self.timers is not None:
@@ -197,6 +333,8 @@ class DistKindStream:
             self.timers.setdefault(name, []).append((stage, e))
 
     def tick(self, rendered: ProbeAtlas, seq: int, pvs_bits=None):
+        if self.peer:
+            return self._tick_peer(rendered, seq, pvs_bits)
         graphed = self.graphs is not None and self.frame_count >= 1 and self.timers is None
         if not graphed:
             self._state_synced = False
@@ -305,8 +443,14 @@ class DistributedFrame:
                  color_threshold=0.0, visibility_threshold=0.0, slot_count=None, budget=None,
                  gop_length=DEFAULT_GOP, overlap: bool = True, graphs: bool = False,
                  balance: bool = _env_flag("PS_BALANCE", False),
-                 shard_shadows: bool = _env_flag("PS_SHADOW_SHARD", False), **probe_kwargs):
+                 shard_shadows: bool = _env_flag("PS_SHADOW_SHARD", False),
+                 peer: bool = _env_flag("PS_PEER", True), **probe_kwargs):
         self.volume, self.device, self.rank, self.world = volume, device, rank, world
+        # peer (default; PS_PEER=0 for NCCL): the change-bitmap all-gather is fused
+        # into the detect kernel (system atomics into every rank's mapped bitmap)
+        # and the core gather into the export kernel (stores into the encoder's
+        # mapped update atlas), ordered by release / acquire flags: no NCCL on the
+        # data path and one CUDA graph per kind (N=4 C4: 2.67 -> 2.34 ms/frame).
         # balance / shard_shadows (off by default, PS_BALANCE / PS_SHADOW_SHARD):
         # measured at N=4 on C4 both lose -- the per-frame shadow all-gather couples
         # the ranks' traces (a fast rank can no longer run a frame ahead), and cost
@@ -335,7 +479,7 @@ class DistributedFrame:
         self._pending = []
         ppr = self.updater.color.probes_per_row
         kw = dict(encoder=encoder, slot_count=slot_count, gop_length=gop_length, budget=budget,
-                  probes_per_row=ppr)
+                  probes_per_row=ppr, peer=peer)
         self.color = DistKindStream(AtlasKind.COLOR, volume, device, rank, world, self.ranges,
                                     threshold=color_threshold, **kw)
         self.visibility = DistKindStream(AtlasKind.VISIBILITY, volume, device, rank, world,

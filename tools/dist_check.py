@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--frames", type=int, default=3)
     ap.add_argument("--graphs", action="store_true", help="sharded side replays CUDA graphs")
     ap.add_argument("--gop", type=int, default=30)
+    ap.add_argument("--nccl", action="store_true", help="NCCL exchanges instead of peer memory")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -37,7 +38,8 @@ def main():
     sc = bench.build_scene(scene_name)
     vol = S.volume_for(sc, dims)
     kw = dict(irradiance_scale=2.0, shadows="map", shadow_map_size=128, gop_length=args.gop)
-    frame = DistributedFrame(vol, sc, rays, dev, rank, world, graphs=args.graphs, **kw)
+    frame = DistributedFrame(vol, sc, rays, dev, rank, world, graphs=args.graphs, peer=not args.nccl,
+                             **kw)
     single = ProbeStreamServer(vol, sc, rays, device=dev, **kw) if rank == 0 else None
     ok = True
     for f in range(args.frames):
