@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define PS_ABI_VERSION 6
+#define PS_ABI_VERSION 7
 
 /* status codes */
 #define PS_OK 0
@@ -390,6 +390,11 @@ typedef struct ps_trace_params {
      * -1 = miss), shadow mask (int bits, bit l = light l visible), 0);
      * NULL = off */
     float *ray_records;
+    /* sharded shadow maps: when non-NULL the shadow pass stores each map texel
+     * it traces into all shadow_ndst buffers (peers' maps mapped with CUDA
+     * IPC, this rank's included) instead of shadow_maps */
+    float *const *shadow_dst;
+    int32_t shadow_ndst;
 } ps_trace_params;
 
 /* Per-frame weights: from ray_dirs and the texel directions

@@ -16,7 +16,7 @@ from pathlib import Path
 from .errors import LayoutMismatchError, NativeLibraryError, SlotOverflowError
 
 LIB_PATH = Path(os.environ.get("PROBESTREAM_LIB", Path(__file__).resolve().parent / "libprobestream.so"))
-ABI_VERSION = 6
+ABI_VERSION = 7
 
 PS_OK = 0
 PS_ERR_VALUE = -1
@@ -64,6 +64,7 @@ class TraceParams(C.Structure):
         ("probes_per_row_color", _i32), ("probes_per_row_vis", _i32),
         ("records", _vp), ("work_counter", _vp), ("reserve_sms", _i32),
         ("ray_records", _vp),
+        ("shadow_dst", _vp), ("shadow_ndst", _i32),
     ]
 
 

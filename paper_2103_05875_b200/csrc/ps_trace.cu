@@ -184,7 +184,11 @@ __global__ void __launch_bounds__(256) shadow_map_kernel(ps_trace_params prm) {
                 __ldg(prm.lights + 6 * l + 2), d[0] * inv, d[1] * inv, d[2] * inv};
         float t;
         const int slot = traverse<false, 1, WIDTH>(nodes, tris, ray, INFINITY, t);
-        prm.shadow_maps[idx] = slot < 0 ? INFINITY : t;
+        const float v = slot < 0 ? INFINITY : t;
+        if (prm.shadow_dst)
+            for (int d = 0; d < prm.shadow_ndst; ++d) prm.shadow_dst[d][idx] = v;  // peers too
+        else
+            prm.shadow_maps[idx] = v;
     }
 }
 

@@ -470,9 +470,13 @@ class DistributedFrame:
                                     probe_range=self.ranges[rank],
                                     atlas_buffers=2 if overlap else 1,
                                     reserve_sms=probe_kwargs.pop("reserve_sms", RESERVE_SMS) if overlap else 0, **probe_kwargs)
-        # shadow maps: each rank traces 1/world of the texels, all-gathered
+        # shadow maps: each rank traces 1/world of the texels; peer mode stores
+        # them into every rank's maps directly, NCCL mode all-gathers them
         if shard_shadows:
-            self.updater.shadow_split = (rank, world, None)
+            if peer:
+                self.updater.set_shadow_peers(rank, world)
+            else:
+                self.updater.shadow_split = (rank, world, None)
         self.streams = {"color": torch.cuda.Stream(device, priority=-1),
                         "visibility": torch.cuda.Stream(device, priority=-1)}
         self._buf_done = [[], []]

@@ -199,9 +199,35 @@ class ProbeUpdater:
         # each rank traces a slice of the map texels and the slices are
         # all-gathered before the probe rays are traced
         self.shadow_split = None
+        # peer-memory variant (set_shadow_peers): the slice is stored straight
+        # into every rank's mapped maps, ordered by flags -- no collective
+        self.shadow_peer = None
 
     def enable_graphs(self, on: bool = True) -> None:
         self.graphs = {} if on else None
+
+    def set_shadow_peers(self, rank: int, world: int, group=None) -> None:
+        """Shard the shadow-map pass over the process group through peer
+        memory: two-parity maps mapped into every rank (CUDA IPC), the shadow
+        kernel stores its texel slice into all of them, then a release flag per
+        rank and an acquire wait before the probe rays are traced."""
+        from .distributed import PeerBuffers
+
+        if self.shadow_mode != N.PS_SHADOW_MAP or world < 2:
+            return
+        dev = self.device
+        maps2 = torch.empty((2,) + tuple(self.shadow_maps.shape), dtype=torch.float32, device=dev)
+        flags = torch.zeros(world, dtype=torch.int64, device=dev)
+        pb = PeerBuffers({"maps": maps2, "flags": flags}, rank, world, group)
+        per = self.shadow_maps.numel() * 4
+        ptr = lambda xs: torch.tensor(xs, dtype=torch.int64, device=dev)
+        self.shadow_peer = {
+            "maps2": maps2, "flags": flags, "pb": pb,
+            "dst": [ptr([m + k * per for m in pb.ptrs["maps"]]) for k in range(2)],
+            "sig": ptr([f + rank * 8 for f in pb.ptrs["flags"]]),
+            "state": torch.zeros(3, dtype=torch.int64, device=dev),
+        }
+        self.shadow_split = (rank, world, group)
 
     def _shadow_slice(self):
         """(begin, end, chunk) of this rank's map texels, or None when unsharded."""
@@ -216,7 +242,8 @@ class ProbeUpdater:
             return None  # no room for the padded gather: every rank traces all texels
         return rank * chunk, min((rank + 1) * chunk, total), chunk
 
-    def _params(self, hysteresis: float, passes: int = 0, texels=None) -> N.TraceParams:
+    def _params(self, hysteresis: float, passes: int = 0, texels=None, shadow_maps=None,
+                shadow_dst=None, ndst: int = 0) -> N.TraceParams:
         v, s = self.volume, self.dscene
         p = N.TraceParams()
         p.nx, p.ny, p.nz = v.dims
@@ -234,7 +261,10 @@ class ProbeUpdater:
         p.normal_bias = self.normal_bias
         p.shadow_mode = self.shadow_mode
         p.shadow_map_size = self.shadow_map_size
-        p.shadow_maps = self.shadow_maps.data_ptr() if self.shadow_maps is not None else None
+        maps = shadow_maps if shadow_maps is not None else self.shadow_maps
+        p.shadow_maps = maps.data_ptr() if maps is not None else None
+        p.shadow_dst = D.ptr(shadow_dst)
+        p.shadow_ndst = ndst
         p.shadow_bias = self.shadow_bias
         p.passes = passes
         if texels is not None:
@@ -274,10 +304,35 @@ class ProbeUpdater:
     def _issue(self, hysteresis: float) -> None:
         """Weights + shadow maps + trace + blend on the current stream."""
         sl = self._shadow_slice()
+        if self.shadow_peer is not None and sl is not None:
+            self._issue_peer(hysteresis, sl)
+            return
         self._issue_pre(hysteresis, sl)
         if sl is not None:
             self._gather_shadow(sl)
             self._issue_post(hysteresis)
+
+    def _issue_peer(self, hysteresis: float, sl) -> None:
+        """Weights, this rank's shadow slice into every rank's maps (parity k),
+        flag, wait for all slices, trace + blend: kernels only."""
+        sp = self.shadow_peer
+        stream = D.stream_ptr(self.device)
+        k = self.frames_done & 1
+        rank, world = self.shadow_split[:2]
+        N.call("ps_blend_weights", self.ray_dirs.data_ptr(), self.rays_per_probe,
+               self.texdir.data_ptr(), self.sharpness, self.w_color.data_ptr(),
+               self.w_depth.data_ptr(), self.inv_wsum.data_ptr(), D.ptr(self.w_image), stream)
+        N.call("ps_frame_advance", sp["state"].data_ptr(), 1 << 30, stream)
+        b, e, _ = sl
+        if e > b:
+            params = self._params(hysteresis, passes=1, texels=(b, e), shadow_maps=sp["maps2"][k],
+                                  shadow_dst=sp["dst"][k], ndst=world)
+            N.call("ps_trace_blend", ctypes.byref(params), stream)
+        seq = sp["state"][0:1]
+        N.call("ps_peer_signal", sp["sig"].data_ptr(), world, 0, seq.data_ptr(), 1, stream)
+        N.call("ps_peer_wait", sp["flags"].data_ptr(), world, 0, seq.data_ptr(), 1, stream)
+        params = self._params(hysteresis, passes=6, shadow_maps=sp["maps2"][k])
+        N.call("ps_trace_blend", ctypes.byref(params), stream)
 
     def _issue_pre(self, hysteresis: float, sl) -> None:
         """Weights, then everything (unsharded) or this rank's shadow-map slice."""
@@ -329,6 +384,13 @@ class ProbeUpdater:
         sl = self._shadow_slice()
         key = (k, kb, s.light_count)
         g = self.graphs.get(key)
+        if g is None and self.shadow_peer is not None and sl is not None:
+            g = [torch.cuda.CUDAGraph()]  # peer shadow maps: no collective, one graph
+            with torch.cuda.graph(g[0], capture_error_mode="thread_local"):
+                self.ray_dirs.copy_(self._pinned_dirs[k], non_blocking=True)
+                s.lights.copy_(self._pinned_lights[k], non_blocking=True)
+                self._issue_peer(self.hysteresis, sl)
+            self.graphs[key] = g
         if g is None:
             # unsharded: one graph; sharded shadow maps: graph (inputs, weights, map
             # slice) -> eager NCCL all-gather -> graph (trace, blend)

@@ -54,6 +54,14 @@ class SlabServer:
 
     # --- bench helpers ----------------------------------------------------------------
 
+    def _barrier(self) -> None:
+        torch.cuda.synchronize(self.device)
+        if self.world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+            torch.cuda.synchronize(self.device)
+
     def run_e2e(self, steps: int, first_frame: int, lights_for):
         """Public-API frames with host I/O: per step the ray table and lights go
         H2D from pinned memory (inside tick) and the index entries, counts and
@@ -73,7 +81,7 @@ class SlabServer:
         h2d = impl.h2d_bytes_per_frame()
         stream = torch.cuda.current_stream(self.device)
         start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize(self.device)
+        self._barrier()  # every rank done with its setup before any starts the clock
         start.record(stream)
         for k in range(steps):
             f = first_frame + 1 + k
@@ -135,7 +143,7 @@ class SlabServer:
 
             stream = torch.cuda.current_stream(self.device)
             start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            torch.cuda.synchronize(self.device)
+            self._barrier()
             start.record(stream)
             prev = None
             for k in range(steps):
