@@ -408,6 +408,11 @@ size_t ps_blend_weight_image_floats(int32_t rays_per_probe);
 
 int ps_trace_blend(const ps_trace_params *params, void *stream);
 
+/* Tuning only: traversal statistics gathered by the PS_TRACE_VARIANT=90
+ * kernel, {inner-node visits, leaf visits, triangle tests, rays}; reset on
+ * read. */
+int ps_trace_stats(unsigned long long *out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -79,11 +79,11 @@ template <int SHADOW, int WIDTH>
 __device__ Shade shade_hit(const ps_trace_params &p, const float4 *nodes, const float4 *tris,
                            const Ray &ray, int slot, float t);
 
-template <int SHADOW, int LEAFV, int WIDTH>
+template <int SHADOW, int LEAFV, int WIDTH, int STATS = 0>
 __device__ Shade shade_ray(const ps_trace_params &p, const float4 *nodes, const float4 *tris,
                            const Ray &ray) {
     float t;
-    const int slot = traverse<false, LEAFV, WIDTH>(nodes, tris, ray, INFINITY, t);
+    const int slot = traverse<false, LEAFV, WIDTH, STATS>(nodes, tris, ray, INFINITY, t);
     return shade_hit<SHADOW, WIDTH>(p, nodes, tris, ray, slot, t);
 }
 
@@ -202,7 +202,8 @@ __global__ void __launch_bounds__(256) shadow_map_kernel(ps_trace_params prm) {
 // grid of sms - reserve CTAs leaves whole SMs free (a grid of 256-thread CTAs
 // would be spread over every SM and leave only fragments, too small for NCCL's
 // kernels).  The kernel is per-warp, so the block size is free.
-template <int SHADOW, int LEAFV, int MINB, int PROBE_PARALLEL, int WIDTH, int TPB = THREADS>
+template <int SHADOW, int LEAFV, int MINB, int PROBE_PARALLEL, int WIDTH, int TPB = THREADS,
+          int STATS = 0>
 __global__ void __launch_bounds__(TPB, TPB == THREADS ? MINB : 1) trace_kernel(ps_trace_params prm) {
     const float4 *nodes = reinterpret_cast<const float4 *>(prm.nodes);
     const float4 *tris = reinterpret_cast<const float4 *>(prm.tris);
@@ -247,7 +248,7 @@ __global__ void __launch_bounds__(TPB, TPB == THREADS ? MINB : 1) trace_kernel(p
         ray.dx = d.x;
         ray.dy = d.y;
         ray.dz = d.z;
-        const Shade s = shade_ray<SHADOW, LEAFV, WIDTH>(prm, nodes, tris, ray);
+        const Shade s = shade_ray<SHADOW, LEAFV, WIDTH, STATS>(prm, nodes, tris, ray);
         const int64_t ray_id = q * R + r;
         records[ray_id] = make_float4(s.r, s.g, s.b, s.depth);
         if (prm.ray_records) {
@@ -703,6 +704,11 @@ void launch_trace_s(const ps_trace_params &p, int variant, int sms, cudaStream_t
             case 10: launch_trace_t<SHADOW, 0, 4, 0, 4>(p, sms, s, big); break;
             case 11: launch_trace_t<SHADOW, 1, 4, 0, 4>(p, sms, s, big); break;
             case 30: launch_trace_t<SHADOW, 1, 1, 1, 4>(p, sms, s, big); break;
+            case 90: {  // traversal statistics (tuning only)
+                const int per_sm = resident_blocks(trace_kernel<SHADOW, 1, 1, 0, 4, THREADS, 1>, THREADS, 0);
+                trace_kernel<SHADOW, 1, 1, 0, 4, THREADS, 1><<<sms * per_sm, THREADS, 0, s>>>(p);
+                break;
+            }
             default: launch_trace_t<SHADOW, 1, 1, 0, 4>(p, sms, s, big); break;
         }
         return;
@@ -732,6 +738,17 @@ void launch_trace(const ps_trace_params &p, int variant, int sms, cudaStream_t s
 using namespace ps;
 
 extern "C" {
+
+// traversal statistics of PS_TRACE_VARIANT=90 (tuning only): {inner-node
+// visits, leaf visits, triangle tests, rays}; reset after reading
+int ps_trace_stats(unsigned long long *out) {
+    PS_ABI_BEGIN
+    check_cuda(cudaMemcpyFromSymbol(out, trav::g_trav_stats, sizeof(unsigned long long) * 4),
+               "read stats");
+    const unsigned long long zero[4] = {0, 0, 0, 0};
+    check_cuda(cudaMemcpyToSymbol(trav::g_trav_stats, zero, sizeof(zero)), "reset stats");
+    PS_ABI_END
+}
 
 size_t ps_blend_weight_image_floats(int32_t rays_per_probe) {
     return weight_image_floats(rays_per_probe);

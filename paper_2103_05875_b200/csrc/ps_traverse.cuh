@@ -162,9 +162,14 @@ __device__ __forceinline__ void node4h_hits(const float4 *nodes, int node, float
     cswap(d[1], c[1], d[2], c[2]);
 }
 
-template <bool ANY_HIT, int LEAFV = 0, int WIDTH = 2>
+// traversal statistics of the STATS variant (tuning only): inner-node visits,
+// leaf visits, triangle tests, rays
+static __device__ unsigned long long g_trav_stats[4];
+
+template <bool ANY_HIT, int LEAFV = 0, int WIDTH = 2, int STATS = 0>
 __device__ int traverse(const float4 *__restrict__ nodes, const float4 *__restrict__ tris,
                         const Ray &r, float tmax, float &t_best) {
+    unsigned long long st_nodes = 0, st_leaves = 0, st_tris = 0;
     // reciprocal direction; tiny components replaced so the slabs stay finite
     const float sx = fabsf(r.dx) < 1e-12f ? copysignf(1e-12f, r.dx) : r.dx;
     const float sy = fabsf(r.dy) < 1e-12f ? copysignf(1e-12f, r.dy) : r.dy;
@@ -177,6 +182,13 @@ __device__ int traverse(const float4 *__restrict__ nodes, const float4 *__restri
     int hit_slot = -1;
     t_best = tmax;
     while (true) {
+        if (STATS) {
+            if (node >= 0) ++st_nodes;
+            else {
+                ++st_leaves;
+                st_tris += (~node) & 7;
+            }
+        }
         if (node >= 0 && (WIDTH == 4 || WIDTH == 5)) {
             float d[4];
             int c[4];
@@ -290,6 +302,12 @@ __device__ int traverse(const float4 *__restrict__ nodes, const float4 *__restri
             }
         }
         if (!found) break;
+    }
+    if (STATS) {
+        atomicAdd(&g_trav_stats[0], st_nodes);
+        atomicAdd(&g_trav_stats[1], st_leaves);
+        atomicAdd(&g_trav_stats[2], st_tris);
+        atomicAdd(&g_trav_stats[3], 1ull);
     }
     return hit_slot;
 }
