@@ -124,6 +124,22 @@ def load_peaks():
     return 6650.0, "fallback"
 
 
+def profile_metric(prefix: str, key: str):
+    """A fraction (pct / 100) for the first kernel starting with `prefix` in the
+    committed ncu summary, or None."""
+    p = ROOT / "profiles" / "ncu_summary.json"
+    if not p.exists():
+        return None
+    try:
+        d = json.loads(p.read_text()).get("kernels", {})
+        for k, v in d.items():
+            if k.startswith(prefix) and key in v:
+                return round(float(v[key]) / 100.0, 4)
+    except Exception:
+        return None
+    return None
+
+
 def profile_traffic(prefix: str):
     """DRAM bytes (read + write) per launch, summed over the kernels whose name
     starts with `prefix` (one launch per texture kind), from the committed
@@ -221,12 +237,17 @@ def run_ours(args, rank, world, local):
     slabs = getattr(server.impl, "ranges", None)
     launches_per_step, kernel_names = server.count_launches(base + 3, frame_lights)
     encode = server.encode_times() if world == 1 else {}
+    passes = server.pass_times()  # last: re-running the blend advances the probe state
 
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
     rays_total = n * rays
+    # tcgen05 blend flops issued per frame: per probe and k-step of 8 rays, two
+    # depth tiles (128 x 2P... per probe 128 texels x 2 moments x 8 rays x 2 flops)
+    # and one colour tile (128 x 3 channels x 8) -- each issued twice (hi, lo)
+    blend_flops = n * (rays // 8) * 2 * 2 * 8 * (2 * 128 * 2 + 128 * 3)
     value = n / (ms_max / 1e3)
     peak, peak_kind = load_peaks()
     # roofline of the HBM-bound pack kernel (pack + temporal delta over the update atlas)
@@ -278,10 +299,28 @@ def run_ours(args, rank, world, local):
             "algorithmic_bytes_per_launch": pk,
         },
         "roofline_trace": {
-            "kernel": "trace_blend_kernel",
-            "rays_per_s": round(rays_total / (trace_ms / 1e3), 1) if trace_ms else None,
-            "ms": trace_ms,
-            "note": "no dense roofline (BVH traversal, SIMT); see profiles/ for SM/L1 throughput",
+            "kernel": "trace_kernel (probe rays, this rank's slab; CUDA events, pass alone)",
+            "ms": round(passes["trace"], 4),
+            "rays_per_s": round(rays_total / world / (passes["trace"] / 1e3), 1),
+            "l1_data_pipe_frac": profile_metric("trace_kernel", "l1_pct"),
+            "sm_frac": profile_metric("trace_kernel", "sm_pct"),
+            "note": "BVH traversal on SIMT cores has no dense roofline: bound by L1 "
+                    "data-pipe wavefronts of divergent node fetches (fractions from "
+                    "profiles/ncu_summary.json); 10.7 inner nodes, 1.1 leaves, 2.4 "
+                    "triangle tests per ray (tools/trav_stats.py)",
+        },
+        "roofline_blend": {
+            "bound": "tensor",
+            "kernel": "blend_tc_kernel (tcgen05.mma kind::tf32, this rank's slab)",
+            "ms": round(passes["blend"], 4),
+            "achieved": round(blend_flops / world / (passes["blend"] / 1e3) / 1e12, 2),
+            "peak": 1100.0,
+            "unit": "TFLOP/s",
+            "frac": round(blend_flops / world / (passes["blend"] / 1e3) / 1e12 / 1100.0, 4),
+            "flops_per_launch": blend_flops // world,
+            "note": "tf32 MMA flops issued: 2 MMAs (W*B_hi + W*B_lo) per 128-texel tile, "
+                    "colour tile padded to 128 rows; peak = B200 dense tf32 (B200_PROFILING.md); "
+                    "the useful fp32 work is 47 GFLOP/frame at C4",
         },
         "clocks": clocks.summary(),
         "e2e": {"value": round(n / (e2e_ms / 1e3), 1), "unit": "probe updates/s",

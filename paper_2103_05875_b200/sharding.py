@@ -210,6 +210,12 @@ class SlabServer:
     def pack_delta_bytes(self) -> dict:
         return self.impl.pack_delta_bytes()
 
+    def pass_times(self, reps: int = 3) -> dict:
+        """Probe-ray and blend pass device times of this rank (last measurement:
+        it advances the probe state)."""
+        torch.cuda.synchronize(self.device)
+        return self.impl.updater.pass_times_ms(reps)
+
     def encode_times(self, reps: int = 3) -> dict:
         """§8(f)1 LPF1 encoding of the last frame's planes (key and P-frame),
         device time per frame and compression ratio; not part of the step."""
