@@ -182,14 +182,43 @@ __global__ void __launch_bounds__(TILE_X *TILE_Y)
         for (int e = 0; e < 3; ++e) dirty[e][tx] = 0u;
     __syncthreads();
     if (seg < a.nseg && r < a.h) {
+        // colour keeps the 16 texel words and extracts one plane at a time (the
+        // three planes at once held ~120 registers); visibility's byte shuffles
+        // produce all planes together
         uint32_t cur[3][8];
-        load_segment<KIND>(a, r, seg, cur);
+        uint32_t tex[16];
+        if (KIND == PS_KIND_COLOR) {
+            const int64_t x0 = seg * SEG;
+            const uint8_t *row = a.texels + r * a.row_stride_b;
+            if (a.vec_in && x0 + 16 <= a.w) {
+                const uint4 *p = reinterpret_cast<const uint4 *>(row + x0 * 4);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const uint4 q = __ldg(p + i);
+                    tex[4 * i] = q.x;
+                    tex[4 * i + 1] = q.y;
+                    tex[4 * i + 2] = q.z;
+                    tex[4 * i + 3] = q.w;
+                }
+            } else {
+                const uint32_t *p = reinterpret_cast<const uint32_t *>(row);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) tex[i] = (x0 + i < a.w) ? __ldg(p + x0 + i) : 0u;
+            }
+        } else {
+            load_segment<KIND>(a, r, seg, cur);
+        }
         const int64_t x0_b = seg * NB;
         const int64_t valid_b = (a.pw - seg * SEG) * EB;
         const int64_t plane_b = a.h * a.pw * EB;
         const int64_t row_b = r * a.pw * EB;
 #pragma unroll
         for (int e = 0; e < 3; ++e) {
+            if (KIND == PS_KIND_COLOR) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    cur[e][i] = bfe10(tex[2 * i], e) | (bfe10(tex[2 * i + 1], e) << 16);
+            }
             uint8_t *dst = a.cur + e * plane_b + row_b;
             if (a.prev) {
                 uint32_t pv[8];
