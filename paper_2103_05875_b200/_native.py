@@ -109,6 +109,7 @@ _SIGNATURES = {
     "ps_index_workspace_bytes": (_sz, [_i64]),
     "ps_encode_index": (_int, [_vp, _vp, _i64, _vp, _vp, _vp, _sz, _vp]),
     "ps_frame_advance": (_int, [_vp, _i64, _vp]),
+    "ps_trace_stats": (_int, [_vp]),
     "ps_detect_changed_bcast": (_int, [_int, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _f64,
                                        _int, _vp, _int, _vp]),
     "ps_export_tiles_peer": (_int, [_int, _vp, _i64, _i64, _vp, _vp, _i64, _i64, _i64, _i64, _vp,
