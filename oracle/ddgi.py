@@ -40,6 +40,9 @@ def _lib():
         vp, i64 = ctypes.c_void_p, ctypes.c_int64
         lib.oracle_raycast.argtypes = [vp, i64, vp, vp, i64, vp, vp]
         lib.oracle_occluded.argtypes = [vp, i64, vp, vp, vp, i64, vp]
+        lib.oracle_set_threads.argtypes = [ctypes.c_int]
+        # every host thread, whatever OMP_NUM_THREADS a launcher exported
+        lib.oracle_set_threads(int(os.environ.get("PS_ORACLE_THREADS", os.cpu_count() or 1)))
         _LIB = lib
     return _LIB
 

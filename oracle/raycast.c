@@ -16,6 +16,9 @@
  * three-element reduction does.
  */
 #include <math.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 #include <stdint.h>
 
 #define EPS 1e-6
@@ -48,6 +51,16 @@ static inline double tri_t(const double *tri, const double *o, const double *d) 
     const double t = dot3(e2, q) * inv;
     if (u >= -EPS && v >= -EPS && u + v <= 1.0 + EPS && t > EPS) return t;
     return INFINITY;
+}
+
+/* OpenMP team size (torchrun exports OMP_NUM_THREADS=1 to every rank; the
+ * CPU baseline wants every host thread) */
+void oracle_set_threads(int n) {
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
 }
 
 /* nearest hit per ray; prim = -1 on a miss */
