@@ -193,10 +193,16 @@ __global__ void __launch_bounds__(256) shadow_map_kernel(ps_trace_params prm) {
 }
 
 // ---- pass 1: probe rays -> per-ray records (persistent, dynamic chunks) -----------------
-// A warp claims 32 consecutive rays of one probe (neighbouring directions in
-// the coherence-ordered set) from a global counter, traces + shades them and
-// writes {rgb, depth}.  Dynamic claiming keeps every SM busy regardless of the
-// large per-direction cost differences.
+// A warp claims a chunk of 32 rays from a global counter, traces + shades them
+// and writes {rgb, depth}; dynamic claiming keeps every SM busy regardless of
+// the large per-chunk cost differences.  The chunk shape is the kernel's main
+// lever (PROBE_PARALLEL): every probe shoots the same frame-rotated ray set, so
+// the default chunk is ONE direction for a compact 2 x 4 x 4 tile of probes --
+// 32 near-parallel rays from origins at most 1.5 x 2 x 2 spacings apart that
+// walk largely the same BVH nodes, so a warp's node fetches hit few lines
+// (6.74 ms vs 7.90 ms per C4 trace + blend for 32 neighbouring directions of
+// one probe, 8.70 ms for a row of 32 probes; more than one direction per warp
+// was slower).
 // TPB = 1024 is the "SM-sized" launch used when SMs are reserved for
 // concurrent streams: one CTA fills an SM (64 registers x 1024 threads), so a
 // grid of sms - reserve CTAs leaves whole SMs free (a grid of 256-thread CTAs
@@ -216,7 +222,24 @@ __global__ void __launch_bounds__(TPB, TPB == THREADS ? MINB : 1) trace_kernel(p
     // (parallel rays from neighbouring origins) instead of 32 directions of
     // one probe
     const int64_t probe_groups = (nloc + 31) / 32;
-    const int64_t total_chunks = PROBE_PARALLEL ? probe_groups * R : nloc * chunks_per_probe;
+    // PROBE_PARALLEL == 2: one direction for a compact 4 x 4 x 2 tile of probes
+    // (near-parallel rays from origins <= 2 spacings apart walk the same nodes)
+    const int64_t plane = int64_t(prm.nx) * prm.ny;
+    const int64_t k0 = prm.probe_begin / plane;
+    const int64_t k1 = nloc > 0 ? (prm.probe_end - 1) / plane : k0;
+    // tile shapes (x, y, z probes) x D neighbouring directions = 32 rays
+    constexpr int PPV = PROBE_PARALLEL;
+    constexpr int TX = PPV == 3 || PPV == 6 ? 8 : (PPV == 4 || PPV >= 8) ? 2 : 4;
+    constexpr int TY = PPV == 5 || PPV == 6 || PPV >= 8 ? 2 : 4;
+    constexpr int DD = PPV == 8 ? 2 : PPV == 9 ? 4 : PPV == 10 ? 8 : 1;
+    constexpr int TZ = 32 / (TX * TY * DD);
+    constexpr bool TILED = PROBE_PARALLEL >= 2;
+    const int64_t tiles_x = (prm.nx + TX - 1) / TX, tiles_y = (prm.ny + TY - 1) / TY;
+    const int64_t tiles_z = (k1 - k0 + TZ) / TZ;
+    const int64_t tiles = tiles_x * tiles_y * tiles_z;
+    const int64_t dgroups = (R + DD - 1) / DD;
+    const int64_t total_chunks = TILED ? tiles * dgroups
+                               : PROBE_PARALLEL ? probe_groups * R : nloc * chunks_per_probe;
     const int lane = threadIdx.x & 31;
     float4 *records = reinterpret_cast<float4 *>(prm.records);
     while (true) {
@@ -226,7 +249,24 @@ __global__ void __launch_bounds__(TPB, TPB == THREADS ? MINB : 1) trace_kernel(p
         if (int64_t(task) >= total_chunks) break;
         int64_t q;
         int r;
-        if (PROBE_PARALLEL) {
+        if (TILED) {
+            int64_t t;
+            if (PROBE_PARALLEL == 7) {  // direction-major: all tiles for one direction
+                r = int(int64_t(task) / tiles);
+                t = int64_t(task) - int64_t(r) * tiles;
+            } else {
+                t = int64_t(task) / dgroups;
+                r = int(int64_t(task) - t * dgroups) * DD + lane / (TX * TY * TZ);
+                if (r >= R) continue;
+            }
+            const int pl = lane % (TX * TY * TZ);
+            const int64_t tx = t % tiles_x, ty = (t / tiles_x) % tiles_y, tz = t / (tiles_x * tiles_y);
+            const int64_t pi = tx * TX + (pl % TX), pj = ty * TY + ((pl / TX) % TY);
+            const int64_t pk = k0 + tz * TZ + pl / (TX * TY);
+            const int64_t pp = pi + prm.nx * (pj + prm.ny * pk);
+            if (pi >= prm.nx || pj >= prm.ny || pp < prm.probe_begin || pp >= prm.probe_end) continue;
+            q = pp - prm.probe_begin;
+        } else if (PROBE_PARALLEL) {
             const int64_t g = int64_t(task) / R;
             r = int(int64_t(task) - g * R);
             q = g * 32 + lane;
@@ -704,11 +744,20 @@ void launch_trace_s(const ps_trace_params &p, int variant, int sms, cudaStream_t
             case 10: launch_trace_t<SHADOW, 0, 4, 0, 4>(p, sms, s, big); break;
             case 11: launch_trace_t<SHADOW, 1, 4, 0, 4>(p, sms, s, big); break;
             case 30: launch_trace_t<SHADOW, 1, 1, 1, 4>(p, sms, s, big); break;
+            case 32: launch_trace_t<SHADOW, 1, 1, 2, 4>(p, sms, s, big); break;
+            case 33: launch_trace_t<SHADOW, 1, 1, 3, 4>(p, sms, s, big); break;
+            case 35: launch_trace_t<SHADOW, 1, 1, 5, 4>(p, sms, s, big); break;
+            case 36: launch_trace_t<SHADOW, 1, 1, 6, 4>(p, sms, s, big); break;
+            case 37: launch_trace_t<SHADOW, 1, 1, 7, 4>(p, sms, s, big); break;
+            case 38: launch_trace_t<SHADOW, 1, 1, 8, 4>(p, sms, s, big); break;
+            case 39: launch_trace_t<SHADOW, 1, 1, 9, 4>(p, sms, s, big); break;
+            case 40: launch_trace_t<SHADOW, 1, 1, 10, 4>(p, sms, s, big); break;
             case 90: {  // traversal statistics (tuning only)
                 const int per_sm = resident_blocks(trace_kernel<SHADOW, 1, 1, 0, 4, THREADS, 1>, THREADS, 0);
                 trace_kernel<SHADOW, 1, 1, 0, 4, THREADS, 1><<<sms * per_sm, THREADS, 0, s>>>(p);
                 break;
             }
+            case 34: launch_trace_t<SHADOW, 1, 1, 4, 4>(p, sms, s, big); break;
             default: launch_trace_t<SHADOW, 1, 1, 0, 4>(p, sms, s, big); break;
         }
         return;
@@ -825,7 +874,7 @@ int ps_trace_blend(const ps_trace_params *params, void *stream) {
         // 2 = four in flight; +10 = cap registers for 4 resident CTAs per SM
         static const int variant = [] {
             const char *e = getenv("PS_TRACE_VARIANT");
-            return e ? atoi(e) : 1;
+            return e ? atoi(e) : 34;  // BVH4: 2 x 4 x 4 probe tiles, one direction per warp
         }();
         const int keep = p.reserve_sms > 0 && p.reserve_sms < sms / 2 ? p.reserve_sms : 0;
         launch_trace(p, variant, sms - keep, s, keep > 0);
