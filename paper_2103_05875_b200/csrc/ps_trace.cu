@@ -197,12 +197,13 @@ __global__ void __launch_bounds__(256) shadow_map_kernel(ps_trace_params prm) {
 // and writes {rgb, depth}; dynamic claiming keeps every SM busy regardless of
 // the large per-chunk cost differences.  The chunk shape is the kernel's main
 // lever (PROBE_PARALLEL): every probe shoots the same frame-rotated ray set, so
-// the default chunk is ONE direction for a compact 2 x 4 x 4 tile of probes --
-// 32 near-parallel rays from origins at most 1.5 x 2 x 2 spacings apart that
-// walk largely the same BVH nodes, so a warp's node fetches hit few lines
-// (6.74 ms vs 7.90 ms per C4 trace + blend for 32 neighbouring directions of
-// one probe, 8.70 ms for a row of 32 probes; more than one direction per warp
-// was slower).
+// the default chunk is ONE direction for a compact tile of probes (2 x 2 x 8
+// when the slab is 8 planes deep) -- 32 near-parallel rays from neighbouring
+// origins that walk largely the same BVH nodes, so a warp's node fetches hit
+// few lines
+// (6.18 ms per C4 trace + blend for a 2 x 2 x 8 tile vs 7.90 ms for 32
+// neighbouring directions of one probe and 8.70 ms for a row of 32 probes;
+// more than one direction per warp was slower).
 // TPB = 1024 is the "SM-sized" launch used when SMs are reserved for
 // concurrent streams: one CTA fills an SM (64 registers x 1024 threads), so a
 // grid of sms - reserve CTAs leaves whole SMs free (a grid of 256-thread CTAs
@@ -229,9 +230,9 @@ __global__ void __launch_bounds__(TPB, TPB == THREADS ? MINB : 1) trace_kernel(p
     const int64_t k1 = nloc > 0 ? (prm.probe_end - 1) / plane : k0;
     // tile shapes (x, y, z probes) x D neighbouring directions = 32 rays
     constexpr int PPV = PROBE_PARALLEL;
-    constexpr int TX = PPV == 3 || PPV == 6 ? 8 : (PPV == 4 || PPV >= 8) ? 2 : 4;
-    constexpr int TY = PPV == 5 || PPV == 6 || PPV >= 8 ? 2 : 4;
-    constexpr int DD = PPV == 8 ? 2 : PPV == 9 ? 4 : PPV == 10 ? 8 : 1;
+    constexpr int TX = PPV == 11 ? 1 : (PPV == 3 || PPV == 6) ? 8 : (PPV == 4 || PPV >= 8) ? 2 : 4;
+    constexpr int TY = PPV == 11 ? 4 : PPV == 13 ? 8 : (PPV == 5 || PPV == 6 || PPV >= 8) ? 2 : 4;
+    constexpr int DD = PPV == 8 ? 2 : PPV == 9 ? 4 : PPV == 10 ? 8 : 1;  // 11-13: 1
     constexpr int TZ = 32 / (TX * TY * DD);
     constexpr bool TILED = PROBE_PARALLEL >= 2;
     const int64_t tiles_x = (prm.nx + TX - 1) / TX, tiles_y = (prm.ny + TY - 1) / TY;
@@ -752,6 +753,16 @@ void launch_trace_s(const ps_trace_params &p, int variant, int sms, cudaStream_t
             case 38: launch_trace_t<SHADOW, 1, 1, 8, 4>(p, sms, s, big); break;
             case 39: launch_trace_t<SHADOW, 1, 1, 9, 4>(p, sms, s, big); break;
             case 40: launch_trace_t<SHADOW, 1, 1, 10, 4>(p, sms, s, big); break;
+            case 41: launch_trace_t<SHADOW, 1, 1, 11, 4>(p, sms, s, big); break;  // 1x4x8
+            case 42: launch_trace_t<SHADOW, 1, 1, 12, 4>(p, sms, s, big); break;  // 2x2x8
+            case 43: launch_trace_t<SHADOW, 1, 1, 13, 4>(p, sms, s, big); break;  // 2x8x2
+            case 44: launch_trace_t<SHADOW, 0, 1, 4, 4>(p, sms, s, big); break;   // 2x4x4, seq leaf
+            case 45: launch_trace_t<SHADOW, 1, 4, 4, 4>(p, sms, s, big); break;   // 2x4x4, 4 CTAs/SM
+            case 46: launch_trace_t<SHADOW, 0, 1, 12, 4>(p, sms, s, big); break;  // 2x2x8, seq leaf
+            case 47: launch_trace_t<SHADOW, 0, 1, 11, 4>(p, sms, s, big); break;  // 1x4x8, seq leaf
+            case 48: launch_trace_t<SHADOW, 2, 1, 12, 4>(p, sms, s, big); break;  // 2x2x8, 4-wide leaf
+            case 49: launch_trace_t<SHADOW, 2, 1, 4, 4>(p, sms, s, big); break;   // 2x4x4, 4-wide leaf
+            case 50: launch_trace_t<SHADOW, 0, 1, 2, 4>(p, sms, s, big); break;   // 4x4x2, seq leaf
             case 90: {  // traversal statistics (tuning only)
                 const int per_sm = resident_blocks(trace_kernel<SHADOW, 1, 1, 0, 4, THREADS, 1>, THREADS, 0);
                 trace_kernel<SHADOW, 1, 1, 0, 4, THREADS, 1><<<sms * per_sm, THREADS, 0, s>>>(p);
@@ -872,10 +883,17 @@ int ps_trace_blend(const ps_trace_params *params, void *stream) {
         check_cuda(cudaMemsetAsync(p.work_counter, 0, sizeof(uint32_t), s), "memset counter");
         // PS_TRACE_VARIANT (tuning knob): leaf fetch 0 = sequential, 1 = pairs,
         // 2 = four in flight; +10 = cap registers for 4 resident CTAs per SM
-        static const int variant = [] {
+        static const int forced = [] {
             const char *e = getenv("PS_TRACE_VARIANT");
-            return e ? atoi(e) : 34;  // BVH4: 2 x 4 x 4 probe tiles, one direction per warp
+            return e ? atoi(e) : -1;
         }();
+        // default (BVH4): one direction per warp over the deepest probe tile the
+        // slab holds -- 2x2x8 (C4 trace + blend 6.18 ms), 2x4x4 (6.39), 4x4x2 --
+        // with leaves tested one triangle at a time (LEAFV 0 beats pairs once the
+        // warp's rays are coherent)
+        const int64_t plane = int64_t(p.nx) * p.ny;
+        const int64_t depth = (p.probe_end - 1) / plane - p.probe_begin / plane + 1;
+        const int variant = forced >= 0 ? forced : depth >= 8 ? 46 : depth >= 4 ? 44 : 50;
         const int keep = p.reserve_sms > 0 && p.reserve_sms < sms / 2 ? p.reserve_sms : 0;
         launch_trace(p, variant, sms - keep, s, keep > 0);
     }
