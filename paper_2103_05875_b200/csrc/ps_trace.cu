@@ -165,12 +165,22 @@ __global__ void __launch_bounds__(256) shadow_map_kernel(ps_trace_params prm) {
                               ? prm.shadow_texel_end : all;
     const float4 *nodes = reinterpret_cast<const float4 *>(prm.nodes);
     const float4 *tris = reinterpret_cast<const float4 *>(prm.tris);
-    for (int64_t idx = prm.shadow_texel_begin + blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-         idx < total; idx += int64_t(gridDim.x) * blockDim.x) {
-        const int l = int(idx / per_light);
-        const int rem = int(idx - int64_t(l) * per_light);
+    // a warp traces an 8 x 4 texel block of one face (a compact cone of
+    // directions from the light) when the whole map is traced and S allows it;
+    // otherwise consecutive texels of a row
+    const bool blocked = prm.shadow_texel_begin == 0 && total == all && S % 8 == 0;
+    for (int64_t wi = prm.shadow_texel_begin + blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+         wi < total; wi += int64_t(gridDim.x) * blockDim.x) {
+        const int l = int(wi / per_light);
+        const int rem = int(wi - int64_t(l) * per_light);
         const int f = rem / (S * S);
-        const int j = (rem / S) % S, i = rem % S;
+        int j = (rem / S) % S, i = rem % S;
+        if (blocked) {
+            const int r2 = rem - f * S * S, blk = r2 >> 5, ln = r2 & 31;
+            i = (blk % (S / 8)) * 8 + (ln & 7);
+            j = (blk / (S / 8)) * 4 + (ln >> 3);
+        }
+        const int64_t idx = int64_t(l) * per_light + int64_t(f) * S * S + int64_t(j) * S + i;
         const int a = f >> 1;
         const float sgn = (f & 1) ? -1.0f : 1.0f;
         const float u = (float(i) + 0.5f) / float(S) * 2.0f - 1.0f;
