@@ -89,17 +89,31 @@ __device__ __forceinline__ void cswap(float &da, int &ca, float &db, int &cb) {
     ca = tc;
 }
 
+// 32-byte read-only load (sm_100 LDG.256): a 128-byte BVH4 node is four of
+// them instead of seven 16-byte loads; with coherent warps (one ray direction
+// over a probe tile) the lanes share node lines, so fewer load instructions
+// per node are fewer L1 wavefronts
+__device__ __forceinline__ void ldg256(const void *p, float (&v)[8]) {
+    asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]),
+          "=f"(v[7])
+        : "l"(p));
+}
+
 __device__ __forceinline__ void node4_hits(const float4 *nodes, int node, float ix, float iy,
                                            float iz, float oix, float oiy, float oiz, float tmax,
                                            float d[4], int c[4]) {
     const float4 *nd = nodes + 8 * node;
-    const float4 lx = __ldg(nd + 0), hx = __ldg(nd + 1), ly = __ldg(nd + 2), hy = __ldg(nd + 3);
-    const float4 lz = __ldg(nd + 4), hz = __ldg(nd + 5);
-    const int4 ch = __ldg(reinterpret_cast<const int4 *>(nd + 6));
-    const float lxa[4] = {lx.x, lx.y, lx.z, lx.w}, hxa[4] = {hx.x, hx.y, hx.z, hx.w};
-    const float lya[4] = {ly.x, ly.y, ly.z, ly.w}, hya[4] = {hy.x, hy.y, hy.z, hy.w};
-    const float lza[4] = {lz.x, lz.y, lz.z, lz.w}, hza[4] = {hz.x, hz.y, hz.z, hz.w};
-    const int ca[4] = {ch.x, ch.y, ch.z, ch.w};
+    float x[8], y[8], z[8], w[8];
+    ldg256(nd + 0, x);
+    ldg256(nd + 2, y);
+    ldg256(nd + 4, z);
+    ldg256(nd + 6, w);
+    const float lxa[4] = {x[0], x[1], x[2], x[3]}, hxa[4] = {x[4], x[5], x[6], x[7]};
+    const float lya[4] = {y[0], y[1], y[2], y[3]}, hya[4] = {y[4], y[5], y[6], y[7]};
+    const float lza[4] = {z[0], z[1], z[2], z[3]}, hza[4] = {z[4], z[5], z[6], z[7]};
+    const int ca[4] = {__float_as_int(w[0]), __float_as_int(w[1]), __float_as_int(w[2]),
+                       __float_as_int(w[3])};
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const float ax = fmaf(lxa[k], ix, -oix), bx = fmaf(hxa[k], ix, -oix);
