@@ -68,7 +68,7 @@ class Scene:
         m[:, 8:11] = self.face_normals()
         return m
 
-    def device(self, device=None, leaf_size: int = 4, width: int | None = None) -> "DeviceScene":
+    def device(self, device=None, leaf_size: int = 2, width: int | None = None) -> "DeviceScene":
         """BVH layouts: 2 = BVH2, 4 = BVH4 (fp32 boxes), 5 = BVH4 with fp16
         boxes (64-byte nodes); default from PS_BVH_WIDTH or BVH4."""
         import os
@@ -84,7 +84,7 @@ DEFAULT_BVH_WIDTH = 4
 class DeviceScene:
     """BVH + triangles + materials + lights resident in HBM (replicated per GPU)."""
 
-    def __init__(self, scene: Scene, device=None, leaf_size: int = 4, width: int = DEFAULT_BVH_WIDTH):
+    def __init__(self, scene: Scene, device=None, leaf_size: int = 2, width: int = DEFAULT_BVH_WIDTH):
         import torch
 
         from . import _device as D

@@ -16,7 +16,7 @@ def main():
     ap.add_argument("--config", default="c4")
     ap.add_argument("--frames", type=int, default=10)
     ap.add_argument("--shadows", default="map")
-    ap.add_argument("--leaf-size", type=int, default=4)
+    ap.add_argument("--leaf-size", type=int, default=2)
     ap.add_argument("--width", type=int, default=4)
     args = ap.parse_args()
     import torch

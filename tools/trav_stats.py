@@ -12,7 +12,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c4")
-    ap.add_argument("--leaf-size", type=int, default=4)
+    ap.add_argument("--leaf-size", type=int, default=2)
     ap.add_argument("--width", type=int, default=4)
     args = ap.parse_args()
     import torch
