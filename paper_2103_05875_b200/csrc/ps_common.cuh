@@ -70,6 +70,36 @@ struct Carver {
     }
 };
 
+
+#ifdef __CUDACC__
+// One warp moves probe block (y0, x0) -- SIDE x SIDE words of a rendered
+// atlas, row stride src_w -- handing each interior (core) word to `core(r, c,
+// v)` and, if last_sent is set, committing the whole block there.  Every load
+// of the block is issued before the first store (the source is read-only for
+// the kernel), so a warp keeps SIDE^2 / 32 loads in flight instead of one.
+template <int SIDE, class CoreStore>
+__device__ __forceinline__ void warp_copy_block(const uint32_t *__restrict__ src, int64_t src_w,
+                                                int64_t y0, int64_t x0, int lane,
+                                                uint32_t *last_sent, CoreStore core) {
+    constexpr int WORDS = SIDE * SIDE, CORE = SIDE - 2, N = (WORDS + 31) / 32;
+    uint32_t v[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+        const int k = lane + 32 * j;
+        if (k < WORDS) v[j] = __ldg(src + (y0 + k / SIDE) * src_w + x0 + k % SIDE);
+    }
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+        const int k = lane + 32 * j;
+        if (k < WORDS) {
+            const int r = k / SIDE, c = k % SIDE;
+            if (r >= 1 && r <= CORE && c >= 1 && c <= CORE) core(r - 1, c - 1, v[j]);
+            if (last_sent) last_sent[(y0 + r) * src_w + x0 + c] = v[j];
+        }
+    }
+}
+#endif
+
 }  // namespace ps
 
 #define PS_ABI_BEGIN try {

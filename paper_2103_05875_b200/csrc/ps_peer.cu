@@ -34,7 +34,6 @@ __global__ void __launch_bounds__(256)
                        int64_t slots_per_row, uint32_t *dst, int64_t dst_w, uint32_t *last_sent,
                        int64_t *last_sent_seq, int64_t current_seq, const int64_t *seq_dev) {
     constexpr int CORE = SIDE - 2;
-    constexpr int WORDS = SIDE * SIDE;
     const int64_t count = *entry_count;
     if (seq_dev) current_seq = *seq_dev;
     const int lane = threadIdx.x & 31;
@@ -46,14 +45,9 @@ __global__ void __launch_bounds__(256)
         if (p < probe_begin || p >= probe_end) continue;
         const int64_t y0 = (p / ppr) * SIDE, x0 = (p % ppr) * SIDE;
         const int64_t sy = (slot / slots_per_row) * CORE, sx = (slot % slots_per_row) * CORE;
-#pragma unroll 4
-        for (int k = lane; k < WORDS; k += 32) {
-            const int r = k / SIDE, c = k % SIDE;
-            const uint32_t v = src[(y0 + r) * src_w + x0 + c];
-            if (r >= 1 && r <= CORE && c >= 1 && c <= CORE)
-                dst[(sy + r - 1) * dst_w + sx + c - 1] = v;  // encoder's atlas, maybe remote
-            if (last_sent) last_sent[(y0 + r) * src_w + x0 + c] = v;
-        }
+        warp_copy_block<SIDE>(src, src_w, y0, x0, lane, last_sent, [&](int r, int c, uint32_t v) {
+            dst[(sy + r) * dst_w + sx + c] = v;  // encoder's atlas, maybe remote
+        });
     }
 }
 
