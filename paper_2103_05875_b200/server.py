@@ -37,6 +37,11 @@ DEFAULT_GOP = 30  # codec.py:46
 # Measured at C4 (ms/frame, reserve 2 / 4 / 8): N=1 8.31 / 8.26 / 8.38,
 # N=2 - / 4.79 / 4.88, N=4 - / 2.73 / 2.77
 RESERVE_SMS = int(__import__("os").environ.get("PS_RESERVE_SMS", "4"))
+# stream priority of the per-kind stage chains (-1 = high, 0 = as the trace)
+CHAIN_PRIORITY = int(__import__("os").environ.get("PS_CHAIN_PRIORITY", "-1"))
+# optional stream priority of the trace + blend path (unset: the caller's stream)
+_mp = __import__("os").environ.get("PS_MAIN_PRIORITY")
+MAIN_PRIORITY = int(_mp) if _mp not in (None, "") else None
 
 
 @dataclass
@@ -230,8 +235,10 @@ class ProbeStreamServer:
                                     device=self.device, atlas_buffers=2 if overlap else 1,
                                     reserve_sms=probe_kwargs.pop("reserve_sms", RESERVE_SMS) if overlap else 0,
                                     **probe_kwargs)
-        self.streams = ({"color": torch.cuda.Stream(self.device, priority=-1),
-                         "visibility": torch.cuda.Stream(self.device, priority=-1)} if overlap else None)
+        self.streams = ({"color": torch.cuda.Stream(self.device, priority=CHAIN_PRIORITY),
+                         "visibility": torch.cuda.Stream(self.device, priority=CHAIN_PRIORITY)} if overlap else None)
+        self.trace_stream = (torch.cuda.Stream(self.device, priority=MAIN_PRIORITY)
+                             if overlap and MAIN_PRIORITY is not None else None)
         self._buf_done = [[], []]   # events: stages finished reading atlas buffer k
         self._pending = []          # events of the last frame's stage chains
         ppr = self.updater.color.probes_per_row
@@ -265,8 +272,12 @@ class ProbeStreamServer:
         With ``overlap`` the outputs are produced on ``self.streams[kind]``;
         call ``join()`` (or wait on those streams) before reading them."""
         frame = self.seq if frame is None else frame
-        main = torch.cuda.current_stream(self.device)
+        caller = torch.cuda.current_stream(self.device)
         timing = self.timers is not None
+        main = caller
+        if self.trace_stream is not None and not timing:
+            main = self.trace_stream
+            main.wait_stream(caller)
         if self.overlap:
             buf = self.updater.frames_done % 2
             for ev in self._buf_done[buf]:  # trace may overwrite that atlas half now
@@ -275,7 +286,10 @@ class ProbeStreamServer:
             e = torch.cuda.Event(enable_timing=True)
             e.record()
             self.timers.setdefault("trace_blend", []).append((0, e))
-        color, vis = self.updater.update(frame, lights)
+        with torch.cuda.stream(main):
+            color, vis = self.updater.update(frame, lights)
+        if main is not caller:
+            caller.wait_stream(main)
         if timing:
             e = torch.cuda.Event(enable_timing=True)
             e.record()
