@@ -306,7 +306,7 @@ def run_ours(args, rank, world, local):
             "sm_frac": profile_metric("trace_kernel", "sm_pct"),
             "note": "BVH traversal on SIMT cores has no dense roofline: bound by L1 "
                     "data-pipe wavefronts of divergent node fetches (fractions from "
-                    "profiles/ncu_summary.json); 10.7 inner nodes, 1.1 leaves, 2.4 "
+                    "profiles/ncu_summary.json); 10.7 inner nodes, 1.07 leaves, 2.1 "
                     "triangle tests per ray (tools/trav_stats.py)",
         },
         "roofline_blend": {

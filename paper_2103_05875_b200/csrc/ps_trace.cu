@@ -773,6 +773,12 @@ void launch_trace_s(const ps_trace_params &p, int variant, int sms, cudaStream_t
             case 48: launch_trace_t<SHADOW, 2, 1, 12, 4>(p, sms, s, big); break;  // 2x2x8, 4-wide leaf
             case 49: launch_trace_t<SHADOW, 2, 1, 4, 4>(p, sms, s, big); break;   // 2x4x4, 4-wide leaf
             case 50: launch_trace_t<SHADOW, 0, 1, 2, 4>(p, sms, s, big); break;   // 4x4x2, seq leaf
+            // octant-specialised node tests: per node (6) / per ray (7)
+            case 56: launch_trace_t<SHADOW, 0, 1, 12, 6>(p, sms, s, big); break;  // 2x2x8
+            case 57: launch_trace_t<SHADOW, 0, 1, 12, 7>(p, sms, s, big); break;
+            case 58: launch_trace_t<SHADOW, 0, 1, 4, 6>(p, sms, s, big); break;   // 2x4x4
+            case 59: launch_trace_t<SHADOW, 0, 1, 4, 7>(p, sms, s, big); break;
+            case 60: launch_trace_t<SHADOW, 0, 1, 2, 6>(p, sms, s, big); break;   // 4x4x2
             case 90: {  // traversal statistics (tuning only)
                 const int per_sm = resident_blocks(trace_kernel<SHADOW, 1, 1, 0, 4, THREADS, 1>, THREADS, 0);
                 trace_kernel<SHADOW, 1, 1, 0, 4, THREADS, 1><<<sms * per_sm, THREADS, 0, s>>>(p);
@@ -882,7 +888,7 @@ int ps_trace_blend(const ps_trace_params *params, void *stream) {
         if (p.bvh_width == 5)
             shadow_map_kernel<5><<<blocks, 256, 0, s>>>(p);
         else if (p.bvh_width == 4)
-            shadow_map_kernel<4><<<blocks, 256, 0, s>>>(p);
+            shadow_map_kernel<6><<<blocks, 256, 0, s>>>(p);  // octant-specialised BVH4 tests
         else
             shadow_map_kernel<2><<<blocks, 256, 0, s>>>(p);
         check_launch("shadow_map_kernel");
@@ -900,10 +906,12 @@ int ps_trace_blend(const ps_trace_params *params, void *stream) {
         // default (BVH4): one direction per warp over the deepest probe tile the
         // slab holds -- 2x2x8 (C4 trace + blend 6.18 ms), 2x4x4 (6.39), 4x4x2 --
         // with leaves tested one triangle at a time (LEAFV 0 beats pairs once the
-        // warp's rays are coherent)
+        // warp's rays are coherent) and octant-specialised node tests picked per
+        // node (trace 5.39 -> 5.32 ms; one traversal per octant, 57, thrashes
+        // the instruction cache: 7.58 ms)
         const int64_t plane = int64_t(p.nx) * p.ny;
         const int64_t depth = (p.probe_end - 1) / plane - p.probe_begin / plane + 1;
-        const int variant = forced >= 0 ? forced : depth >= 8 ? 46 : depth >= 4 ? 44 : 50;
+        const int variant = forced >= 0 ? forced : depth >= 8 ? 56 : depth >= 4 ? 58 : 60;
         const int keep = p.reserve_sms > 0 && p.reserve_sms < sms / 2 ? p.reserve_sms : 0;
         launch_trace(p, variant, sms - keep, s, keep > 0);
     }

@@ -177,6 +177,45 @@ __device__ __forceinline__ void node4h_hits(const float4 *nodes, int node, float
 }
 
 // traversal statistics of the STATS variant (tuning only): inner-node visits,
+// BVH4 node test for a ray octant known at compile time (OCT bit a set = the
+// direction's axis-a component is negative): the entry / exit planes of each
+// slab are picked by the octant instead of a min / max pair per axis, so a
+// child costs 6 FFMA + 4 min/max instead of 6 FFMA + 10 min/max.  For l <= h
+// and i > 0, fma(l, i, -oi) <= fma(h, i, -oi) (fma is monotone in l), so the
+// picked planes are exactly min / max of the generic test: identical results.
+template <int OCT>
+__device__ __forceinline__ void node4o_hits(const float4 *nodes, int node, float ix, float iy,
+                                            float iz, float oix, float oiy, float oiz,
+                                            float tmax, float d[4], int c[4]) {
+    constexpr bool NX = OCT & 1, NY = OCT & 2, NZ = OCT & 4;
+    const float4 *nd = nodes + 8 * node;
+    float x[8], y[8], z[8], w[8];
+    ldg256(nd + 0, x);
+    ldg256(nd + 2, y);
+    ldg256(nd + 4, z);
+    ldg256(nd + 6, w);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const float nx = fmaf(x[NX ? 4 + k : k], ix, -oix), fx = fmaf(x[NX ? k : 4 + k], ix, -oix);
+        const float ny = fmaf(y[NY ? 4 + k : k], iy, -oiy), fy = fmaf(y[NY ? k : 4 + k], iy, -oiy);
+        const float nz = fmaf(z[NZ ? 4 + k : k], iz, -oiz), fz = fmaf(z[NZ ? k : 4 + k], iz, -oiz);
+        const float tn = fmaxf(fmaxf(nx, ny), fmaxf(nz, 0.0f));
+        const float tf = fminf(fminf(fx, fy), fminf(fz, tmax));
+        const int ck = __float_as_int(w[k]);
+        const bool hit = tn <= tf && ck != EMPTY_CHILD;
+        d[k] = hit ? tn : INFINITY;
+        c[k] = ck;
+    }
+    cswap(d[0], c[0], d[1], c[1]);
+    cswap(d[2], c[2], d[3], c[3]);
+    cswap(d[0], c[0], d[2], c[2]);
+    cswap(d[1], c[1], d[3], c[3]);
+    cswap(d[1], c[1], d[2], c[2]);
+}
+
+// WIDTH 6: BVH4, octant-specialised node test chosen per node (warp-uniform
+// when the warp's rays share a direction); WIDTH 7: the whole traversal
+// instantiated per octant (WIDTH 8 + octant) and chosen once per ray
 // leaf visits, triangle tests, rays
 static __device__ unsigned long long g_trav_stats[4];
 
@@ -188,6 +227,19 @@ __device__ int traverse(const float4 *__restrict__ nodes, const float4 *__restri
     const float sx = fabsf(r.dx) < 1e-12f ? copysignf(1e-12f, r.dx) : r.dx;
     const float sy = fabsf(r.dy) < 1e-12f ? copysignf(1e-12f, r.dy) : r.dy;
     const float sz = fabsf(r.dz) < 1e-12f ? copysignf(1e-12f, r.dz) : r.dz;
+    const int oct = (sx < 0.0f ? 1 : 0) | (sy < 0.0f ? 2 : 0) | (sz < 0.0f ? 4 : 0);
+    if constexpr (WIDTH == 7) {
+        switch (oct) {
+            case 0: return traverse<ANY_HIT, LEAFV, 8, STATS>(nodes, tris, r, tmax, t_best);
+            case 1: return traverse<ANY_HIT, LEAFV, 9, STATS>(nodes, tris, r, tmax, t_best);
+            case 2: return traverse<ANY_HIT, LEAFV, 10, STATS>(nodes, tris, r, tmax, t_best);
+            case 3: return traverse<ANY_HIT, LEAFV, 11, STATS>(nodes, tris, r, tmax, t_best);
+            case 4: return traverse<ANY_HIT, LEAFV, 12, STATS>(nodes, tris, r, tmax, t_best);
+            case 5: return traverse<ANY_HIT, LEAFV, 13, STATS>(nodes, tris, r, tmax, t_best);
+            case 6: return traverse<ANY_HIT, LEAFV, 14, STATS>(nodes, tris, r, tmax, t_best);
+            default: return traverse<ANY_HIT, LEAFV, 15, STATS>(nodes, tris, r, tmax, t_best);
+        }
+    }
     const float ix = 1.0f / sx, iy = 1.0f / sy, iz = 1.0f / sz;
     const float oix = r.ox * ix, oiy = r.oy * iy, oiz = r.oz * iz;
     int2 stack[STACK];
@@ -203,13 +255,25 @@ __device__ int traverse(const float4 *__restrict__ nodes, const float4 *__restri
                 st_tris += (~node) & 7;
             }
         }
-        if (node >= 0 && (WIDTH == 4 || WIDTH == 5)) {
+        if (node >= 0 && (WIDTH == 4 || WIDTH == 5 || WIDTH == 6 || WIDTH >= 8)) {
             float d[4];
             int c[4];
-            if (WIDTH == 5)
+            if constexpr (WIDTH == 5) {
                 node4h_hits(nodes, node, ix, iy, iz, oix, oiy, oiz, t_best, d, c);
-            else
+            } else if constexpr (WIDTH >= 8) {
+                node4o_hits<(WIDTH - 8) & 7>(nodes, node, ix, iy, iz, oix, oiy, oiz, t_best, d, c);
+            } else if constexpr (WIDTH == 6) {
+#define PS_OCT_CASE(o) \
+    case o: node4o_hits<o>(nodes, node, ix, iy, iz, oix, oiy, oiz, t_best, d, c); break;
+                switch (oct) {
+                    PS_OCT_CASE(0) PS_OCT_CASE(1) PS_OCT_CASE(2) PS_OCT_CASE(3)
+                    PS_OCT_CASE(4) PS_OCT_CASE(5) PS_OCT_CASE(6)
+                    default: node4o_hits<7>(nodes, node, ix, iy, iz, oix, oiy, oiz, t_best, d, c);
+                }
+#undef PS_OCT_CASE
+            } else {
                 node4_hits(nodes, node, ix, iy, iz, oix, oiy, oiz, t_best, d, c);
+            }
             if (d[0] != INFINITY) {
                 if (d[3] != INFINITY) stack[sp++] = make_int2(c[3], __float_as_int(d[3]));
                 if (d[2] != INFINITY) stack[sp++] = make_int2(c[2], __float_as_int(d[2]));

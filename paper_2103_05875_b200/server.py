@@ -39,9 +39,6 @@ DEFAULT_GOP = 30  # codec.py:46
 RESERVE_SMS = int(__import__("os").environ.get("PS_RESERVE_SMS", "4"))
 # stream priority of the per-kind stage chains (-1 = high, 0 = as the trace)
 CHAIN_PRIORITY = int(__import__("os").environ.get("PS_CHAIN_PRIORITY", "-1"))
-# optional stream priority of the trace + blend path (unset: the caller's stream)
-_mp = __import__("os").environ.get("PS_MAIN_PRIORITY")
-MAIN_PRIORITY = int(_mp) if _mp not in (None, "") else None
 
 
 @dataclass
@@ -237,8 +234,6 @@ class ProbeStreamServer:
                                     **probe_kwargs)
         self.streams = ({"color": torch.cuda.Stream(self.device, priority=CHAIN_PRIORITY),
                          "visibility": torch.cuda.Stream(self.device, priority=CHAIN_PRIORITY)} if overlap else None)
-        self.trace_stream = (torch.cuda.Stream(self.device, priority=MAIN_PRIORITY)
-                             if overlap and MAIN_PRIORITY is not None else None)
         self._buf_done = [[], []]   # events: stages finished reading atlas buffer k
         self._pending = []          # events of the last frame's stage chains
         ppr = self.updater.color.probes_per_row
@@ -272,12 +267,8 @@ class ProbeStreamServer:
         With ``overlap`` the outputs are produced on ``self.streams[kind]``;
         call ``join()`` (or wait on those streams) before reading them."""
         frame = self.seq if frame is None else frame
-        caller = torch.cuda.current_stream(self.device)
+        main = torch.cuda.current_stream(self.device)
         timing = self.timers is not None
-        main = caller
-        if self.trace_stream is not None and not timing:
-            main = self.trace_stream
-            main.wait_stream(caller)
         if self.overlap:
             buf = self.updater.frames_done % 2
             for ev in self._buf_done[buf]:  # trace may overwrite that atlas half now
@@ -286,10 +277,7 @@ class ProbeStreamServer:
             e = torch.cuda.Event(enable_timing=True)
             e.record()
             self.timers.setdefault("trace_blend", []).append((0, e))
-        with torch.cuda.stream(main):
-            color, vis = self.updater.update(frame, lights)
-        if main is not caller:
-            caller.wait_stream(main)
+        color, vis = self.updater.update(frame, lights)
         if timing:
             e = torch.cuda.Event(enable_timing=True)
             e.record()
