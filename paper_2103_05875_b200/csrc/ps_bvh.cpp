@@ -407,6 +407,12 @@ static int bvh_build_impl(const double *vertices, int64_t tri_count, int leaf_si
                         nd[4 * k + 0] = 1.f; nd[4 * k + 1] = -1.f;
                         nd[4 * k + 2] = 1.f; nd[4 * k + 3] = -1.f;
                         nd[8 + 2 * k] = 1.f; nd[8 + 2 * k + 1] = -1.f;
+                    } else {  // lo = +inf, hi = -inf: the octant test's entry plane is
+                              // +inf for either sign, so it never hits (no child check)
+                        for (int a = 0; a < 3; ++a) {
+                            nd[8 * a + k] = INFINITY;
+                            nd[8 * a + 4 + k] = -INFINITY;
+                        }
                     }
                     continue;
                 }

@@ -907,7 +907,7 @@ int ps_trace_blend(const ps_trace_params *params, void *stream) {
         // slab holds -- 2x2x8 (C4 trace + blend 6.18 ms), 2x4x4 (6.39), 4x4x2 --
         // with leaves tested one triangle at a time (LEAFV 0 beats pairs once the
         // warp's rays are coherent) and octant-specialised node tests picked per
-        // node (trace 5.39 -> 5.32 ms; one traversal per octant, 57, thrashes
+        // node (trace 5.39 -> 5.27 ms; one traversal per octant, 57, thrashes
         // the instruction cache: 7.58 ms)
         const int64_t plane = int64_t(p.nx) * p.ny;
         const int64_t depth = (p.probe_end - 1) / plane - p.probe_begin / plane + 1;

@@ -201,10 +201,9 @@ __device__ __forceinline__ void node4o_hits(const float4 *nodes, int node, float
         const float nz = fmaf(z[NZ ? 4 + k : k], iz, -oiz), fz = fmaf(z[NZ ? k : 4 + k], iz, -oiz);
         const float tn = fmaxf(fmaxf(nx, ny), fmaxf(nz, 0.0f));
         const float tf = fminf(fminf(fx, fy), fminf(fz, tmax));
-        const int ck = __float_as_int(w[k]);
-        const bool hit = tn <= tf && ck != EMPTY_CHILD;
-        d[k] = hit ? tn : INFINITY;
-        c[k] = ck;
+        // unused slots hold lo = +inf, hi = -inf: tn = +inf, never a hit
+        d[k] = tn <= tf ? tn : INFINITY;
+        c[k] = __float_as_int(w[k]);
     }
     cswap(d[0], c[0], d[1], c[1]);
     cswap(d[2], c[2], d[3], c[3]);
