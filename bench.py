@@ -248,6 +248,10 @@ def run_ours(args, rank, world, local):
     # depth tiles (128 x 2P... per probe 128 texels x 2 moments x 8 rays x 2 flops)
     # and one colour tile (128 x 3 channels x 8) -- each issued twice (hi, lo)
     blend_flops = n * (rays // 8) * 2 * 2 * 8 * (2 * 128 * 2 + 128 * 3)
+    # blend HBM bytes per probe: ray records read (16 B / ray), float state
+    # read + written (64 x 3 irradiance + 256 x 2 moments, fp32), colour atlas
+    # block (10 x 10 u32) and visibility block (18 x 18 half2) written
+    blend_bytes = n * (16 * rays + 2 * 4 * (64 * 3 + 256 * 2) + 4 * 100 + 4 * 324)
     value = n / (ms_max / 1e3)
     peak, peak_kind = load_peaks()
     # roofline of the HBM-bound pack kernel (pack + temporal delta over the update atlas)
@@ -318,6 +322,13 @@ def run_ours(args, rank, world, local):
             "unit": "TFLOP/s",
             "frac": round(blend_flops / world / (passes["blend"] / 1e3) / 1e12 / 1100.0, 4),
             "flops_per_launch": blend_flops // world,
+            "hbm": {"algorithmic_bytes_per_launch": blend_bytes // world,
+                    "achieved_gbs": round(blend_bytes / world / (passes["blend"] / 1e3) / 1e9, 1),
+                    "peak": peak,
+                    "frac": round(blend_bytes / world / (passes["blend"] / 1e3) / 1e9 / peak, 4),
+                    "traffic": profile_traffic("tc::blend_tc_kernel"),
+                    "note": "HBM is the blend's binding roofline (ray records + state "
+                            "read-modify-write + atlas blocks)"},
             "note": "tf32 MMA flops issued: 2 MMAs (W*B_hi + W*B_lo) per 128-texel tile, "
                     "colour tile padded to 128 rows; peak = B200 dense tf32 (B200_PROFILING.md); "
                     "the useful fp32 work is 47 GFLOP/frame at C4",

@@ -192,6 +192,11 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
 }
 
 // TMA bulk copy global -> shared, completing `bytes` of the barrier's transaction count
+// bulk prefetch of a global range into L2 (16-byte aligned, multiple of 16 bytes)
+__device__ __forceinline__ void bulk_prefetch_l2(const void *src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,
                                          uint64_t *bar) {
     asm volatile(
@@ -357,6 +362,13 @@ __global__ void __launch_bounds__(THREADS, 2) blend_tc_kernel(ps_trace_params pr
         __syncwarp();
     } else if (warp == 5) {
         if (lane == 0) {
+            if (prm.hysteresis != 0.f) {
+                // the epilogue reads this CTA's old state: pull it into L2 while the
+                // MMAs run, so the epilogue's loads are L2 hits, not HBM round trips
+                bulk_prefetch_l2(reinterpret_cast<const float2 *>(prm.moments) + pl0 * 256,
+                                 uint32_t(nq) * 256 * 8);
+                bulk_prefetch_l2(prm.irradiance + pl0 * 64 * 3, uint32_t(nq) * 64 * 3 * 4);
+            }
 #pragma unroll 1
             for (int c = 0; c < NK; ++c) {
                 const int s = c % STAGES, u = c / STAGES;
