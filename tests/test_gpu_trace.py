@@ -187,3 +187,38 @@ def test_slab_sharding_is_consistent(pkg):
     assert torch.equal(full.irradiance[256:], b.irradiance)
     merged = a.color.texels.view(torch.int32) | b.color.texels.view(torch.int32)
     assert torch.equal(merged, full.color.texels.view(torch.int32))
+
+
+def _axis_ray_set(count=64, seed=11):
+    """Directions that stress the octant-specialised node test: the six axes
+    with signed-zero components, the eight diagonals, then random ones."""
+    z = -0.0
+    fixed = [(1, 0, 0), (-1, 0, 0), (0, 1, 0), (0, -1, 0), (0, 0, 1), (0, 0, -1),
+             (1, z, z), (z, z, -1), (z, 1, z), (-1, z, 0)]
+    fixed += [(sx, sy, sz) for sx in (1, -1) for sy in (1, -1) for sz in (1, -1)]
+    d = np.array(fixed, np.float64)
+    rng = np.random.default_rng(seed)
+    r = rng.normal(size=(count - len(d), 3))
+    d = np.concatenate([d, r])
+    n = np.linalg.norm(d, axis=1, keepdims=True)
+    d = np.where(d == 0, d, d / n)  # keeps the signed zeros
+    out = np.zeros((count, 4), np.float32)
+    out[:, :3] = d
+    return out
+
+
+@pytest.mark.parametrize("probe_range", [None, (3 * 64, 4 * 64)])
+def test_axis_aligned_and_signed_zero_rays(pkg, monkeypatch, probe_range):
+    """Axis-aligned rays (tiny reciprocal stand-ins, -0.0 components) through
+    the octant-specialised BVH4 trace -- deep slab (2x2x8 tiles) and a
+    one-plane slab (4x4x2 tiles) -- against the float64 oracle."""
+    p, probes, scene = pkg
+    monkeypatch.setattr(probes, "frame_ray_directions", lambda count, seed, frame: _axis_ray_set(count))
+    sc = scene.cornell_box()
+    vol = scene.volume_for(sc, (8, 8, 8))
+    kw = {"probe_range": probe_range} if probe_range else {}
+    upd = probes.ProbeUpdater(vol, sc, rays_per_probe=64, record_rays=True, shadows="rays", **kw)
+    upd.update(0)
+    torch.cuda.synchronize()
+    _check_trace(upd, sc, 0)
+    _check_blend(upd, None, None, 0.0)
