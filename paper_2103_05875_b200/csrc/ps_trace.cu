@@ -214,6 +214,7 @@ __global__ void __launch_bounds__(256) shadow_map_kernel(ps_trace_params prm) {
 // (6.18 ms per C4 trace + blend for a 2 x 2 x 8 tile vs 7.90 ms for 32
 // neighbouring directions of one probe and 8.70 ms for a row of 32 probes;
 // more than one direction per warp was slower).
+// TPB = 640 (two CTAs per SM, 48 registers, 40 warps) is the default launch;
 // TPB = 1024 is the "SM-sized" launch used when SMs are reserved for
 // concurrent streams: one CTA fills an SM (64 registers x 1024 threads), so a
 // grid of sms - reserve CTAs leaves whole SMs free (a grid of 256-thread CTAs
@@ -221,7 +222,8 @@ __global__ void __launch_bounds__(256) shadow_map_kernel(ps_trace_params prm) {
 // kernels).  The kernel is per-warp, so the block size is free.
 template <int SHADOW, int LEAFV, int MINB, int PROBE_PARALLEL, int WIDTH, int TPB = THREADS,
           int STATS = 0>
-__global__ void __launch_bounds__(TPB, TPB == THREADS ? MINB : 1) trace_kernel(ps_trace_params prm) {
+__global__ void __launch_bounds__(TPB, TPB == THREADS ? MINB : (TPB == 640 ? 2 : 1))
+    trace_kernel(ps_trace_params prm) {
     const float4 *nodes = reinterpret_cast<const float4 *>(prm.nodes);
     const float4 *tris = reinterpret_cast<const float4 *>(prm.tris);
     const float4 *dirs = reinterpret_cast<const float4 *>(prm.ray_dirs);
@@ -734,6 +736,13 @@ void launch_trace_t(const ps_trace_params &p, int sms, cudaStream_t s, bool sm_s
     trace_kernel<SHADOW, LEAFV, MINB, PP, WIDTH><<<sms * per_sm, THREADS, 0, s>>>(p);
 }
 
+// two 640-thread CTAs per SM (40 warps at <= 48 registers) on all but the
+// reserved SMs
+template <int SHADOW, int LEAFV, int PP, int WIDTH>
+void launch_trace_640(const ps_trace_params &p, int sms, cudaStream_t s) {
+    trace_kernel<SHADOW, LEAFV, 1, PP, WIDTH, 640><<<2 * sms, 640, 0, s>>>(p);
+}
+
 template <int SHADOW, int MINB>
 void launch_trace_ww(const ps_trace_params &p, int sms, cudaStream_t s) {
     const int per_sm = resident_blocks(trace_ww_kernel<SHADOW, MINB>, THREADS, 0);
@@ -779,6 +788,11 @@ void launch_trace_s(const ps_trace_params &p, int variant, int sms, cudaStream_t
             case 58: launch_trace_t<SHADOW, 0, 1, 4, 6>(p, sms, s, big); break;   // 2x4x4
             case 59: launch_trace_t<SHADOW, 0, 1, 4, 7>(p, sms, s, big); break;
             case 60: launch_trace_t<SHADOW, 0, 1, 2, 6>(p, sms, s, big); break;   // 4x4x2
+            case 61: launch_trace_t<SHADOW, 0, 5, 12, 6>(p, sms, s, false); break;  // 40 warps/SM
+            case 62: launch_trace_t<SHADOW, 0, 6, 12, 6>(p, sms, s, false); break;  // 48 warps/SM
+            case 63: launch_trace_640<SHADOW, 0, 12, 6>(p, sms, s); break;  // 2 x 640 per SM
+            case 64: launch_trace_640<SHADOW, 0, 4, 6>(p, sms, s); break;
+            case 65: launch_trace_640<SHADOW, 0, 2, 6>(p, sms, s); break;
             case 90: {  // traversal statistics (tuning only)
                 const int per_sm = resident_blocks(trace_kernel<SHADOW, 1, 1, 0, 4, THREADS, 1>, THREADS, 0);
                 trace_kernel<SHADOW, 1, 1, 0, 4, THREADS, 1><<<sms * per_sm, THREADS, 0, s>>>(p);
@@ -908,10 +922,11 @@ int ps_trace_blend(const ps_trace_params *params, void *stream) {
         // with leaves tested one triangle at a time (LEAFV 0 beats pairs once the
         // warp's rays are coherent) and octant-specialised node tests picked per
         // node (trace 5.39 -> 5.27 ms; one traversal per octant, 57, thrashes
-        // the instruction cache: 7.58 ms)
+        // the instruction cache: 7.58 ms), launched as two 640-thread CTAs per
+        // SM at <= 48 registers (40 warps instead of 32: 5.27 -> 5.08 ms)
         const int64_t plane = int64_t(p.nx) * p.ny;
         const int64_t depth = (p.probe_end - 1) / plane - p.probe_begin / plane + 1;
-        const int variant = forced >= 0 ? forced : depth >= 8 ? 56 : depth >= 4 ? 58 : 60;
+        const int variant = forced >= 0 ? forced : depth >= 8 ? 63 : depth >= 4 ? 64 : 65;
         const int keep = p.reserve_sms > 0 && p.reserve_sms < sms / 2 ? p.reserve_sms : 0;
         launch_trace(p, variant, sms - keep, s, keep > 0);
     }
