@@ -290,6 +290,7 @@ def run_ours(args, rank, world, local):
         "grays_per_s": round(rays_total / (ms_max / 1e3) / 1e9, 4),
         "frame_hz": round(1e3 / ms_max, 2),
         "stages_ms": {k: round(v, 4) for k, v in stages.items()},
+        "passes_ms": {k: round(v, 4) for k, v in passes.items()},
         "packed_atlas_gbs": round(achieved, 1) if achieved else None,
         "roofline": {
             "bound": "hbm",

@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(256) shadow_map_kernel(ps_trace_params prm) {
 // kernels).  The kernel is per-warp, so the block size is free.
 template <int SHADOW, int LEAFV, int MINB, int PROBE_PARALLEL, int WIDTH, int TPB = THREADS,
           int STATS = 0>
-__global__ void __launch_bounds__(TPB, TPB == THREADS ? MINB : (TPB == 640 ? 2 : 1))
+__global__ void __launch_bounds__(TPB, TPB == THREADS ? MINB : (TPB == 1024 ? 1 : 2))
     trace_kernel(ps_trace_params prm) {
     const float4 *nodes = reinterpret_cast<const float4 *>(prm.nodes);
     const float4 *tris = reinterpret_cast<const float4 *>(prm.tris);

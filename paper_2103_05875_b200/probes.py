@@ -430,14 +430,16 @@ class ProbeUpdater:
         return self.color, self.visibility
 
     def pass_times_ms(self, reps: int = 3) -> dict:
-        """Device time of the probe-ray pass and of the blend pass alone
-        (CUDA events around ps_trace_blend with passes = 2 / 4 on the current
-        frame's inputs).  Re-running the blend advances the float state, so
-        call this only after the frames being measured."""
+        """Device time of the shadow-map pass (unsharded maps only), the
+        probe-ray pass and the blend pass alone (CUDA events around
+        ps_trace_blend with passes = 1 / 2 / 4 on the current frame's inputs).
+        Re-running the blend advances the float state, so call this only
+        after the frames being measured."""
         stream = D.stream_ptr(self.device)
         out = {}
         shadow = self.shadow_peer["maps2"][(self.frames_done - 1) & 1] if self.shadow_peer else None
-        for name, passes in (("trace", 2), ("blend", 4)):
+        runs = (("shadow_maps", 1),) if self.shadows == "map" and not self.shadow_peer else ()
+        for name, passes in runs + (("trace", 2), ("blend", 4)):
             params = self._params(self.hysteresis, passes=passes, shadow_maps=shadow)
             N.call("ps_trace_blend", ctypes.byref(params), stream)  # warm
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
