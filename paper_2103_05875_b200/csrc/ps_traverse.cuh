@@ -31,7 +31,10 @@ __device__ __forceinline__ float tri_hit(const Ray &r, float4 v0, float4 e1, flo
     const float pz = r.dx * e2.y - r.dy * e2.x;
     const float det = dot3(e1.x, e1.y, e1.z, px, py, pz);
     if (!(fabsf(det) > RAY_EPS)) return INFINITY;
-    const float inv = 1.0f / det;
+    // MUFU.RCP alone (<= 1 ulp): |det| > 1e-6 keeps it far from the range
+    // where the IEEE division's slow path matters, so the rn fix-up and its
+    // slow-path branch are dropped from every triangle test
+    const float inv = __fdividef(1.0f, det);
     const float tx = r.ox - v0.x, ty = r.oy - v0.y, tz = r.oz - v0.z;
     const float u = dot3(tx, ty, tz, px, py, pz) * inv;
     const float qx = ty * e1.z - tz * e1.y;
