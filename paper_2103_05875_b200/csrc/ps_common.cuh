@@ -82,11 +82,15 @@ __device__ __forceinline__ void warp_copy_block(const uint32_t *__restrict__ src
                                                 int64_t y0, int64_t x0, int lane,
                                                 uint32_t *last_sent, CoreStore core) {
     constexpr int WORDS = SIDE * SIDE, CORE = SIDE - 2, N = (WORDS + 31) / 32;
+    // one 64-bit block base, 32-bit offsets inside the block (a block spans
+    // SIDE rows, far below 2^31 words): fewer live 64-bit addresses
+    const int w32 = int(src_w);
+    const uint32_t *__restrict__ sb = src + y0 * src_w + x0;
     uint32_t v[N];
 #pragma unroll
     for (int j = 0; j < N; ++j) {
         const int k = lane + 32 * j;
-        if (k < WORDS) v[j] = __ldg(src + (y0 + k / SIDE) * src_w + x0 + k % SIDE);
+        if (k < WORDS) v[j] = __ldg(sb + (k / SIDE) * w32 + k % SIDE);
     }
 #pragma unroll
     for (int j = 0; j < N; ++j) {
@@ -94,7 +98,7 @@ __device__ __forceinline__ void warp_copy_block(const uint32_t *__restrict__ src
         if (k < WORDS) {
             const int r = k / SIDE, c = k % SIDE;
             if (r >= 1 && r <= CORE && c >= 1 && c <= CORE) core(r - 1, c - 1, v[j]);
-            if (last_sent) last_sent[(y0 + r) * src_w + x0 + c] = v[j];
+            if (last_sent) last_sent[(y0 * src_w + x0) + (r * w32 + c)] = v[j];
         }
     }
 }

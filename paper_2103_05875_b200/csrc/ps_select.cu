@@ -196,8 +196,11 @@ __global__ void entry_bits_kernel(const int32_t *slot_probe, const uint32_t *sel
 
 // --- build + commit --------------------------------------------------------------
 
+// visibility (SIDE 18) at <= 80 registers: 24 warps per SM keep more block
+// loads in flight than 16 at 102 registers (0.157 -> 0.127 ms at C4);
+// colour keeps its 64
 template <int SIDE>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, SIDE == 18 ? 3 : 4)
     build_kernel(const uint32_t *src, int64_t src_w, int64_t ppr, const int64_t *entries,
                  const int64_t *entry_count, int64_t slots_per_row, uint32_t *dst,
                  int64_t dst_w, uint32_t *last_sent, int64_t *last_sent_seq,
