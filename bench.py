@@ -247,7 +247,7 @@ def run_ours(args, rank, world, local):
     # tcgen05 blend flops issued per frame: per probe and k-step of 8 rays, two
     # depth tiles (128 x 2P... per probe 128 texels x 2 moments x 8 rays x 2 flops)
     # and one colour tile (128 x 3 channels x 8) -- each issued twice (hi, lo)
-    blend_flops = n * (rays // 8) * 2 * 2 * 8 * (2 * 128 * 2 + 128 * 3)
+    blend_flops = n * (rays // 8) * 2 * 8 * (3 * 2 * 128 * 2 + 2 * 128 * 3)
     # blend HBM bytes per probe: ray records read (16 B / ray), float state
     # read + written (64 x 3 irradiance + 256 x 2 moments, fp32), colour atlas
     # block (10 x 10 u32) and visibility block (18 x 18 half2) written
@@ -330,9 +330,10 @@ def run_ours(args, rank, world, local):
                     "traffic": profile_traffic("tc::blend_tc_kernel"),
                     "note": "HBM is the blend's binding roofline (ray records + state "
                             "read-modify-write + atlas blocks)"},
-            "note": "tf32 MMA flops issued: 2 MMAs (W*B_hi + W*B_lo) per 128-texel tile, "
-                    "colour tile padded to 128 rows; peak = B200 dense tf32 (B200_PROFILING.md); "
-                    "the useful fp32 work is 47 GFLOP/frame at C4",
+            "note": "tf32 MMA flops issued (3xTF32, fp32-accurate): 3 MMAs (W_hi*B_hi + "
+                    "W_hi*B_lo + W_lo*B_hi) per 128-texel depth tile, 2 for the colour tile "
+                    "(W_hi rows 0-63, W_lo rows 64-127); peak = B200 dense tf32 "
+                    "(B200_PROFILING.md); the useful fp32 work is 47 GFLOP/frame at C4",
         },
         "clocks": clocks.summary(),
         "e2e": {"value": round(n / (e2e_ms / 1e3), 1), "unit": "probe updates/s",

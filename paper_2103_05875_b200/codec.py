@@ -135,18 +135,23 @@ class _Buffers:
 
 
 def encode_frame_device(planes: torch.Tensor, reference: torch.Tensor | None, stream_id: int,
-                        frame_seq: int, out=None, frame_len=None):
+                        frame_seq: int, out=None, frame_len=None, workspace=None):
     """Encode one frame on the device; returns (frame buffer uint8, length
-    int64[1]) -- the first ``length`` bytes are the LPF1 wire frame.  Buffers
-    are cached per (shape, stream id), so concurrent streams do not share."""
+    int64[1]) -- the first ``length`` bytes are the LPF1 wire frame.  A
+    session passes its own ``out`` / ``frame_len`` / ``workspace``
+    (server.KindStream does); otherwise buffers come from a cache keyed by
+    (shape, stream id) for one-off calls on the current stream."""
     if planes.dim() != 3 or planes.shape[0] != 3:
         raise ValueError("plane data must be (3, h, w)")
     eb = planes.element_size()
     _, h, w = planes.shape
     dev = planes.device
-    o, ln, ws = _Buffers.get(h, w, eb, dev, int(stream_id))
+    if out is None or frame_len is None or workspace is None:
+        o, ln, ws = _Buffers.get(h, w, eb, dev, int(stream_id))
     out = o if out is None else out
     frame_len = ln if frame_len is None else frame_len
+    ws = ws if workspace is None else D.Workspace.get(
+        N.lib().ps_encode_workspace_bytes(h, w, eb), dev, workspace)
     ref = reference.contiguous() if reference is not None else None
     N.call("ps_encode_frame", eb, planes.contiguous().data_ptr(), D.ptr(ref), h, w,
            int(stream_id) & 0xFFFFFFFF, int(frame_seq) & 0xFFFFFFFF, out.data_ptr(), out.numel(),

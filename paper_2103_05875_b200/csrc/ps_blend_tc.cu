@@ -3,34 +3,39 @@
 //
 // Per frame every probe blends its R rays into 64 colour texels and 256 depth
 // texels with weights that are shared by all probes (cosine / cosine^s of the
-// texel and ray directions).  For a CTA of P = 64 probes that is
+// texel and ray directions).  For a CTA of P = 32 probes that is
 //
 //   D_depth[t, n] = sum_r Wd[r, t] * Bd[r, n]     t < 256, n = (d | d^2, probe)
 //   D_col  [t, n] = sum_r Wc[r, t] * Bc[r, n]     t < 64,  n = (r | g | b, probe)
 //
-// i.e. M = texels (two M=128 tiles for depth, one zero-padded M=128 tile for
-// colour), N = 64 / 96 probe channels, K = rays in steps of 8.  TMEM holds
-// all three accumulators (64 + 64 + 96 = 224 of a 256-column allocation), so
-// two CTAs share an SM and one's epilogue overlaps the other's MMAs.
+// i.e. M = texels (two M=128 tiles for depth, one M=128 tile for colour),
+// N = 64 / 96 probe channels, K = rays in steps of 8.  TMEM holds all three
+// accumulators (64 + 64 + 96 = 224 of a 256-column allocation), so two CTAs
+// share an SM and one's epilogue overlaps the other's MMAs.
 //
-// Precision (parity bar: 1e-4 relative vs the fp32 oracle): the weights are
-// tf32 numbers by definition (the weights pass clears their low 13 mantissa
-// bits; oracle/ddgi.py does the same), and each fp32 probe channel is split
-// x = hi + lo, hi = x with its low 13 mantissa bits cleared (exact in tf32),
-// lo = x - hi (exact in fp32).  Every product is issued as W*B_hi + W*B_lo:
-// only the tf32 truncation of lo is lost (<= 2^-21 relative), so the result
-// is fp32-accurate with two MMAs per tile.
+// Precision (parity bar: 1e-4 relative / 1e-5 absolute vs the fp32 oracle,
+// BASELINE.json north_star): 3xTF32.  Weights and probe channels are plain
+// fp32; each is split x = hi + lo, hi = x with its low 13 mantissa bits
+// cleared (exact in tf32), lo = x - hi (exact in fp32), and every product is
+// issued as W_hi*B_hi + W_hi*B_lo + W_lo*B_hi.  What is lost is W_lo*B_lo and
+// the tf32 truncation of the lo terms, <= 2^-20 relative per product: the
+// sums are fp32-accurate.
+//   * depth: 3 MMAs per 128-texel tile and k-step (A = W_hi, W_hi, W_lo);
+//   * colour: the 64 live texels use rows 0-63 of the M=128 tile for W_hi and
+//     rows 64-127 for W_lo, so A_c x B_hi yields W_hi*B_hi (rows 0-63) and
+//     W_lo*B_hi (rows 64-127) in one MMA, and A_c x B_lo adds W_hi*B_lo (and
+//     W_lo*B_lo) -- 2 MMAs; the epilogue adds TMEM lanes t and t + 64.
 //
-// Warp-specialised pipeline over k-steps of 8 rays, 3 shared-memory stages
-// of 22 KB, mbarriers between the roles:
-//   * warp 5 (one thread) streams the weights (3 operand images, 12 KB per
-//     k-step) with TMA bulk copies from a per-frame image the weights pass
+// Warp-specialised pipeline over k-steps of 8 rays, STAGES shared-memory
+// stages of 30 KB, mbarriers between the roles:
+//   * warp 5 (one thread) streams the weights (5 operand images, 20 KB per
+//     k-step, one TMA bulk copy) from a per-frame image the weights pass
 //     writes in the canonical K-major no-swizzle UMMA layout;
-//   * warps 0-3 stream their ray records through a cp.async ring (7 k-steps
-//     ahead) and convert them into the B images (channels d, d^2, r, g, b),
-//     hi and lo;
-//   * warp 4 (one thread) issues 6 MMAs per k-step (3 tiles x 2 terms) and
-//     commits them to the stage's "empty" barrier.
+//   * warps 0-3 stream their ray records through a cp.async ring (RING - 1
+//     k-steps ahead) and convert them into the B images (channels d, d^2, r,
+//     g, b), hi and lo;
+//   * warp 4 (one thread) issues 8 MMAs per k-step and commits them to the
+//     stage's "empty" barrier.
 // The epilogue reads the accumulators with tcgen05.ld (one texel per TMEM
 // lane), applies the normalisation / hysteresis / quantisation of the
 // CUDA-core blend and writes the guard-banded atlas blocks.
@@ -49,22 +54,35 @@ constexpr int P = 32;         // probes per CTA (two CTAs per SM: one's epilogue
                               // the other's MMAs)
 constexpr int THREADS = 256;  // warps 0-3 convert records, 4 issues MMAs, 5 loads weights
 constexpr int PRODUCERS = 128;
-constexpr int STAGES = 3;
-constexpr int PART = 128 * 8;                 // floats of one 128-row x 8-k operand image
-constexpr int A_FLOATS = 3 * PART;            // depth tile 0, depth tile 1, colour
+#ifndef PS_BLEND_STAGES
+#define PS_BLEND_STAGES 3
+#endif
+#ifndef PS_BLEND_RING
+#define PS_BLEND_RING 5
+#endif
+constexpr int STAGES = PS_BLEND_STAGES;
+constexpr int PART = 128 * 8;  // floats of one 128-row x 8-k operand image
+// A images of a k-step: depth hi tile 0, depth hi tile 1, depth lo tile 0,
+// depth lo tile 1, colour (rows 0-63 hi, 64-127 lo)
+constexpr int A_DHI = 0, A_DLO = 2 * PART, A_COL = 4 * PART;
+constexpr int A_FLOATS = 5 * PART;
 constexpr int BD_ROWS = 2 * P;                // d (probe q) then d^2 (probe q)
 constexpr int BC_ROWS = 3 * P;                // r, g, b
 constexpr int BD = BD_ROWS * 8;               // floats of one depth B image
 constexpr int BC = BC_ROWS * 8;
-constexpr int STAGE = A_FLOATS + 2 * BD + 2 * BC;  // 5632 floats = 22 KB
-constexpr uint32_t A_LOAD_BYTES = (2 * PART + 2 * 256) * 4;  // colour rows 64-127 stay zero
+constexpr int STAGE = A_FLOATS + 2 * BD + 2 * BC;  // 7680 floats = 30 KB
+constexpr uint32_t A_LOAD_BYTES = A_FLOATS * 4;
 constexpr int RAW = P * 8 * 4;  // floats of one k-step's raw ray records (4 KB)
-constexpr int RING = 8;         // raw record ring: records stream RING - 1 k-steps ahead
+constexpr int RING = PS_BLEND_RING;  // raw record ring: records stream RING - 1 k-steps ahead
 constexpr size_t SMEM_BYTES = (size_t(STAGES) * STAGE + size_t(RING) * RAW) * 4 + 1024;
+// epilogue: quantised cores + the colour lo partials handed from TMEM lanes 64-127
+constexpr int XBUF = 2 * 3 * 64 * 16;  // [half][ch][texel][probe of the half]
 constexpr uint32_t COL_D0 = 0, COL_D1 = BD_ROWS, COL_C = 2 * BD_ROWS, TMEM_COLS = 256;
 
 static_assert(COL_C + BC_ROWS <= TMEM_COLS, "accumulators must fit the TMEM allocation");
-static_assert(P * 64 + P * 256 <= STAGES * STAGE, "epilogue staging must fit the stages");
+static_assert(P * 64 + P * 256 + XBUF <= STAGES * STAGE + RING * RAW,
+              "epilogue staging must fit the stages and the ring");
+static_assert(2 * (SMEM_BYTES + 1024) + 1024 <= 233472, "two CTAs per SM");
 
 // canonical K-major, no-swizzle operand image: 8-row x 16-byte core matrices,
 // row groups 128 B apart (SBO), the two 4-wide k halves rows*16 B apart (LBO);
@@ -159,8 +177,8 @@ __device__ __forceinline__ float tf32_hi(float x) {
     return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
 }
 
-// weights pass: the per-frame A image, (R/8) k-steps x 3 operand images of the
-// (already tf32) weights
+// weights pass: the per-frame A image, (R/8) k-steps x 5 operand images of
+// the fp32 weights split hi + lo
 __global__ void weight_image_kernel(const float *w_color, const float *w_depth, int R,
                                     float *img) {
     const int total = (R / 8) * A_FLOATS;
@@ -172,12 +190,17 @@ __global__ void weight_image_kernel(const float *w_color, const float *w_depth, 
         const int m = (in >> 5) * 8 + ((in & 31) >> 2);
         const int k = kh * 4 + (in & 3);
         const int r = s * 8 + k;
-        float w = 0.f;
-        if (part == 2)
-            w = m < 64 ? w_color[r * 64 + m] : 0.f;
-        else
-            w = w_depth[r * 256 + part * 128 + m];
-        img[i] = w;
+        bool lo;
+        float w;
+        if (part == 4) {  // colour: rows 0-63 hi, rows 64-127 lo of texel m & 63
+            w = w_color[r * 64 + (m & 63)];
+            lo = m >= 64;
+        } else {
+            w = w_depth[r * 256 + (part & 1) * 128 + m];
+            lo = part >= 2;
+        }
+        const float hi = tf32_hi(w);
+        img[i] = lo ? w - hi : hi;
     }
 }
 
@@ -266,14 +289,16 @@ __device__ __forceinline__ void issue_mma(const float *st, uint32_t tmem, int c)
     const uint64_t b_ch = smem_desc(bch, BC_ROWS), b_cl = smem_desc(bcl, BC_ROWS);
 #pragma unroll
     for (int t = 0; t < 2; ++t) {  // depth tiles (texels 0-127, 128-255)
-        const uint64_t aw = smem_desc(a + t * PART, 128);
+        const uint64_t a_hi = smem_desc(a + A_DHI + t * PART, 128);
+        const uint64_t a_lo = smem_desc(a + A_DLO + t * PART, 128);
         const uint32_t d = tmem + (t ? COL_D1 : COL_D0);
-        mma_tf32(d, aw, b_dh, ID_D, acc);
-        mma_tf32(d, aw, b_dl, ID_D, 1u);
+        mma_tf32(d, a_hi, b_dh, ID_D, acc);
+        mma_tf32(d, a_hi, b_dl, ID_D, 1u);
+        mma_tf32(d, a_lo, b_dh, ID_D, 1u);
     }
-    const uint64_t aw = smem_desc(a + 2 * PART, 128);
-    mma_tf32(tmem + COL_C, aw, b_ch, ID_C, acc);
-    mma_tf32(tmem + COL_C, aw, b_cl, ID_C, 1u);
+    const uint64_t a_c = smem_desc(a + A_COL, 128);
+    mma_tf32(tmem + COL_C, a_c, b_ch, ID_C, acc);
+    mma_tf32(tmem + COL_C, a_c, b_cl, ID_C, 1u);
 }
 
 __global__ void __launch_bounds__(THREADS, 2) blend_tc_kernel(ps_trace_params prm) {
@@ -305,13 +330,6 @@ __global__ void __launch_bounds__(THREADS, 2) blend_tc_kernel(ps_trace_params pr
                      "r"(TMEM_COLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    for (int i = tid; i < STAGES * 2 * 64; i += THREADS) {  // colour A rows 64-127: zero
-        const int st = i / 128, r = i % 128;
-        float4 *z = reinterpret_cast<float4 *>(stages + st * STAGE + 2 * PART + 256 +
-                                               (r >> 6) * 512) + (r & 63);
-        *z = make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-    fence_async_smem();
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -373,14 +391,10 @@ __global__ void __launch_bounds__(THREADS, 2) blend_tc_kernel(ps_trace_params pr
             for (int c = 0; c < NK; ++c) {
                 const int s = c % STAGES, u = c / STAGES;
                 if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
-                // depth tiles (8 KB) + the 64 live rows of each k half of the colour tile
-                // (its rows 64-127 are zero in every stage since the prologue)
-                float *dst = stages + s * STAGE;
-                const float *src = prm.w_image + size_t(c) * A_FLOATS;
+                // the k-step's five operand images are contiguous in the weight image
                 mbar_expect_tx(&a_full[s], A_LOAD_BYTES);
-                bulk_g2s(dst, src, 2 * PART * 4, &a_full[s]);
-                bulk_g2s(dst + 2 * PART, src + 2 * PART, 256 * 4, &a_full[s]);
-                bulk_g2s(dst + 2 * PART + 512, src + 2 * PART + 512, 256 * 4, &a_full[s]);
+                bulk_g2s(stages + s * STAGE, prm.w_image + size_t(c) * A_FLOATS, A_LOAD_BYTES,
+                         &a_full[s]);
             }
         }
         __syncwarp();
@@ -430,36 +444,58 @@ __global__ void __launch_bounds__(THREADS, 2) blend_tc_kernel(ps_trace_params pr
             }
         }
     }
-    if (sub < 2) {  // colour: TMEM lanes 0-63 are the 64 texels; warp half h owns P/2 probes
-        const int t = sub * 32 + lane;
-        const float inv = __ldg(prm.inv_wsum + t);
-        const uint32_t base = lane_base + COL_C;
-        const bool need_old = inv == 0.f || h != 0.f;
-        const int q0 = half * (P / 2);
-        static_assert(P / 2 == 16, "one 16-column TMEM load per channel");
-        float old[16][3];
+    // colour: TMEM lanes 0-63 hold W_hi*B (+ W_hi*B_lo) of the 64 texels, lanes
+    // 64-127 the W_lo*B_hi terms of the same texels; warp half h owns probes
+    // h*16..h*16+15.  Warps of lane quarters 2-3 hand their partials over
+    // through shared memory to the warps of quarters 0-1, which finish.
+    float *xbuf = reinterpret_cast<float *>(s_vcore + P * 256);  // [half][ch][t][i]
+    const int q0c = half * (P / 2);
+    static_assert(P / 2 == 16, "one 16-column TMEM load per channel");
+    const uint32_t cbase = lane_base + COL_C;
+    if (sub >= 2) {
+        const int t = (sub - 2) * 32 + lane;
+        float v[16];
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+            tmem_ld16(cbase + ch * P + q0c, v);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) xbuf[((half * 3 + ch) * 64 + t) * 16 + i] = v[i];
+        }
+    }
+    float old[16][3];
+    float cr[16], cg[16], cb[16];
+    const int tc_ = sub * 32 + lane;
+    const float inv_c = sub < 2 ? __ldg(prm.inv_wsum + tc_) : 0.f;
+    const bool need_old_c = inv_c == 0.f || h != 0.f;
+    if (sub < 2) {
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-            const float *st = prm.irradiance + ((pl0 + q0 + i) * 64 + t) * 3;
-            const bool ld = need_old && q0 + i < nq;
+            const float *st = prm.irradiance + ((pl0 + q0c + i) * 64 + tc_) * 3;
+            const bool ld = need_old_c && q0c + i < nq;
 #pragma unroll
             for (int ch = 0; ch < 3; ++ch) old[i][ch] = ld ? __ldcs(st + ch) : 0.f;
         }
-        float cr[16], cg[16], cb[16];
-        tmem_ld16(base + q0, cr);
-        tmem_ld16(base + P + q0, cg);
-        tmem_ld16(base + 2 * P + q0, cb);
+        tmem_ld16(cbase + q0c, cr);
+        tmem_ld16(cbase + P + q0c, cg);
+        tmem_ld16(cbase + 2 * P + q0c, cb);
+    }
+    __syncthreads();  // the lo partials are in xbuf
+    if (sub < 2) {
+        const int t = tc_;
+        const float *xr = xbuf + ((half * 3 + 0) * 64 + t) * 16;
+        const float *xg = xbuf + ((half * 3 + 1) * 64 + t) * 16;
+        const float *xb = xbuf + ((half * 3 + 2) * 64 + t) * 16;
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-            const int qq = q0 + i;
+            const int qq = q0c + i;
             if (qq >= nq) break;
             float *st = prm.irradiance + ((pl0 + qq) * 64 + t) * 3;
-            const float acc[3] = {cr[i], cg[i], cb[i]};
+            const float acc[3] = {cr[i] + xr[i], cg[i] + xg[i], cb[i] + xb[i]};
             uint32_t texel = 0;
 #pragma unroll
             for (int ch = 0; ch < 3; ++ch) {
-                float v = acc[ch] * inv;
-                if (inv == 0.f) v = old[i][ch];  // no ray sees this texel: keep the state
+                float v = acc[ch] * inv_c;
+                if (inv_c == 0.f) v = old[i][ch];  // no ray sees this texel: keep the state
                 else if (h != 0.f) v = fmaf(h, old[i][ch] - v, v);
                 __stcs(st + ch, v);
                 const float x = fminf(fmaxf(v * qs, 0.0f), 1.0f);

@@ -679,12 +679,8 @@ __global__ void __launch_bounds__(THREADS, 2) blend_kernel(ps_trace_params prm) 
     }
 }
 
-// per-frame blend weights: w_color[r][t] = max(0, n_t . d_r),
+// per-frame blend weights (plain fp32): w_color[r][t] = max(0, n_t . d_r),
 // w_depth[r][t] = max(0, n_t . d_r)^sharpness, inv_wsum[t] = 1 / sum_r w
-__device__ __forceinline__ float tf32_trunc(float x) {
-    return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
-}
-
 __global__ void weights_kernel(const float4 *dirs, int R, const float4 *texdir, float sharpness,
                                float *w_color, float *w_depth) {
     const int total = R * 320;
@@ -692,12 +688,10 @@ __global__ void weights_kernel(const float4 *dirs, int R, const float4 *texdir, 
         const int r = i / 320, t = i - r * 320;
         const float4 d = dirs[r], n = texdir[t];
         const float c = fmaxf(dot3(n.x, n.y, n.z, d.x, d.y, d.z), 0.0f);
-        // weights are tf32 numbers (low 13 mantissa bits cleared): the tensor-core
-        // blend then needs only the probe channels split into hi + lo
         if (t < 64)
-            w_color[r * 64 + t] = tf32_trunc(c);
+            w_color[r * 64 + t] = c;
         else
-            w_depth[r * 256 + (t - 64)] = tf32_trunc(powf(c, sharpness));
+            w_depth[r * 256 + (t - 64)] = powf(c, sharpness);
     }
 }
 

@@ -197,6 +197,10 @@ class DistKindStream:
         self.layout = UpdateAtlasLayout(slot_count or n, kind.core_side, probe_count=n,
                                         device=device)
         self.bits = torch.empty((n + 31) // 32, dtype=torch.int32, device=device)
+        # session-owned scratch + pinned active flags (see _device.Workspace)
+        self.active = D.active_flags(volume, device)
+        self.ws_detect = D.workspace(N.lib().ps_detect_workspace_bytes(n), device)
+        self.ws_select = D.workspace(N.lib().ps_select_workspace_bytes(n), device)
         self.sel_ids = torch.empty(n, dtype=torch.int64, device=device)
         self.sel_count = torch.empty(1, dtype=torch.int64, device=device)
         core = kind.core_side ** 2
@@ -267,7 +271,7 @@ class DistKindStream:
         self._mark(f"{tag}.detect", 0)
         N.call("ps_detect_changed_bcast", self.kind.native, src.texels.data_ptr(),
                self.last_sent.texels.data_ptr(), vol.probe_count, src.probes_per_row,
-               src.block_rows, self.begin, self.end, vol.active_device(dev).data_ptr(), thr, is64,
+               src.block_rows, self.begin, self.end, self.active.data_ptr(), thr, is64,
                self.dst_bits[k].data_ptr(), world, st)
         self._mark(f"{tag}.detect", 1)
         self._mark(f"{tag}.exchange_bits", 0)
@@ -277,7 +281,7 @@ class DistKindStream:
         self._mark(f"{tag}.select", 0)
         select_device(self.bits2[k], pvs_bits, vol, self.last_sent_seq, seq, self.budget,
                       out_ids=self.sel_ids, out_count=self.sel_count,
-                      workspace_slot=f"select.{tag}", ordered=False)
+                      workspace_slot=self.ws_select, ordered=False, active=self.active)
         self.bits2[k].zero_()  # ready for frame + 2 (peers write it only after our next flag)
         self._mark(f"{tag}.select", 1)
         self._mark(f"{tag}.assign", 0)
@@ -384,15 +388,15 @@ class DistKindStream:
                        D.stream_ptr(dev))
             self._mark(f"{tag}.detect", 0)
             detect_changed_device(rendered, self.last_sent, self.volume, self.threshold,
-                                  bits=self.bits, with_ids=False, workspace_slot=f"detect.{tag}",
-                                  probe_range=(self.begin, self.end))
+                                  bits=self.bits, with_ids=False, workspace_slot=self.ws_detect,
+                                  probe_range=(self.begin, self.end), active=self.active)
             self._mark(f"{tag}.detect", 1)
 
         def seg_select_export():
             self._mark(f"{tag}.select", 0)
             select_device(self.bits, pvs_bits, self.volume, self.last_sent_seq, seq, self.budget,
                           out_ids=self.sel_ids, out_count=self.sel_count,
-                          workspace_slot=f"select.{tag}", ordered=False)
+                          workspace_slot=self.ws_select, ordered=False, active=self.active)
             self._mark(f"{tag}.select", 1)
             self._mark(f"{tag}.assign", 0)
             entries, count = self.layout.assign_device(self.sel_ids, self.sel_count)

@@ -17,14 +17,19 @@ from . import _device as D
 from . import _native as N
 
 
-def encode_index_device(entries: torch.Tensor, entry_count: torch.Tensor, out=None, out_len=None):
+def encode_index_device(entries: torch.Tensor, entry_count: torch.Tensor, out=None, out_len=None,
+                        workspace=None):
+    """Stream-ordered index buffer of the first ``entry_count`` entries; a
+    session passes its own ``workspace`` (uint8 tensor), one-off calls use a
+    named per-device slot on the current stream."""
     cap = int(entries.shape[0])
     dev = entries.device
     if out is None:
         out = torch.empty(1 + 20 * max(cap, 1), dtype=torch.uint8, device=dev)
     if out_len is None:
         out_len = torch.zeros(1, dtype=torch.int64, device=dev)
-    ws = D.Workspace.get(N.lib().ps_index_workspace_bytes(cap), dev, f"index.{id(entries)}")
+    ws = D.Workspace.get(N.lib().ps_index_workspace_bytes(cap), dev,
+                         "index" if workspace is None else workspace)
     N.call("ps_encode_index", entries.data_ptr(), entry_count.data_ptr(), cap, out.data_ptr(),
            out_len.data_ptr(), ws.data_ptr(), ws.numel(), D.stream_ptr(dev))
     return out, out_len

@@ -338,7 +338,11 @@ class UpdateAtlasLayout:
             raise ValueError("layout has no probe capacity; pass probe_count")
         ids = ids.to(torch.int64).contiguous()
         nbytes = N.lib().ps_assign_workspace_bytes(self._cap, self.slot_count)
-        ws = D.Workspace.get(nbytes, self.device, f"assign.{id(self)}")
+        ws = getattr(self, "_ws", None)
+        if ws is None or ws.numel() < nbytes:
+            # the layout owns its scratch (sized for its capacity, which only
+            # grows before the first device assign)
+            ws = self._ws = D.workspace(nbytes, self.device)
         N.call("ps_assign_slots", ids.data_ptr(), D.ptr(count), int(ids.numel()), self._cap,
                self.slot_count, self._probe_slot.data_ptr(), self._slot_probe.data_ptr(),
                self._last_selected.data_ptr(), self._meta.data_ptr(), self._entries.data_ptr(),

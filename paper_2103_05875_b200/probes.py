@@ -29,10 +29,10 @@ returns the sky colour.  Depth = ``min(t, max_distance)`` (miss:
 
 Blend (device): colour texel t (8x8, texel_directions) averages radiance
 with weights ``max(0, n_t . d_r)``; depth texel t (16x16) averages depth and
-depth^2 with ``max(0, n_t . d_r)^sharpness``; weights are float32 rounded
-toward zero to tf32 (10 mantissa bits), which lets the tensor-core blend
-(csrc/ps_blend_tc.cu) be fp32-accurate with two tf32 MMAs per product; state = frame + h (prev -
-frame) (h = 0 on the first frame); a texel no ray reaches keeps its state.
+depth^2 with ``max(0, n_t . d_r)^sharpness`` (plain float32 weights); the
+tensor-core blend (csrc/ps_blend_tc.cu) is fp32-accurate by 3xTF32 (weights
+and ray channels split hi + lo); state = fma(h, prev - frame, frame) (h = 0
+on the first frame); a texel no ray reaches keeps its state.
 Output: colour unorm10 of ``state / irradiance_scale`` (round to nearest
 even), visibility raw float16 halves; border texels by the guard-band rule
 (packing.py:180-196).

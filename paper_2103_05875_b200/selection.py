@@ -56,7 +56,7 @@ def _check_layout(rendered, last_sent, volume):
 
 def detect_changed_device(rendered, last_sent, volume, threshold=0.0, *, bits=None,
                           ids=None, count=None, with_ids=True, workspace_slot="detect",
-                          probe_range=None):
+                          probe_range=None, active=None):
     """Stream-ordered detection.  Returns (changed_bits uint32[(N+31)/32],
     ids int64[N] (first ``count`` valid) or None, count int64[1] or None).
     ``probe_range`` restricts the test to a z-slab [begin, end)."""
@@ -80,7 +80,8 @@ def detect_changed_device(rendered, last_sent, volume, threshold=0.0, *, bits=No
             count = torch.empty(1, dtype=torch.int64, device=dev)
     ws = D.Workspace.get(N.lib().ps_detect_workspace_bytes(n), dev, workspace_slot)
     thr, is64 = _threshold_args(threshold)
-    active = volume.active_device(dev)
+    if active is None:
+        active = D.active_flags(volume, dev)
     begin, end = probe_range if probe_range is not None else (0, n)
     N.call("ps_detect_changed_range", kind_of(rendered.kind).native, a.data_ptr(), b.data_ptr(),
            n, ppr, block_rows, begin, end, active.data_ptr(), thr, is64, bits.data_ptr(),
@@ -133,7 +134,7 @@ def bits_to_ids(bits, probe_count: int):
 
 def select_device(changed_bits, pvs_bits, volume, last_sent_seq, current_seq: int,
                   budget=None, *, out_ids=None, out_count=None, workspace_slot="select",
-                  ordered: bool = True):
+                  ordered: bool = True, active=None):
     """Stream-ordered selection over bitmaps; pvs_bits None means every probe.
     Returns (ids int64[N], count int64[1]) with the first count ids valid, in
     staleness order (``ordered``) or, without a budget, ascending id order --
@@ -149,9 +150,10 @@ def select_device(changed_bits, pvs_bits, volume, last_sent_seq, current_seq: in
         out_count = torch.empty(1, dtype=torch.int64, device=dev)
     ws = D.Workspace.get(N.lib().ps_select_workspace_bytes(n), dev, workspace_slot)
     has_budget = budget is not None
-    N.call("ps_select", changed_bits.data_ptr(), D.ptr(pvs_bits),
-           volume.active_device(dev).data_ptr(), seq.data_ptr(), int(current_seq), n,
-           int(has_budget), int(budget) if has_budget else 0, int(bool(ordered)), out_ids.data_ptr(),
+    if active is None:
+        active = D.active_flags(volume, dev)
+    N.call("ps_select", changed_bits.data_ptr(), D.ptr(pvs_bits), active.data_ptr(),
+           seq.data_ptr(), int(current_seq), n, int(has_budget), int(budget) if has_budget else 0, int(bool(ordered)), out_ids.data_ptr(),
            out_count.data_ptr(), ws.data_ptr(), ws.numel(), D.stream_ptr(dev))
     return out_ids, out_count
 
@@ -338,7 +340,7 @@ def pvs_probes_device(pose: CameraPose, scene, volume, params: SelectionParams, 
     nx, ny, nz = volume.dims
     N.call("ps_pvs", ds.nodes.data_ptr(), ds.width, ds.tris.data_ptr(), v64.data_ptr(),
            d_rays.data_ptr(), len(rays), cam.ctypes.data, nx, ny, nz, vo.ctypes.data, vs.ctypes.data,
-           volume.active_device(dev).data_ptr(), bits.data_ptr(), ids.data_ptr(), count.data_ptr(),
+           D.active_flags(volume, dev).data_ptr(), bits.data_ptr(), ids.data_ptr(), count.data_ptr(),
            ws.data_ptr(), ws.numel(), D.stream_ptr(dev))
     return bits, ids, count
 

@@ -87,6 +87,12 @@ class KindStream:
         self.bits = torch.empty((n + 31) // 32, dtype=torch.int32, device=device)
         self.sel_ids = torch.empty(n, dtype=torch.int64, device=device)
         self.sel_count = torch.empty(1, dtype=torch.int64, device=device)
+        # session-owned scratch and flags: never shared with another session or
+        # stream, never reallocated after a CUDA graph captured their pointers
+        lib = N.lib()
+        self.active = D.active_flags(volume, device)
+        self.ws_detect = D.workspace(lib.ps_detect_workspace_bytes(n), device)
+        self.ws_select = D.workspace(lib.ps_select_workspace_bytes(n), device)
         self._cur = 0
         self.timers = None  # optional dict of per-stage (start, end) event lists
         # CUDA-graph replay (enable_graphs): {seq, frame_count, key} live on the
@@ -147,12 +153,13 @@ class KindStream:
             key_dev = self.frame_state[2:3].view(torch.int32)[:1]
         self._mark(f"{tag}.detect", 0)
         detect_changed_device(rendered, self.last_sent, self.volume, self.threshold,
-                              bits=self.bits, with_ids=False, workspace_slot=f"detect.{tag}")
+                              bits=self.bits, with_ids=False, workspace_slot=self.ws_detect,
+                              active=self.active)
         self._mark(f"{tag}.detect", 1)
         self._mark(f"{tag}.select", 0)
         select_device(self.bits, pvs_bits, self.volume, self.last_sent_seq, seq, self.budget,
                       out_ids=self.sel_ids, out_count=self.sel_count,
-                      workspace_slot=f"select.{tag}", ordered=False)
+                      workspace_slot=self.ws_select, ordered=False, active=self.active)
         self._mark(f"{tag}.select", 1)
         self._mark(f"{tag}.assign", 0)
         entries, count = self.layout.assign_device(self.sel_ids, self.sel_count)
@@ -206,10 +213,17 @@ class KindStream:
                                torch.empty(icap, dtype=torch.uint8, device=self.device),
                                torch.zeros(1, dtype=torch.int64, device=self.device))
                               for _ in range(2)]
+                lib = N.lib()
+                self._ws_encode = D.workspace(lib.ps_encode_workspace_bytes(
+                    cur.shape[1], cur.shape[2], cur.element_size()), self.device)
+                self._ws_index = D.workspace(
+                    lib.ps_index_workspace_bytes(int(entries.shape[0])), self.device)
             fb, fl, ib, il = self._wire[k]
             frame, frame_len = encode_frame_device(cur, prev, self.stream_id, self.frame_count,
-                                                   out=fb, frame_len=fl)
-            index, index_len = encode_index_device(entries, count, out=ib, out_len=il)  # §8(f)4
+                                                   out=fb, frame_len=fl,
+                                                   workspace=self._ws_encode)
+            index, index_len = encode_index_device(entries, count, out=ib, out_len=il,
+                                                   workspace=self._ws_index)  # §8(f)4
             self._mark(f"{tag}.encode", 1)
         return self._advance(frame, frame_len, index, index_len)
 

@@ -227,7 +227,7 @@ class SlabServer:
         torch.cuda.synchronize(self.device)
         out = {}
         for ks in (impl.color, impl.visibility):
-            cur, prev = ks.planes[ks._cur - 1 if ks._cur else 1], ks.planes[ks._cur]
+            cur, prev = ks.planes[ks._cur], ks.planes[1 - ks._cur]  # newest after _advance
             raw = cur.numel() * cur.element_size()
             for tag, ref in (("key", None), ("p", prev)):
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

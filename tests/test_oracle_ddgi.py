@@ -75,3 +75,49 @@ def test_quantize_is_round_half_even():
     q = ddgi.quantize_color(irr, 1.0)
     r, g, b = q[0, 0, 0] & 1023, (q[0, 0, 0] >> 10) & 1023, q[0, 0, 0] >> 20
     assert (r, g, b) == (np.rint(np.float32(0.5 / 1023) * np.float32(1023)), 2, 1023)
+
+
+@pytest.mark.parametrize("rays,h", [(64, 0.0), (256, 0.97)])
+def test_oracle_blend_is_fp32_accurate(rays, h):
+    """The float32 oracle blend (float64 ray sums rounded once, float32
+    normalisation and hysteresis) equals an all-float64 blend of the same
+    float32 inputs to 1e-6 relative: the oracle is an honest fp32 DDGI
+    blend, with plain (not tf32-rounded) float32 weights."""
+    rng = np.random.default_rng(rays)
+    dirs = ddgi.ray_table(rays, 5, 1).astype(np.float32)
+    w = ddgi.blend_weights(dirs, 50.0)
+    # weights are plain float32: the low 13 mantissa bits are not all zero
+    assert np.any(w[0].view(np.uint32) & np.uint32(0x1FFF))
+    assert np.any(w[1].view(np.uint32) & np.uint32(0x1FFF))
+    P = 24
+    rgb = rng.gamma(2.0, 0.3, size=(P, rays, 3)).astype(np.float32)
+    rgb[:, ::7] = 0.0  # sky-less misses / unlit hits
+    dep = rng.uniform(0.05, 12.0, size=(P, rays)).astype(np.float32)
+    prev_i = rng.uniform(0, 2, size=(P, 64, 3)).astype(np.float32) if h else None
+    prev_m = rng.uniform(0, 20, size=(P, 256, 2)).astype(np.float32) if h else None
+    irr, mom = ddgi.blend(rgb, dep, w, prev_i, prev_m, h)
+    irr64, mom64 = ddgi.blend_f64(rgb, dep, w, prev_i, prev_m, h)
+    if not h:
+        np.testing.assert_allclose(irr, irr64, rtol=1e-6, atol=1e-7)
+        np.testing.assert_allclose(mom, mom64, rtol=1e-6, atol=1e-7)
+    else:
+        # fma(h, prev - frame, frame) in float32: the difference prev - frame
+        # is rounded once, so the error scales with |prev| + |frame|
+        f_irr, f_mom = ddgi.blend_f64(rgb, dep, w, None, None, 0.0)
+        for got, want, prev, frame in ((irr, irr64, prev_i, f_irr), (mom, mom64, prev_m, f_mom)):
+            tol = 1e-6 * np.abs(want) + 2 * np.spacing(np.abs(prev) + np.abs(frame).astype(np.float32))
+            assert np.all(np.abs(got - want) <= tol)
+
+
+def test_oracle_weights_follow_the_definition():
+    """Colour weight = max(0, n.d) within 2 ulp of the float64 dot product;
+    depth weight = that cosine ^ sharpness rounded once."""
+    dirs = ddgi.ray_table(256, 2, 3).astype(np.float32)
+    wc, wd, inv_c, inv_d = ddgi.blend_weights(dirs, 50.0)
+    n8 = ddgi.texel_directions(8).astype(np.float32).astype(np.float64)
+    exact = np.maximum(n8 @ dirs[:, :3].astype(np.float64).T, 0.0)
+    assert np.all(np.abs(wc - exact) <= 2 * np.spacing(np.float32(1.0)))
+    _, cd = ddgi.texel_cosines(dirs)
+    assert np.array_equal(wd, np.power(cd.astype(np.float64), 50.0).astype(np.float32))
+    np.testing.assert_allclose(inv_c, 1.0 / wc.astype(np.float64).sum(1), rtol=1.2e-7)
+    np.testing.assert_allclose(inv_d, 1.0 / wd.astype(np.float64).sum(1), rtol=1.2e-7)
