@@ -455,7 +455,51 @@ def gen_codec():
     save("codec", **arrays)
 
 
+def _ref_index_buffer(entries):
+    """SPEC.md:355-362 composed from the reference's own varint primitives
+    (varint.py:16-19 zigzag, :27-38 encode_uvarint): count, then per entry
+    the slot delta and the zig-zagged probe delta (both from 0)."""
+    out = bytearray(rvarint.encode_uvarint(len(entries)))
+    ps = pp = 0
+    for slot, probe in entries:
+        out += rvarint.encode_uvarint(slot - ps)
+        out += rvarint.encode_uvarint(int(rvarint.zigzag(np.array([probe - pp]))[0]))
+        ps, pp = slot, probe
+    return bytes(out)
+
+
+def gen_index():
+    """Index buffers (§8(f)4) built from the reference's varint / zig-zag, and
+    the primitives themselves on edge values."""
+    rng = np.random.default_rng(113)
+    arrays = {}
+    lists = [[], [(0, 5), (1, 9)], [(i, 1000 + i) for i in range(400)],
+             [(0, 131071), (1, 0), (7, 65536), (300, 65535)]]
+    for n in (1, 17, 130, 4096):
+        slots = np.sort(rng.choice(10 * n, size=n, replace=False))
+        lists.append(list(zip(slots.tolist(), rng.integers(0, 131072, size=n).tolist())))
+    for i, e in enumerate(lists):
+        arrays[f"e{i}"] = np.asarray(e, np.int64).reshape(-1, 2)
+        arrays[f"b{i}"] = np.frombuffer(_ref_index_buffer(e), np.uint8)
+    arrays["n"] = np.int64(len(lists))
+    vals = np.array([0, 1, -1, 63, -64, 64, -65, 8191, -8192, 2**31 - 1, -2**31, 2**40, -2**40],
+                    np.int64)
+    arrays["zz_in"] = vals
+    arrays["zz_out"] = rvarint.zigzag(vals)
+    uv = [0, 1, 127, 128, 255, 300, 16383, 16384, 2**21, 2**28 - 1, 2**35, 2**56 + 3]
+    arrays["uv_in"] = np.array(uv, np.uint64)
+    blob = b"".join(rvarint.encode_uvarint(v) for v in uv)
+    arrays["uv_lens"] = np.array([len(rvarint.encode_uvarint(v)) for v in uv], np.int64)
+    arrays["uv_out"] = np.frombuffer(blob, np.uint8)
+    save("index", **arrays)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1:
+        for name in sys.argv[1:]:
+            globals()[f"gen_{name}"]()
+        sys.exit(0)
+    gen_index()
     gen_codec()
     gen_pvs()
     gen_pack()

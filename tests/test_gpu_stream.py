@@ -117,8 +117,12 @@ def test_delta_golden(ps, golden, tag):
 
 
 @pytest.mark.parametrize("kind", ["color", "visibility"])
-@pytest.mark.parametrize("slots", [1, 5, 17, 363, 1000, 4096, 16384])
+@pytest.mark.parametrize("slots", [1, 5, 9, 17, 363, 1000, 1089, 4096, 16384, 131072])
 def test_pack_delta_matches_pack_then_delta(ps, kind, slots):
+    """Every row-alignment class of the visibility planes: 16-byte aligned
+    rows (slots 9: one CTA in x; 1,089: 704-byte rows, several CTAs; 131,072:
+    the C4 update atlas, 7,744-byte rows, partial last slot row) and
+    unaligned ones (5, 17, 363, 1,000, 4,096, 16,384)."""
     pkg, packing, _, delta = ps
     rng = np.random.default_rng(slots)
     core = 8 if kind == "color" else 16
