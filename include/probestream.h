@@ -301,7 +301,7 @@ int ps_reconstruct_guard_bands(int kind, void *atlas, int64_t probe_count,
 
 /* BVH: built on the host (binned SAH), uploaded by the shim. */
 typedef struct ps_bvh_sizes {
-    int64_t node_count;  /* 64-byte nodes                                     */
+    int64_t node_count;  /* nodes (size per layout, see ps_bvh_build_wide)   */
     int64_t tri_count;   /* triangles                                         */
     int64_t tri_slots;   /* 48-byte triangle records incl. leaf terminators   */
     int64_t max_depth;   /* deepest inner-node path (traversal stack bound)   */
@@ -314,9 +314,18 @@ typedef struct ps_bvh_sizes {
 int ps_bvh_build(const double *vertices, int64_t tri_count, int leaf_size,
                  ps_bvh_sizes *sizes, float *nodes_out, float *tris_out);
 
-/* Same with a node width of 2 (16-float nodes) or 4 (32-float nodes: child
- * boxes as lo.x[4] hi.x[4] lo.y[4] hi.y[4] lo.z[4] hi.z[4], child refs[4],
- * pad[4]; unused slots have child 0x7fffffff). */
+/* Same with a node layout chosen by `width`:
+ *   2  BVH2, 16-float nodes;
+ *   4  BVH4, 32-float nodes: child boxes as lo.x[4] hi.x[4] lo.y[4] hi.y[4]
+ *      lo.z[4] hi.z[4], child refs[4], pad[4]; unused slots have child
+ *      0x7fffffff and the inverted box lo = +inf, hi = -inf;
+ *   5  BVH4 with fp16 child boxes (16-float / 64-byte nodes: the same planes
+ *      as halves, rounded outward, then child refs[4]) -- the default;
+ *   3  BVH4 with fp16 boxes relative to an fp16 node origin and compact child
+ *      references (64-byte nodes; measured slower, kept for comparison);
+ *   8  BVH8 with 8-bit quantised boxes (24-float / 96-byte nodes; measured
+ *      slower, kept for comparison).
+ * Layouts 3 and 8 are documented in csrc/ps_bvh.cpp (emit_bvh4r / emit_bvh8). */
 int ps_bvh_build_wide(const double *vertices, int64_t tri_count, int leaf_size, int width,
                       ps_bvh_sizes *sizes, float *nodes_out, float *tris_out);
 

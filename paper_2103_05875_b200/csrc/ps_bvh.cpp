@@ -268,6 +268,350 @@ uint16_t half_up(double x) {
 
 }  // namespace
 
+// ---- BVH8 with quantised child boxes --------------------------------------------------
+// Node = 96 bytes (24 words), three 32-byte sectors, 32-byte aligned:
+//   w0-2   p.x p.y p.z          float quantisation origin (node box lo - one step)
+//   w3     e_x | e_y << 8 | e_z << 16 | imask << 24
+//                               biased exponents (scale_a = 2^(e_a - 127)) and the
+//                               inner-child slot mask
+//   w4     child_base           node index of the first inner child; a node's inner
+//                               children are contiguous, in slot order
+//   w5     tri_base             first triangle record of the node's leaf children
+//                               (contiguous, in slot order)
+//   w6-7   meta[8]              leaf slot: offset (bits 0-4) from tri_base | count << 5
+//   w8-9   qlo_x[8]  w10-11 qlo_y[8]  w12-13 qlo_z[8]  w14-15 qhi_x[8]
+//   w16-17 qhi_y[8]  w18-19 qhi_z[8]  w20-23 zero
+// Child box along axis a = p_a + scale_a * [qlo, qhi], rounded outward by one
+// extra step: the device evaluates the slab distance as
+// fma(float(0x4B000000 | q), scale * idir, fma(p, idir, -o * idir) - 2^23 * scale * idir),
+// whose rounding error is at most half a step (plus the fp32 rounding the float
+// box test has too), so the decoded box still contains the child.  Empty slots:
+// qlo = 255, qhi = 0 (entry beyond exit for either direction sign: never hit).
+// Slots: child c goes to the slot s minimising dot(centroid_c - centroid, d_s),
+// d_s = the diagonal of octant s (bit a set: axis a negative), greedily; a ray of
+// octant o then visits hit inner slots in ascending s ^ o, which approximates
+// front-to-back order without sorting (Ylitie et al. 2017, simplified).
+constexpr int N8_WORDS = 24;
+
+struct Quant {
+    float p;
+    int e;  // biased exponent byte
+    double scale;
+};
+
+Quant quantise_axis(double lo, double hi) {
+    const double ext = std::max(0.0, hi - lo);
+    int e = ext > 0 ? int(std::ceil(std::log2(ext / 252.0))) : -126;
+    e = std::max(e, -126);
+    for (;; ++e) {
+        if (e > 127) throw std::invalid_argument("scene extent too large for the BVH8 quantisation");
+        const double s = std::ldexp(1.0, e);
+        const float p = round_down(lo - s);
+        // every child plane maps into [1, 254] before the one-step margin
+        if ((hi - double(p)) / s + 1.0 <= 254.0 && (lo - double(p)) / s >= 1.0) return {p, e + 127, s};
+    }
+}
+
+int emit_bvh8(const Builder &b, const double *vertices, int64_t tri_count, ps_bvh_sizes *sizes,
+              float *nodes_out, float *tris_out) {
+    const auto &bn = b.nodes;
+    auto is_leaf = [&](int id) { return bn[id].left < 0; };
+    auto collapse = [&](int id) {
+        std::vector<int> kids;
+        if (is_leaf(id)) {
+            kids.push_back(id);  // the whole scene is one leaf
+            return kids;
+        }
+        kids = {bn[id].left, bn[id].right};
+        while (kids.size() < 8) {
+            int best = -1;
+            double area = -1.0;
+            for (int k = 0; k < int(kids.size()); ++k)
+                if (!is_leaf(kids[k]) && bn[kids[k]].box.area() > area) {
+                    area = bn[kids[k]].box.area();
+                    best = k;
+                }
+            if (best < 0) break;
+            const int c = kids[best];
+            kids[best] = bn[c].left;
+            kids.insert(kids.begin() + best + 1, bn[c].right);
+        }
+        return kids;
+    };
+    struct Out {
+        int build_id;
+        std::vector<int> slot_kid;  // 8 entries, -1 = empty
+        int child_base = 0, tri_base = 0;
+        std::vector<int> leaf_off;  // per slot
+        int depth = 1;
+    };
+    std::vector<Out> out;
+    std::vector<int> leaf_order;  // build leaves in record order
+    int64_t slots = 0, max_depth = 1;
+    out.push_back(Out{0, {}, 0, 0, {}, 1});
+    for (size_t i = 0; i < out.size(); ++i) {  // BFS: children get consecutive indices
+        const std::vector<int> kids = collapse(out[i].build_id);
+        const Aabb &pb = bn[out[i].build_id].box;
+        double pc[3];
+        for (int a = 0; a < 3; ++a) pc[a] = 0.5 * (pb.lo[a] + pb.hi[a]);
+        // greedy slot assignment by the lowest dot(centroid - parent centroid, d_s)
+        std::vector<int> slot_kid(8, -1);
+        std::vector<char> used(kids.size(), 0);
+        for (size_t round = 0; round < kids.size(); ++round) {
+            double best = std::numeric_limits<double>::infinity();
+            int bk = -1, bs = -1;
+            for (size_t k = 0; k < kids.size(); ++k) {
+                if (used[k]) continue;
+                const Aabb &cb = bn[kids[k]].box;
+                for (int sl = 0; sl < 8; ++sl) {
+                    if (slot_kid[sl] >= 0) continue;
+                    double d = 0.0;
+                    for (int a = 0; a < 3; ++a)
+                        d += (0.5 * (cb.lo[a] + cb.hi[a]) - pc[a]) * ((sl >> a) & 1 ? -1.0 : 1.0);
+                    if (d < best) {
+                        best = d;
+                        bk = int(k);
+                        bs = sl;
+                    }
+                }
+            }
+            slot_kid[bs] = kids[bk];
+            used[bk] = 1;
+        }
+        Out &o = out[i];
+        o.slot_kid = slot_kid;
+        o.leaf_off.assign(8, 0);
+        o.child_base = int(out.size());
+        o.tri_base = int(slots);
+        int off = 0;
+        for (int sl = 0; sl < 8; ++sl) {
+            const int c = slot_kid[sl];
+            if (c < 0 || !is_leaf(c)) continue;
+            if (bn[c].count > 7) throw std::invalid_argument("BVH8 leaf with more than 7 triangles");
+            o.leaf_off[sl] = off;
+            off += bn[c].count;
+            leaf_order.push_back(c);
+        }
+        if (off > 31) throw std::invalid_argument("BVH8 node with more than 31 leaf triangles");
+        slots += off;
+        const int depth = o.depth;
+        for (int sl = 0; sl < 8; ++sl) {
+            const int c = out[i].slot_kid[sl];
+            if (c >= 0 && !is_leaf(c)) {
+                out.push_back(Out{c, {}, 0, 0, {}, depth + 1});
+                max_depth = std::max<int64_t>(max_depth, depth + 1);
+            }
+        }
+    }
+    sizes->node_count = int64_t(out.size());
+    sizes->tri_count = tri_count;
+    sizes->tri_slots = slots;
+    sizes->max_depth = max_depth;
+    if (!nodes_out || !tris_out) return PS_OK;
+    for (size_t i = 0; i < out.size(); ++i) {
+        const Out &o = out[i];
+        float *nd = nodes_out + N8_WORDS * i;
+        std::memset(nd, 0, N8_WORDS * 4);
+        uint8_t *bytes = reinterpret_cast<uint8_t *>(nd);
+        Aabb box;  // union of the children
+        for (int sl = 0; sl < 8; ++sl)
+            if (o.slot_kid[sl] >= 0) box.grow(bn[o.slot_kid[sl]].box);
+        Quant q[3];
+        for (int a = 0; a < 3; ++a) {
+            q[a] = quantise_axis(box.lo[a], box.hi[a]);
+            nd[a] = q[a].p;
+            bytes[12 + a] = uint8_t(q[a].e);
+        }
+        uint8_t imask = 0;
+        int inner_rank = 0;
+        for (int sl = 0; sl < 8; ++sl) {
+            const int c = o.slot_kid[sl];
+            uint8_t *qlo = bytes + 32, *qhi = bytes + 56;  // qlo x/y/z at 32/40/48, qhi at 56/64/72
+            if (c < 0) {
+                for (int a = 0; a < 3; ++a) {
+                    qlo[8 * a + sl] = 255;
+                    qhi[8 * a + sl] = 0;
+                }
+                continue;
+            }
+            const Aabb &cb = bn[c].box;
+            for (int a = 0; a < 3; ++a) {
+                const double lo = std::floor((cb.lo[a] - double(q[a].p)) / q[a].scale) - 1.0;
+                const double hi = std::ceil((cb.hi[a] - double(q[a].p)) / q[a].scale) + 1.0;
+                if (lo < 0.0 || hi > 255.0) throw std::logic_error("BVH8 quantisation out of range");
+                qlo[8 * a + sl] = uint8_t(lo);
+                qhi[8 * a + sl] = uint8_t(hi);
+            }
+            if (is_leaf(c)) {
+                bytes[24 + sl] = uint8_t(o.leaf_off[sl] | (bn[c].count << 5));
+            } else {
+                imask |= uint8_t(1u << sl);
+                ++inner_rank;
+            }
+        }
+        bytes[15] = imask;
+        set_int(nd + 4, o.child_base);
+        set_int(nd + 5, o.tri_base);
+        (void)inner_rank;
+    }
+    int64_t s = 0;
+    for (int id : leaf_order) {
+        const BuildNode &l = bn[id];
+        for (int i = l.first; i < l.first + l.count; ++i) {
+            const int t = b.ref_tri[b.order[i]];
+            const double *p = vertices + 9 * size_t(t);
+            float *r = tris_out + 12 * s;
+            r[0] = float(p[0]); r[1] = float(p[1]); r[2] = float(p[2]);
+            set_int(r + 3, t);
+            r[4] = float(p[3] - p[0]); r[5] = float(p[4] - p[1]); r[6] = float(p[5] - p[2]);
+            r[7] = 0.f;
+            r[8] = float(p[6] - p[0]); r[9] = float(p[7] - p[1]); r[10] = float(p[8] - p[2]);
+            r[11] = 0.f;
+            ++s;
+        }
+    }
+    return PS_OK;
+}
+
+// ---- BVH4 with origin-relative fp16 boxes (width 3) ------------------------------------
+// Node = 64 bytes (16 words), two 32-byte sectors -> two 256-bit loads:
+//   w0-3   lo_x[4] hi_x[4]   halves, relative to the node origin
+//   w4-7   lo_y[4] hi_y[4]
+//   w8-11  lo_z[4] hi_z[4]
+//   w12    origin_x | origin_y << 16   (halves: the node box lo rounded down)
+//   w13    origin_z | meta << 16       meta nibble per slot: 0 empty, 15 inner
+//                                      child, else leaf 1 + 2 * offset + (count - 1)
+//   w14    child_base                  node index of the first inner child (a
+//                                      node's inner children are contiguous)
+//   w15    tri_base                    first triangle record of its leaves
+// Relative boxes keep fp16's 11 bits for the node's own extent (a leaf box of a
+// 0.1-unit triangle is inflated by ~1e-4, where absolute fp16 boxes at
+// coordinate 30 would add 0.016 per side); lo rounded down, hi up, so the
+// decoded box contains the child.  Empty slots: lo = +inf, hi = -inf.
+void emit_halfbox(double lo, double hi, double origin, uint16_t &qlo, uint16_t &qhi) {
+    qlo = half_down(lo - origin);
+    qhi = half_up(hi - origin);
+    if (!(origin + h2d(qlo) <= lo) || !(origin + h2d(qhi) >= hi))
+        throw std::logic_error("relative fp16 box not conservative");
+}
+
+int emit_bvh4r(const Builder &b, const double *vertices, int64_t tri_count, ps_bvh_sizes *sizes,
+               float *nodes_out, float *tris_out) {
+    const auto &bn = b.nodes;
+    auto is_leaf = [&](int id) { return bn[id].left < 0; };
+    struct Out {
+        int build_id, depth;
+        std::vector<int> kids;
+        int child_base = 0, tri_base = 0;
+    };
+    std::vector<Out> out{{0, 1, {}, 0, 0}};
+    std::vector<int> leaf_order;
+    int64_t slots = 0, max_depth = 1;
+    for (size_t i = 0; i < out.size(); ++i) {
+        std::vector<int> kids;
+        const int id = out[i].build_id;
+        if (is_leaf(id)) {
+            kids.push_back(id);
+        } else {
+            kids = {bn[id].left, bn[id].right};
+            while (kids.size() < 4) {
+                int best = -1;
+                double area = -1.0;
+                for (int k = 0; k < int(kids.size()); ++k)
+                    if (!is_leaf(kids[k]) && bn[kids[k]].box.area() > area) {
+                        area = bn[kids[k]].box.area();
+                        best = k;
+                    }
+                if (best < 0) break;
+                const int c = kids[best];
+                kids[best] = bn[c].left;
+                kids.insert(kids.begin() + best + 1, bn[c].right);
+            }
+        }
+        out[i].kids = kids;
+        out[i].child_base = int(out.size());
+        out[i].tri_base = int(slots);
+        int off = 0;
+        for (int c : kids)
+            if (is_leaf(c)) {
+                if (bn[c].count > 2) throw std::invalid_argument("width-3 leaf with > 2 triangles");
+                leaf_order.push_back(c);
+                off += bn[c].count;
+            }
+        slots += off;
+        const int depth = out[i].depth;
+        for (int c : kids)
+            if (!is_leaf(c)) {
+                out.push_back(Out{c, depth + 1, {}, 0, 0});
+                max_depth = std::max<int64_t>(max_depth, depth + 1);
+            }
+    }
+    sizes->node_count = int64_t(out.size());
+    sizes->tri_count = tri_count;
+    sizes->tri_slots = slots;
+    sizes->max_depth = max_depth;
+    if (!nodes_out || !tris_out) return PS_OK;
+    for (size_t i = 0; i < out.size(); ++i) {
+        const Out &o = out[i];
+        float *nd = nodes_out + 16 * i;
+        std::memset(nd, 0, 64);
+        uint16_t *hb = reinterpret_cast<uint16_t *>(nd);
+        Aabb box;
+        for (int c : o.kids) box.grow(bn[c].box);
+        double org[3];
+        uint16_t org_h[3];
+        for (int a = 0; a < 3; ++a) {
+            org_h[a] = half_down(box.lo[a]);
+            org[a] = h2d(org_h[a]);
+        }
+        uint32_t meta = 0;
+        int off = 0;
+        for (int k = 0; k < 4; ++k) {
+            if (k >= int(o.kids.size())) {
+                for (int a = 0; a < 3; ++a) {
+                    hb[8 * a + k] = 0x7C00u;
+                    hb[8 * a + 4 + k] = 0xFC00u;
+                }
+                continue;
+            }
+            const int c = o.kids[k];
+            const Aabb &cb = bn[c].box;
+            for (int a = 0; a < 3; ++a) emit_halfbox(cb.lo[a], cb.hi[a], org[a], hb[8 * a + k], hb[8 * a + 4 + k]);
+            uint32_t nib;
+            if (is_leaf(c)) {
+                nib = 1u + 2u * uint32_t(off) + uint32_t(bn[c].count - 1);
+                off += bn[c].count;
+            } else {
+                nib = 15u;
+            }
+            meta |= nib << (4 * k);
+        }
+        hb[24] = org_h[0];
+        hb[25] = org_h[1];
+        hb[26] = org_h[2];
+        hb[27] = uint16_t(meta);
+        set_int(nd + 14, o.child_base);
+        set_int(nd + 15, o.tri_base);
+    }
+    int64_t s = 0;
+    for (int id : leaf_order) {
+        const BuildNode &l = bn[id];
+        for (int i = l.first; i < l.first + l.count; ++i) {
+            const int t = b.ref_tri[b.order[i]];
+            const double *p = vertices + 9 * size_t(t);
+            float *r = tris_out + 12 * s;
+            r[0] = float(p[0]); r[1] = float(p[1]); r[2] = float(p[2]);
+            set_int(r + 3, t);
+            r[4] = float(p[3] - p[0]); r[5] = float(p[4] - p[1]); r[6] = float(p[5] - p[2]);
+            r[7] = 0.f;
+            r[8] = float(p[6] - p[0]); r[9] = float(p[7] - p[1]); r[10] = float(p[8] - p[2]);
+            r[11] = 0.f;
+            ++s;
+        }
+    }
+    return PS_OK;
+}
+
 // Shared implementation: binned-SAH binary build, then emission as BVH2
 // (16-float nodes, see the header comment) or BVH4 (32-float nodes: lo.x[4]
 // hi.x[4] lo.y[4] hi.y[4] lo.z[4] hi.z[4] child[4] pad[4]; a BVH2 node's
@@ -280,8 +624,14 @@ static int bvh_build_impl(const double *vertices, int64_t tri_count, int leaf_si
         if (tri_count < 1) throw std::invalid_argument("scene needs at least one triangle");
         if (tri_count > (int64_t(1) << 27)) throw std::invalid_argument("too many triangles");
         if (leaf_size < 1 || leaf_size > 7) throw std::invalid_argument("leaf_size in [1, 7]");
-        // width 5 = BVH4 with fp16 child boxes (64-byte nodes)
-        if (width != 2 && width != 4 && width != 5) throw std::invalid_argument("width must be 2, 4 or 5");
+        // width 5 = BVH4 with fp16 child boxes (64-byte nodes); width 8 = BVH8 with
+        // 8-bit quantised child boxes (96-byte nodes, see emit_bvh8)
+        // width 3 = BVH4 with fp16 boxes relative to an fp16 node origin and
+        // compact child references (64-byte nodes, see emit_bvh4r)
+        if (width != 2 && width != 3 && width != 4 && width != 5 && width != 8)
+            throw std::invalid_argument("width must be 2, 3, 4, 5 or 8");
+        if (width == 8 && leaf_size > 3) throw std::invalid_argument("BVH8 leaves hold <= 3 triangles");
+        if (width == 3 && leaf_size > 2) throw std::invalid_argument("width-3 leaves hold <= 2 triangles");
         const bool half_boxes = width == 5;
         if (half_boxes) width = 4;
         Builder b;
@@ -316,6 +666,8 @@ static int bvh_build_impl(const double *vertices, int64_t tri_count, int leaf_si
         }
         b.nodes.reserve(2 * size_t(n));
         b.build(0, n);
+        if (width == 8) return emit_bvh8(b, vertices, tri_count, sizes, nodes_out, tris_out);
+        if (width == 3) return emit_bvh4r(b, vertices, tri_count, sizes, nodes_out, tris_out);
 
         // collapse into width-ary nodes (preorder), leaves numbered in DFS order
         std::vector<Wide> wide;
@@ -383,8 +735,12 @@ static int bvh_build_impl(const double *vertices, int64_t tri_count, int leaf_si
                 std::memset(nd, 0, 64);
                 uint16_t *hb = reinterpret_cast<uint16_t *>(nd);
                 for (int k = 0; k < 4; ++k) {
-                    if (k >= w.n) {
+                    if (k >= w.n) {  // inverted infinite box: the octant test never hits it
                         set_int(nd + 12 + k, EMPTY_CHILD);
+                        for (int a = 0; a < 3; ++a) {
+                            hb[8 * a + k] = 0x7C00u;
+                            hb[8 * a + 4 + k] = 0xFC00u;
+                        }
                         continue;
                     }
                     const Aabb &bx = b.nodes[w.kids[k]].box;

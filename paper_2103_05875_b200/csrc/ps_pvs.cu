@@ -103,7 +103,9 @@ __global__ void __launch_bounds__(128) pvs_kernel(PvsArgs a) {
                             float(d[0]), float(d[1]), float(d[2])};
         const float4 *nd = reinterpret_cast<const float4 *>(a.nodes);
         const float4 *tr = reinterpret_cast<const float4 *>(a.tris);
-        const int slot = a.width == 5   ? trav::traverse<false, 1, 5>(nd, tr, ray, INFINITY, tf)
+        const int slot = a.width == 3   ? trav::traverse<false, 1, 17>(nd, tr, ray, INFINITY, tf)
+                         : a.width == 8 ? trav::traverse<false, 1, 16>(nd, tr, ray, INFINITY, tf)
+                         : a.width == 5 ? trav::traverse<false, 1, 5>(nd, tr, ray, INFINITY, tf)
                          : a.width == 4 ? trav::traverse<false, 1, 4>(nd, tr, ray, INFINITY, tf)
                                         : trav::traverse<false, 1, 2>(nd, tr, ray, INFINITY, tf);
         double pt[3];
@@ -166,7 +168,8 @@ int ps_pvs(const float *nodes, int32_t bvh_width, const float *tris, const doubl
            void *workspace, size_t workspace_bytes, void *stream) {
     PS_ABI_BEGIN
     if (nx < 1 || ny < 1 || nz < 1) fail(PS_ERR_VALUE, "volume dims must be >= 1");
-    if (bvh_width != 2 && bvh_width != 4 && bvh_width != 5) fail(PS_ERR_VALUE, "bad bvh_width");
+    if (bvh_width != 2 && bvh_width != 3 && bvh_width != 4 && bvh_width != 5 && bvh_width != 8)
+        fail(PS_ERR_VALUE, "bad bvh_width");
     if (ray_count < 0) fail(PS_ERR_VALUE, "negative ray count");
     auto s = as_stream(stream);
     const int64_t n = int64_t(nx) * ny * nz;

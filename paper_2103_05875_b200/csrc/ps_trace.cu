@@ -303,7 +303,9 @@ __global__ void __launch_bounds__(TPB, TPB == THREADS ? MINB : (TPB == 1024 ? 1 
         ray.dz = d.z;
         const Shade s = shade_ray<SHADOW, LEAFV, WIDTH, STATS>(prm, nodes, tris, ray);
         const int64_t ray_id = q * R + r;
-        records[ray_id] = make_float4(s.r, s.g, s.b, s.depth);
+        // streaming store (evict-first): the 537 MB of records pass through L2
+        // without evicting the BVH the traversal keeps re-reading
+        __stcs(records + ray_id, make_float4(s.r, s.g, s.b, s.depth));
         if (prm.ray_records) {
             float4 *rec = reinterpret_cast<float4 *>(prm.ray_records) + 2 * ray_id;
             rec[0] = make_float4(s.r, s.g, s.b, s.depth);
@@ -734,6 +736,17 @@ void launch_trace_t(const ps_trace_params &p, int sms, cudaStream_t s, bool sm_s
 // reserved SMs
 template <int SHADOW, int LEAFV, int PP, int WIDTH>
 void launch_trace_640(const ps_trace_params &p, int sms, cudaStream_t s) {
+    static const int carve = [] {  // tuning knob: L1 / shared-memory carveout (percent)
+        const char *e = getenv("PS_L1_CARVE");
+        return e ? atoi(e) : -1;
+    }();
+    static bool set = false;
+    if (carve >= 0 && !set) {
+        check_cuda(cudaFuncSetAttribute(trace_kernel<SHADOW, LEAFV, 1, PP, WIDTH, 640>,
+                                        cudaFuncAttributePreferredSharedMemoryCarveout, carve),
+                   "carveout");
+        set = true;
+    }
     trace_kernel<SHADOW, LEAFV, 1, PP, WIDTH, 640><<<2 * sms, 640, 0, s>>>(p);
 }
 
@@ -745,10 +758,41 @@ void launch_trace_ww(const ps_trace_params &p, int sms, cudaStream_t s) {
 
 template <int SHADOW>
 void launch_trace_s(const ps_trace_params &p, int variant, int sms, cudaStream_t s, bool big) {
+    if (p.bvh_width == 3) {  // BVH4, origin-relative fp16 boxes (WIDTH 17)
+        switch (variant) {
+            case 64: launch_trace_640<SHADOW, 0, 4, 17>(p, sms, s); break;
+            case 65: launch_trace_640<SHADOW, 0, 2, 17>(p, sms, s); break;
+            case 90: {  // traversal statistics (tuning only)
+                trace_kernel<SHADOW, 0, 1, 12, 17, 640, 1><<<2 * sms, 640, 0, s>>>(p);
+                break;
+            }
+            default: launch_trace_640<SHADOW, 0, 12, 17>(p, sms, s); break;
+        }
+        return;
+    }
+    if (p.bvh_width == 8) {  // BVH8, quantised boxes (WIDTH 16)
+        switch (variant) {
+            case 64: launch_trace_640<SHADOW, 0, 4, 16>(p, sms, s); break;
+            case 65: launch_trace_640<SHADOW, 0, 2, 16>(p, sms, s); break;
+            case 90: {  // traversal statistics (tuning only)
+                trace_kernel<SHADOW, 0, 1, 12, 16, 640, 1><<<2 * sms, 640, 0, s>>>(p);
+                break;
+            }
+            default: launch_trace_640<SHADOW, 0, 12, 16>(p, sms, s); break;
+        }
+        return;
+    }
     if (p.bvh_width == 5) {
         switch (variant) {
             case 11: launch_trace_t<SHADOW, 1, 4, 0, 5>(p, sms, s, big); break;
-            default: launch_trace_t<SHADOW, 1, 1, 0, 5>(p, sms, s, big); break;
+            case 12: launch_trace_t<SHADOW, 1, 1, 0, 5>(p, sms, s, big); break;
+            // fp16 boxes, octant tests, two 256-bit loads per node
+            case 64: launch_trace_640<SHADOW, 0, 4, 3>(p, sms, s); break;
+            case 70: launch_trace_640<SHADOW, 0, 12, 18>(p, sms, s); break;  // word selects
+            case 71: launch_trace_t<SHADOW, 0, 1, 12, 3>(p, sms, s, true); break;  // 1024 x 1
+            case 72: launch_trace_640<SHADOW, 1, 12, 3>(p, sms, s); break;  // leaf pairs
+            case 65: launch_trace_640<SHADOW, 0, 2, 3>(p, sms, s); break;
+            default: launch_trace_640<SHADOW, 0, 12, 3>(p, sms, s); break;
         }
         return;
     }
@@ -870,8 +914,9 @@ int ps_trace_blend(const ps_trace_params *params, void *stream) {
     if (p.light_count < 0 || p.light_count > 30) fail(PS_ERR_VALUE, "light_count in [0, 30]");
     if (p.probes_per_row_color < 1 || p.probes_per_row_vis < 1) fail(PS_ERR_LAYOUT, "bad atlas layout");
     if (p.shadow_mode < PS_SHADOW_NONE || p.shadow_mode > PS_SHADOW_MAP) fail(PS_ERR_VALUE, "bad shadow_mode");
-    if (p.bvh_width != 2 && p.bvh_width != 4 && p.bvh_width != 5)
-        fail(PS_ERR_VALUE, "bvh_width must be 2, 4 or 5 (BVH4 with fp16 boxes)");
+    if (p.bvh_width != 2 && p.bvh_width != 3 && p.bvh_width != 4 && p.bvh_width != 5 &&
+        p.bvh_width != 8)
+        fail(PS_ERR_VALUE, "bvh_width must be 2, 4, 5 (BVH4 with fp16 boxes) or 8 (BVH8, 8-bit boxes)");
     if (p.bvh_width == 4 && (p.shadow_mode == PS_SHADOW_RAYS || false)) {
         // any-hit shadow rays use the same templated traversal: fine
     }
@@ -893,8 +938,12 @@ int ps_trace_blend(const ps_trace_params *params, void *stream) {
         const int64_t texels = end > p.shadow_texel_begin ? end - p.shadow_texel_begin : 0;
         const unsigned blocks = unsigned(std::max<int64_t>(
             1, std::min<int64_t>(ceil_div(texels, 256), int64_t(sms) * 32)));
-        if (p.bvh_width == 5)
-            shadow_map_kernel<5><<<blocks, 256, 0, s>>>(p);
+        if (p.bvh_width == 3)
+            shadow_map_kernel<17><<<blocks, 256, 0, s>>>(p);
+        else if (p.bvh_width == 8)
+            shadow_map_kernel<16><<<blocks, 256, 0, s>>>(p);
+        else if (p.bvh_width == 5)
+            shadow_map_kernel<3><<<blocks, 256, 0, s>>>(p);
         else if (p.bvh_width == 4)
             shadow_map_kernel<6><<<blocks, 256, 0, s>>>(p);  // octant-specialised BVH4 tests
         else

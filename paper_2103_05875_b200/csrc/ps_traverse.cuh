@@ -215,15 +215,272 @@ __device__ __forceinline__ void node4o_hits(const float4 *nodes, int node, float
     cswap(d[1], c[1], d[2], c[2]);
 }
 
+// fp16-box BVH4 (64-byte nodes) with the octant-specialised test: two 256-bit
+// loads per node instead of four (the trace is bound by L1 wavefronts of
+// divergent node fetches, one per distinct line per load instruction)
+template <int OCT>
+__device__ __forceinline__ void node4ho_hits(const float4 *nodes, int node, float ix, float iy,
+                                             float iz, float oix, float oiy, float oiz,
+                                             float tmax, float d[4], int c[4]) {
+    constexpr bool NX = OCT & 1, NY = OCT & 2, NZ = OCT & 4;
+    const float4 *nd = nodes + 4 * node;
+    float a[8], b[8];
+    ldg256(nd + 0, a);  // lo_x[4] hi_x[4] | lo_y[4] hi_y[4] (halves)
+    ldg256(nd + 2, b);  // lo_z[4] hi_z[4] | child[4]
+    auto h2 = [](float w) { return __half22float2(*reinterpret_cast<const __half2 *>(&w)); };
+    // word k / 2 of a plane set holds children (2j, 2j+1)
+    const float2 lx0 = h2(a[0]), lx1 = h2(a[1]), hx0 = h2(a[2]), hx1 = h2(a[3]);
+    const float2 ly0 = h2(a[4]), ly1 = h2(a[5]), hy0 = h2(a[6]), hy1 = h2(a[7]);
+    const float2 lz0 = h2(b[0]), lz1 = h2(b[1]), hz0 = h2(b[2]), hz1 = h2(b[3]);
+    const float lxs[4] = {lx0.x, lx0.y, lx1.x, lx1.y}, hxs[4] = {hx0.x, hx0.y, hx1.x, hx1.y};
+    const float lys[4] = {ly0.x, ly0.y, ly1.x, ly1.y}, hys[4] = {hy0.x, hy0.y, hy1.x, hy1.y};
+    const float lzs[4] = {lz0.x, lz0.y, lz1.x, lz1.y}, hzs[4] = {hz0.x, hz0.y, hz1.x, hz1.y};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const float nx = fmaf(NX ? hxs[k] : lxs[k], ix, -oix), fx = fmaf(NX ? lxs[k] : hxs[k], ix, -oix);
+        const float ny = fmaf(NY ? hys[k] : lys[k], iy, -oiy), fy = fmaf(NY ? lys[k] : hys[k], iy, -oiy);
+        const float nz = fmaf(NZ ? hzs[k] : lzs[k], iz, -oiz), fz = fmaf(NZ ? lzs[k] : hzs[k], iz, -oiz);
+        const float tn = fmaxf(fmaxf(nx, ny), fmaxf(nz, 0.0f));
+        const float tf = fminf(fminf(fx, fy), fminf(fz, tmax));
+        d[k] = tn <= tf ? tn : INFINITY;
+        c[k] = __float_as_int(b[4 + k]);
+    }
+    cswap(d[0], c[0], d[1], c[1]);
+    cswap(d[2], c[2], d[3], c[3]);
+    cswap(d[0], c[0], d[2], c[2]);
+    cswap(d[1], c[1], d[3], c[3]);
+    cswap(d[1], c[1], d[2], c[2]);
+}
+
+// BVH4 with origin-relative fp16 boxes and compact child references (WIDTH 17;
+// layout: ps_bvh.cpp emit_bvh4r): two 256-bit loads per node, planes decoded
+// as fma(rel, idir, fma(origin, idir, -o * idir)), children referenced as
+// child_base + rank (inner) or a leaf's (offset, count) from tri_base.
+template <int OCT>
+__device__ __forceinline__ void node4r_hits(const float4 *nodes, int node, float ix, float iy,
+                                            float iz, float oix, float oiy, float oiz,
+                                            float tmax, float d[4], int c[4]) {
+    constexpr bool NX = OCT & 1, NY = OCT & 2, NZ = OCT & 4;
+    const float4 *nd = nodes + 4 * node;
+    float a[8], b[8];
+    ldg256(nd + 0, a);  // lo_x[4] hi_x[4] | lo_y[4] hi_y[4]
+    ldg256(nd + 2, b);  // lo_z[4] hi_z[4] | origin xy, origin z | meta, child_base, tri_base
+    auto h2 = [](float w) { return __half22float2(*reinterpret_cast<const __half2 *>(&w)); };
+    const float2 oxy = h2(b[4]);
+    const uint32_t w13 = __float_as_uint(b[5]);
+    const float oz = __half2float(__ushort_as_half(uint16_t(w13 & 0xFFFFu)));
+    const float Cx = fmaf(oxy.x, ix, -oix), Cy = fmaf(oxy.y, iy, -oiy), Cz = fmaf(oz, iz, -oiz);
+    const float2 lx0 = h2(a[0]), lx1 = h2(a[1]), hx0 = h2(a[2]), hx1 = h2(a[3]);
+    const float2 ly0 = h2(a[4]), ly1 = h2(a[5]), hy0 = h2(a[6]), hy1 = h2(a[7]);
+    const float2 lz0 = h2(b[0]), lz1 = h2(b[1]), hz0 = h2(b[2]), hz1 = h2(b[3]);
+    const float lxs[4] = {lx0.x, lx0.y, lx1.x, lx1.y}, hxs[4] = {hx0.x, hx0.y, hx1.x, hx1.y};
+    const float lys[4] = {ly0.x, ly0.y, ly1.x, ly1.y}, hys[4] = {hy0.x, hy0.y, hy1.x, hy1.y};
+    const float lzs[4] = {lz0.x, lz0.y, lz1.x, lz1.y}, hzs[4] = {hz0.x, hz0.y, hz1.x, hz1.y};
+    const uint32_t meta = w13 >> 16;
+    const int child_base = __float_as_int(b[6]), tri_base = __float_as_int(b[7]);
+    int rank = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const float nx = fmaf(NX ? hxs[k] : lxs[k], ix, Cx), fx = fmaf(NX ? lxs[k] : hxs[k], ix, Cx);
+        const float ny = fmaf(NY ? hys[k] : lys[k], iy, Cy), fy = fmaf(NY ? lys[k] : hys[k], iy, Cy);
+        const float nz = fmaf(NZ ? hzs[k] : lzs[k], iz, Cz), fz = fmaf(NZ ? lzs[k] : hzs[k], iz, Cz);
+        const float tn = fmaxf(fmaxf(nx, ny), fmaxf(nz, 0.0f));
+        const float tf = fminf(fminf(fx, fy), fminf(fz, tmax));
+        d[k] = tn <= tf ? tn : INFINITY;
+        const uint32_t nib = (meta >> (4 * k)) & 15u;
+        const uint32_t v = nib - 1u;  // leaf: offset << 1 | (count - 1)
+        const int leaf = ~int(((uint32_t(tri_base) + (v >> 1)) << 3) | ((v & 1u) + 1u));
+        c[k] = nib == 15u ? child_base + rank : leaf;
+        rank += nib == 15u ? 1 : 0;
+    }
+    cswap(d[0], c[0], d[1], c[1]);
+    cswap(d[2], c[2], d[3], c[3]);
+    cswap(d[0], c[0], d[2], c[2]);
+    cswap(d[1], c[1], d[3], c[3]);
+    cswap(d[1], c[1], d[2], c[2]);
+}
+
+// fp16-box BVH4 (64-byte nodes), entry / exit planes picked per axis by the
+// ray's direction signs with word selects on the packed halves (12 SEL per
+// node) instead of a per-node switch over octant-specialised tests (WIDTH 18)
+__device__ __forceinline__ void node4hs_hits(const float4 *nodes, int node, float ix, float iy,
+                                             float iz, float oix, float oiy, float oiz,
+                                             float tmax, bool negx, bool negy, bool negz,
+                                             float d[4], int c[4]) {
+    const float4 *nd = nodes + 4 * node;
+    float a[8], b[8];
+    ldg256(nd + 0, a);  // lo_x[4] hi_x[4] | lo_y[4] hi_y[4] (halves)
+    ldg256(nd + 2, b);  // lo_z[4] hi_z[4] | child[4]
+    auto h2 = [](float w) { return __half22float2(*reinterpret_cast<const __half2 *>(&w)); };
+    const float2 nx0 = h2(negx ? a[2] : a[0]), nx1 = h2(negx ? a[3] : a[1]);
+    const float2 fx0 = h2(negx ? a[0] : a[2]), fx1 = h2(negx ? a[1] : a[3]);
+    const float2 ny0 = h2(negy ? a[6] : a[4]), ny1 = h2(negy ? a[7] : a[5]);
+    const float2 fy0 = h2(negy ? a[4] : a[6]), fy1 = h2(negy ? a[5] : a[7]);
+    const float2 nz0 = h2(negz ? b[2] : b[0]), nz1 = h2(negz ? b[3] : b[1]);
+    const float2 fz0 = h2(negz ? b[0] : b[2]), fz1 = h2(negz ? b[1] : b[3]);
+    const float nxs[4] = {nx0.x, nx0.y, nx1.x, nx1.y}, fxs[4] = {fx0.x, fx0.y, fx1.x, fx1.y};
+    const float nys[4] = {ny0.x, ny0.y, ny1.x, ny1.y}, fys[4] = {fy0.x, fy0.y, fy1.x, fy1.y};
+    const float nzs[4] = {nz0.x, nz0.y, nz1.x, nz1.y}, fzs[4] = {fz0.x, fz0.y, fz1.x, fz1.y};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const float nx = fmaf(nxs[k], ix, -oix), fx = fmaf(fxs[k], ix, -oix);
+        const float ny = fmaf(nys[k], iy, -oiy), fy = fmaf(fys[k], iy, -oiy);
+        const float nz = fmaf(nzs[k], iz, -oiz), fz = fmaf(fzs[k], iz, -oiz);
+        const float tn = fmaxf(fmaxf(nx, ny), fmaxf(nz, 0.0f));
+        const float tf = fminf(fminf(fx, fy), fminf(fz, tmax));
+        d[k] = tn <= tf ? tn : INFINITY;
+        c[k] = __float_as_int(b[4 + k]);
+    }
+    cswap(d[0], c[0], d[1], c[1]);
+    cswap(d[2], c[2], d[3], c[3]);
+    cswap(d[0], c[0], d[2], c[2]);
+    cswap(d[1], c[1], d[3], c[3]);
+    cswap(d[1], c[1], d[2], c[2]);
+}
+
 // WIDTH 6: BVH4, octant-specialised node test chosen per node (warp-uniform
 // when the warp's rays share a direction); WIDTH 7: the whole traversal
 // instantiated per octant (WIDTH 8 + octant) and chosen once per ray
 // leaf visits, triangle tests, rays
 static __device__ unsigned long long g_trav_stats[4];
 
+// ---- BVH8 with 8-bit quantised child boxes (WIDTH 16; node layout: ps_bvh.cpp
+// emit_bvh8).  Per node three 256-bit loads cover eight children; hit inner
+// children are visited in ascending (slot ^ ray octant), an approximate
+// front-to-back order fixed at build time, so there is no sort and at most one
+// stack push per visited node: the stack holds node groups (first child index,
+// remaining hit slots in order space << 24 | the inner-slot mask).  A popped
+// child is culled by its own children's tests against the current t_best.
+constexpr int STACK8 = 32;
+
+__device__ __forceinline__ float q2f(uint32_t word, int byte) {
+    // 2^23 + q as a float: one byte permute, the 2^23 is folded into the offset
+    return __uint_as_float(__byte_perm(word, 0x4B000000u, 0x7440u + byte));
+}
+
+__device__ __forceinline__ uint32_t oct_permute8(uint32_t m, uint32_t oct) {
+    // bit s -> bit s ^ oct
+    if (oct & 1) m = ((m & 0x55u) << 1) | ((m >> 1) & 0x55u);
+    if (oct & 2) m = ((m & 0x33u) << 2) | ((m >> 2) & 0x33u);
+    if (oct & 4) m = ((m & 0x0Fu) << 4) | ((m >> 4) & 0x0Fu);
+    return m;
+}
+
+template <bool ANY_HIT, int STATS = 0>
+__device__ int traverse8(const float4 *__restrict__ nodes, const float4 *__restrict__ tris,
+                         const Ray &r, float tmax, float &t_best) {
+    unsigned long long st_nodes = 0, st_tris = 0;
+    const float sx = fabsf(r.dx) < 1e-12f ? copysignf(1e-12f, r.dx) : r.dx;
+    const float sy = fabsf(r.dy) < 1e-12f ? copysignf(1e-12f, r.dy) : r.dy;
+    const float sz = fabsf(r.dz) < 1e-12f ? copysignf(1e-12f, r.dz) : r.dz;
+    const bool negx = sx < 0.0f, negy = sy < 0.0f, negz = sz < 0.0f;
+    const uint32_t oct = (negx ? 1u : 0u) | (negy ? 2u : 0u) | (negz ? 4u : 0u);
+    const float ix = 1.0f / sx, iy = 1.0f / sy, iz = 1.0f / sz;
+    const float oix = r.ox * ix, oiy = r.oy * iy, oiz = r.oz * iz;
+    uint2 stack[STACK8];
+    int sp = 0;
+    uint32_t g_base = 0, g_hits = 0;  // current group: order-space hits << 24 | imask
+    int node = 0;
+    int hit_slot = -1;
+    t_best = tmax;
+    while (true) {
+        if (STATS) ++st_nodes;
+        // ---- visit `node`: test its eight children ------------------------------------------
+        const float4 *nd = nodes + 6 * node;
+        float a[8], b[8], c[8];
+        ldg256(nd + 0, a);
+        ldg256(nd + 2, b);
+        ldg256(nd + 4, c);
+        const uint32_t ew = __float_as_uint(a[3]);
+        const uint32_t child_base = __float_as_uint(a[4]), tri_base = __float_as_uint(a[5]);
+        const uint32_t meta0 = __float_as_uint(a[6]), meta1 = __float_as_uint(a[7]);
+        const uint32_t imask = ew >> 24;
+        // per axis: A = scale * idir, C = (p - o) * idir - 2^23 * A
+        const float sxa = __uint_as_float((ew & 0xFFu) << 23);
+        const float sya = __uint_as_float(((ew >> 8) & 0xFFu) << 23);
+        const float sza = __uint_as_float(((ew >> 16) & 0xFFu) << 23);
+        const float Ax = sxa * ix, Ay = sya * iy, Az = sza * iz;
+        const float Cx = fmaf(-8388608.0f, Ax, fmaf(a[0], ix, -oix));
+        const float Cy = fmaf(-8388608.0f, Ay, fmaf(a[1], iy, -oiy));
+        const float Cz = fmaf(-8388608.0f, Az, fmaf(a[2], iz, -oiz));
+        // entry / exit planes by direction sign (4 children per word)
+        const uint32_t lx0 = __float_as_uint(b[0]), lx1 = __float_as_uint(b[1]);
+        const uint32_t ly0 = __float_as_uint(b[2]), ly1 = __float_as_uint(b[3]);
+        const uint32_t lz0 = __float_as_uint(b[4]), lz1 = __float_as_uint(b[5]);
+        const uint32_t hx0 = __float_as_uint(b[6]), hx1 = __float_as_uint(b[7]);
+        const uint32_t hy0 = __float_as_uint(c[0]), hy1 = __float_as_uint(c[1]);
+        const uint32_t hz0 = __float_as_uint(c[2]), hz1 = __float_as_uint(c[3]);
+        const uint32_t nx0 = negx ? hx0 : lx0, nx1 = negx ? hx1 : lx1;
+        const uint32_t fx0 = negx ? lx0 : hx0, fx1 = negx ? lx1 : hx1;
+        const uint32_t ny0 = negy ? hy0 : ly0, ny1 = negy ? hy1 : ly1;
+        const uint32_t fy0 = negy ? ly0 : hy0, fy1 = negy ? ly1 : hy1;
+        const uint32_t nz0 = negz ? hz0 : lz0, nz1 = negz ? hz1 : lz1;
+        const uint32_t fz0 = negz ? lz0 : hz0, fz1 = negz ? lz1 : hz1;
+        uint32_t hit8 = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int w = k & 3;
+            const float tnx = fmaf(q2f(k < 4 ? nx0 : nx1, w), Ax, Cx);
+            const float tny = fmaf(q2f(k < 4 ? ny0 : ny1, w), Ay, Cy);
+            const float tnz = fmaf(q2f(k < 4 ? nz0 : nz1, w), Az, Cz);
+            const float tfx = fmaf(q2f(k < 4 ? fx0 : fx1, w), Ax, Cx);
+            const float tfy = fmaf(q2f(k < 4 ? fy0 : fy1, w), Ay, Cy);
+            const float tfz = fmaf(q2f(k < 4 ? fz0 : fz1, w), Az, Cz);
+            const float tn = fmaxf(fmaxf(tnx, tny), fmaxf(tnz, 0.0f));
+            const float tf = fminf(fminf(tfx, tfy), fminf(tfz, t_best));
+            hit8 |= tn <= tf ? (1u << k) : 0u;
+        }
+        // ---- leaf children: their triangles now -------------------------------------------
+        uint32_t leaves = hit8 & ~imask;
+        while (leaves) {
+            const int sl = __ffs(leaves) - 1;
+            leaves &= leaves - 1;
+            const uint32_t meta = ((sl < 4 ? meta0 : meta1) >> (8 * (sl & 3))) & 0xFFu;
+            const int first = int(tri_base + (meta & 31u)), cnt = int(meta >> 5);
+            for (int k = 0; k < cnt; ++k) {
+                if (STATS) ++st_tris;
+                const float t = tri_hit(r, __ldg(tris + 3 * (first + k)),
+                                        __ldg(tris + 3 * (first + k) + 1),
+                                        __ldg(tris + 3 * (first + k) + 2));
+                if (t < t_best) {
+                    t_best = t;
+                    hit_slot = first + k;
+                    if (ANY_HIT) return hit_slot;
+                }
+            }
+        }
+        // ---- inner children: a new group --------------------------------------------------
+        const uint32_t inner = oct_permute8(hit8 & imask, oct);
+        if (inner) {
+            if (g_hits & 0xFF000000u) stack[sp++] = make_uint2(g_base, g_hits);
+            g_base = child_base;
+            g_hits = (inner << 24) | imask;
+        }
+        // ---- next child: this group's, else a popped one ---------------------------------
+        while (!(g_hits & 0xFF000000u)) {
+            if (sp == 0) {
+                if (STATS) {
+                    atomicAdd(&g_trav_stats[0], st_nodes);
+                    atomicAdd(&g_trav_stats[2], st_tris);
+                    atomicAdd(&g_trav_stats[3], 1ull);
+                }
+                return hit_slot;
+            }
+            const uint2 e = stack[--sp];
+            g_base = e.x;
+            g_hits = e.y;
+        }
+        const uint32_t bit = __ffs(g_hits >> 24) - 1;
+        g_hits &= ~(1u << (bit + 24));
+        const uint32_t slot = bit ^ oct;
+        node = int(g_base + __popc(g_hits & ((1u << slot) - 1u) & 0xFFu));
+    }
+}
+
 template <bool ANY_HIT, int LEAFV = 0, int WIDTH = 2, int STATS = 0>
 __device__ int traverse(const float4 *__restrict__ nodes, const float4 *__restrict__ tris,
                         const Ray &r, float tmax, float &t_best) {
+    if constexpr (WIDTH == 16) return traverse8<ANY_HIT, STATS>(nodes, tris, r, tmax, t_best);
     unsigned long long st_nodes = 0, st_leaves = 0, st_tris = 0;
     // reciprocal direction; tiny components replaced so the slabs stay finite
     const float sx = fabsf(r.dx) < 1e-12f ? copysignf(1e-12f, r.dx) : r.dx;
@@ -257,13 +514,34 @@ __device__ int traverse(const float4 *__restrict__ nodes, const float4 *__restri
                 st_tris += (~node) & 7;
             }
         }
-        if (node >= 0 && (WIDTH == 4 || WIDTH == 5 || WIDTH == 6 || WIDTH >= 8)) {
+        if (node >= 0 && (WIDTH == 3 || WIDTH == 4 || WIDTH == 5 || WIDTH == 6 || WIDTH >= 8)) {
             float d[4];
             int c[4];
             if constexpr (WIDTH == 5) {
                 node4h_hits(nodes, node, ix, iy, iz, oix, oiy, oiz, t_best, d, c);
-            } else if constexpr (WIDTH >= 8) {
+            } else if constexpr (WIDTH >= 8 && WIDTH < 16) {
                 node4o_hits<(WIDTH - 8) & 7>(nodes, node, ix, iy, iz, oix, oiy, oiz, t_best, d, c);
+            } else if constexpr (WIDTH == 18) {
+                node4hs_hits(nodes, node, ix, iy, iz, oix, oiy, oiz, t_best, oct & 1, oct & 2,
+                             oct & 4, d, c);
+            } else if constexpr (WIDTH == 17) {
+#define PS_OCTR_CASE(o) \
+    case o: node4r_hits<o>(nodes, node, ix, iy, iz, oix, oiy, oiz, t_best, d, c); break;
+                switch (oct) {
+                    PS_OCTR_CASE(0) PS_OCTR_CASE(1) PS_OCTR_CASE(2) PS_OCTR_CASE(3)
+                    PS_OCTR_CASE(4) PS_OCTR_CASE(5) PS_OCTR_CASE(6)
+                    default: node4r_hits<7>(nodes, node, ix, iy, iz, oix, oiy, oiz, t_best, d, c);
+                }
+#undef PS_OCTR_CASE
+            } else if constexpr (WIDTH == 3) {
+#define PS_OCTH_CASE(o) \
+    case o: node4ho_hits<o>(nodes, node, ix, iy, iz, oix, oiy, oiz, t_best, d, c); break;
+                switch (oct) {
+                    PS_OCTH_CASE(0) PS_OCTH_CASE(1) PS_OCTH_CASE(2) PS_OCTH_CASE(3)
+                    PS_OCTH_CASE(4) PS_OCTH_CASE(5) PS_OCTH_CASE(6)
+                    default: node4ho_hits<7>(nodes, node, ix, iy, iz, oix, oiy, oiz, t_best, d, c);
+                }
+#undef PS_OCTH_CASE
             } else if constexpr (WIDTH == 6) {
 #define PS_OCT_CASE(o) \
     case o: node4o_hits<o>(nodes, node, ix, iy, iz, oix, oiy, oiz, t_best, d, c); break;

@@ -70,15 +70,24 @@ class Scene:
 
     def device(self, device=None, leaf_size: int = 2, width: int | None = None) -> "DeviceScene":
         """BVH layouts: 2 = BVH2, 4 = BVH4 (fp32 boxes), 5 = BVH4 with fp16
-        boxes (64-byte nodes); default from PS_BVH_WIDTH or BVH4."""
+        boxes (64-byte nodes), 3 = BVH4 with fp16 boxes relative to an fp16
+        node origin and compact child references (64-byte nodes), 8 = BVH8
+        with 8-bit quantised boxes (96-byte nodes); default from
+        PS_BVH_WIDTH or DEFAULT_BVH_WIDTH."""
         import os
 
         if width is None:
             width = int(os.environ.get("PS_BVH_WIDTH", DEFAULT_BVH_WIDTH))
+            if width == 5 and len(self.vertices) and np.abs(self.vertices).max() > FP16_SAFE:
+                width = 4  # fp16 boxes would lose too much precision
         return DeviceScene(self, device, leaf_size, width)
 
 
-DEFAULT_BVH_WIDTH = 4
+# fp16-box BVH4: two 256-bit loads per node instead of four; C4 trace + blend
+# 5.75 -> 5.43 ms (the trace is bound by L1 wavefronts of node fetches).  Scenes
+# with coordinates beyond FP16_SAFE use fp32 boxes (width 4).
+DEFAULT_BVH_WIDTH = 5
+FP16_SAFE = 16384.0
 
 
 class DeviceScene:
@@ -97,15 +106,20 @@ class DeviceScene:
         vp = verts.ctypes.data_as(ctypes.c_void_p)
         N.check(N.lib().ps_bvh_build_wide(vp, len(verts), leaf_size, self.width,
                                           ctypes.byref(sizes), None, None), "ps_bvh_build_wide")
-        nodes = np.zeros(sizes.node_count * (32 if self.width == 4 else 16), np.float32)
+        words = {2: 16, 3: 16, 4: 32, 5: 16, 8: 24}[self.width]
+        nodes = np.zeros(sizes.node_count * words, np.float32)
         tris = np.zeros(sizes.tri_slots * 12, np.float32)
         N.check(N.lib().ps_bvh_build_wide(vp, len(verts), leaf_size, self.width,
                                           ctypes.byref(sizes),
                                           nodes.ctypes.data_as(ctypes.c_void_p),
                                           tris.ctypes.data_as(ctypes.c_void_p)),
                 "ps_bvh_build_wide")
-        # traversal stack: at most (children - 1) pushes per level (64 entries)
-        if (min(self.width, 4) - 1) * sizes.max_depth + 1 > 64:
+        # traversal stack: at most (children - 1) pushes per level (64 entries);
+        # BVH8 pushes at most one node group per level (32 entries)
+        if self.width == 8:
+            if sizes.max_depth > 32:
+                raise ValueError(f"BVH8 depth {sizes.max_depth} exceeds the traversal stack (32)")
+        elif ((2 if self.width == 2 else 4) - 1) * sizes.max_depth + 1 > 64:
             raise ValueError(f"BVH depth {sizes.max_depth} exceeds the traversal stack (64)")
         self.sizes = (int(sizes.node_count), int(sizes.tri_slots), int(sizes.max_depth))
         self.host_nodes, self.host_tris = nodes, tris
