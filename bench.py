@@ -165,6 +165,22 @@ def build_scene(name):
     return S.interior_hall() if name == "hall" else S.cornell_box()
 
 
+def make_config(args, sc, vol, world) -> dict:
+    """The workload description, identical in both arms (ours / reference)."""
+    dims, rays, _ = CONFIGS[args.config]
+    return {
+        "workload": f"config 4: {dims[0]}x{dims[1]}x{dims[2]} probe grid, {rays} rays/probe, "
+                    f"~{sc.triangle_count // 1000}k-triangle interior hall, full-volume update "
+                    "+ change detection + selection + slot assign + build + pack + temporal "
+                    "delta, colour + visibility" if args.config == "c4" else
+                    f"{args.config}: {dims} probes, {rays} rays/probe",
+        "probes": vol.probe_count, "rays_per_probe": rays, "triangles": sc.triangle_count,
+        "lights": len(sc.lights), "shadows": args.shadows,
+        "l2": "per-frame working set (atlases, float state, planes) > 126 MB L2; no flush",
+        "n_gpus_requested": world,
+    }
+
+
 def run_ours(args, rank, world, local):
     import torch
     import torch.distributed as dist
@@ -198,16 +214,21 @@ def run_ours(args, rank, world, local):
     barrier()
     # ---- timed region: K full frames, inputs resident (scene, state), outputs on device
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    outs = (None, None)
     with ClockSampler(local) as clocks:
         barrier()
         start.record(stream)
         for k in range(args.steps):
             f = args.warmup + k
-            server.tick(f, frame_lights(f))
+            outs = server.tick(f, frame_lights(f))
         server.join()  # the last frame's colour / visibility chains run on side streams
         end.record(stream)
         barrier()
     ms = start.elapsed_time(end) / args.steps
+    # probes selected (= entries written) in the last timed frame, per kind:
+    # the full-volume update means every probe, every frame
+    selected = {k: (int(o.entry_count.item()) if o is not None else None)
+                for k, o in zip(("color", "visibility"), outs)}
     ms_max = ms
     if world > 1:
         t = torch.tensor([ms], device=dev)
@@ -239,6 +260,11 @@ def run_ours(args, rank, world, local):
     encode = server.encode_times() if world == 1 else {}
     passes = server.pass_times()  # last: re-running the blend advances the probe state
 
+    peer_ranks = None
+    if world > 1:
+        pb = getattr(getattr(server.impl, "color", None), "_pb", None)
+        if pb is not None:  # peers whose buffers this rank mapped with CUDA IPC
+            peer_ranks = sum(1 for r, p in enumerate(pb.ptrs["flags"]) if r != rank and p)
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -273,20 +299,17 @@ def run_ours(args, rank, world, local):
         "vs_baseline": None,
         "dtype": "f32+u32",
         "data": "synthetic",
-        "config": {
-            "workload": f"config 4: {dims[0]}x{dims[1]}x{dims[2]} probe grid, {rays} rays/probe, "
-                        f"~{sc.triangle_count // 1000}k-triangle interior hall, full-volume update "
-                        "+ change detection + selection + slot assign + build + pack + temporal "
-                        "delta, colour + visibility",
-            "probes": n, "rays_per_probe": rays, "triangles": sc.triangle_count,
-            "lights": len(sc.lights), "shadows": server.impl.updater.shadows
-            if hasattr(server.impl, "updater") else "map",
-            "l2": "per-frame working set (atlases, float state, planes) > 126 MB L2; no flush",
-            "parallelism": f"z-slab x{world}",
+        "config": make_config(args, sc, vol, world),
+        "parallelism": f"z-slab x{world}",
+        "run": {
             "slabs": ([[int(b), int(e)] for b, e in slabs] if slabs and world > 1 else None),
             "rank_trace_blend_ms": rank_trace if world > 1 else None,
             "launch": "eager" if args.eager else "CUDA graphs (trace+blend, one chain per kind)",
+            "exchange": (("peer memory (CUDA IPC over NVLink)" if getattr(server.impl, "peer", False)
+                          else "NCCL") if world > 1 else None),
+            "peer_ranks_mapped": peer_ranks,
         },
+        "selected_last_frame": selected,
         "grays_per_s": round(rays_total / (ms_max / 1e3) / 1e9, 4),
         "frame_hz": round(1e3 / ms_max, 2),
         "stages_ms": {k: round(v, 4) for k, v in stages.items()},
@@ -361,25 +384,37 @@ def run_ours(args, rank, world, local):
 
 
 def cpu_baseline(sc, vol, rays, sample, shadows="map"):
+    """One sampled step of the reference's CPU path (oracle/cpu_frame.py)."""
     from oracle import cpu_frame
 
+    cpu_frame.warm_up(sc)
     r = cpu_frame.time_frame(sc, vol, rays, sample_probes=sample, shadows=shadows)
     return {
-        "value": round(vol.probe_count / r["frame_s"], 3),
+        "value": round(r["probe_updates_per_s"], 4),
         "unit": "probe updates/s",
         "cores": r["threads"],
         "kind": "port",
-        "sample": (f"{r['sample_probes']} probes x {rays} rays traced by the oracle's C restatement "
-                   f"of the reference brute-force raycast (float64, OpenMP on {r['threads']} "
-                   f"threads) + numpy blend, scaled to {vol.probe_count} probes; detect/select/"
-                   f"assign/build/pack/delta by the numpy restatement at full size (1 thread)"),
-        "frame_s": round(r["frame_s"], 3),
+        "sampled": True,
+        "sample": sample_text(r, rays),
+        "wall_s": round(r["wall_s"], 3),
         "detail": {k: (round(v, 6) if isinstance(v, float) else v) for k, v in r.items()},
     }
 
 
+def sample_text(r, rays):
+    return (f"{r['sample_probes']} probes x {rays} rays traced by the oracle's C restatement of "
+            f"the reference brute-force raycast (float64, OpenMP on {r['threads']} threads) + numpy "
+            f"DDGI blend; {r['map_sample_texels']} shadow-map texels by the same query; stages 3-4 "
+            f"on {r['stage_probes']} probes by the {r['stages_impl']} functions (detect_changed, "
+            f"select_for_client, build_update_atlas, pack_texels; temporal delta by the numpy "
+            f"port). value = probes / (probes x measured per-probe cost of each part + measured "
+            f"per-texel shadow-map cost x map texels)")
+
+
 def run_reference(args, rank, world, local):
-    """The reference's CPU path (oracle port) on the host cores."""
+    """The reference's CPU path on the host cores (see oracle/cpu_frame.py):
+    every step is a measured, bounded sample of the frame; ms_per_step is the
+    wall time those steps took, value the per-probe rate they measured."""
     if rank != 0:
         return
     from paper_2103_05875_b200 import scene as S
@@ -388,41 +423,52 @@ def run_reference(args, rank, world, local):
     dims, rays, scene_name = CONFIGS[args.config]
     sc = build_scene(scene_name)
     vol = S.volume_for(sc, dims)
+    cpu_frame.warm_up(sc)
     for w in range(min(args.warmup, 1)):
-        cpu_frame.time_frame(sc, vol, rays, sample_probes=1, stages_full=False, frame=w)
-    times = []
+        cpu_frame.time_frame(sc, vol, rays, sample_probes=1, frame=w, shadows=args.shadows,
+                             stage_probes=dims[0] * dims[1], map_sample=64)
+    steps = []
+    w0 = time.perf_counter()
     for k in range(args.steps):
-        r = cpu_frame.time_frame(sc, vol, rays, sample_probes=args.cpu_sample, frame=k,
-                                 stages_full=(k == 0), rng_seed=k, shadows=args.shadows)
-        times.append(r)
-    stages = times[0]["stages_s"]
-    per_probe = sum(t["trace_shade_s_per_probe"] + t["blend_s_per_probe"] for t in times) / len(times)
-    map_s = sum(t["shadow_map_s"] for t in times) / len(times)
-    frame_s = per_probe * vol.probe_count + map_s + stages
-    value = vol.probe_count / frame_s
+        steps.append(cpu_frame.time_frame(sc, vol, rays, sample_probes=args.cpu_sample, frame=k,
+                                          rng_seed=k, shadows=args.shadows))
+    wall = time.perf_counter() - w0
+    per_probe = sum(1.0 / r["probe_updates_per_s"] for r in steps) / len(steps)
+    value = 1.0 / per_probe
+    r0 = steps[0]
     out = {
-        "metric": METRIC, "value": round(value, 3), "unit": "probe updates/s", "impl": "reference",
+        "metric": METRIC, "value": round(value, 4), "unit": "probe updates/s", "impl": "reference",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(frame_s * 1e3, 1), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64+u32", "data": "synthetic",
-        "config": {"workload": f"config 4 ({dims}, {rays} rays, interior hall) on the host CPU",
-                   "probes": vol.probe_count, "rays_per_probe": rays},
-        "grays_per_s": round(vol.probe_count * rays / frame_s / 1e9, 9),
-        "cpu_baseline": {"value": round(value, 3), "unit": "probe updates/s",
-                         "cores": os.cpu_count(), "kind": "port",
-                         "sample": f"{args.cpu_sample} probes/step traced+blended per step "
-                                   f"(scaled), stages 3-4 at full size once"},
-        "e2e": {"value": round(value, 3), "unit": "probe updates/s", "h2d_bytes_per_step": 0,
+        "ms_per_step": round(wall / args.steps * 1e3, 1), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64+u32", "data": "synthetic",
+        "config": make_config(args, sc, vol, world),
+        "parallelism": f"host CPU, {os.cpu_count()} threads (rank 0 only)",
+        "sampled": True,
+        "note": "ms_per_step is the measured wall time of each sampled step; value is the "
+                "whole-volume rate the step's measured per-probe / per-texel costs give "
+                "(projected frame time per step in detail.frame_s)",
+        "grays_per_s": round(vol.probe_count * rays * value / vol.probe_count / 1e9, 12),
+        "selected_last_frame": r0["selected"],
+        "detail": {"frame_s": [round(r["frame_s"], 1) for r in steps],
+                   "wall_s": [round(r["wall_s"], 3) for r in steps],
+                   "trace_blend_s_per_probe": [round(r["trace_blend_s_per_probe"], 5) for r in steps],
+                   "stages_s": [round(r["stages_s"], 3) for r in steps],
+                   "stages_parts_s": r0["stages_parts_s"],
+                   "shadow_map_frame_s": [round(r["shadow_map_frame_s"], 1) for r in steps]},
+        "cpu_baseline": {"value": round(value, 4), "unit": "probe updates/s",
+                         "cores": os.cpu_count(), "kind": "port", "sampled": True,
+                         "sample": sample_text(r0, rays)},
+        "e2e": {"value": round(value, 4), "unit": "probe updates/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
 
 
 def main():
-    # keep rank 0's stdout to the single JSON line (NCCL prints its version
-    # banner to stdout at init when NCCL_DEBUG asks for it)
-    if os.environ.get("NCCL_DEBUG", "").upper() in ("VERSION", "INFO", "TRACE"):
-        os.environ["NCCL_DEBUG"] = "WARN"
+    # keep rank 0's stdout to the single JSON line: NCCL's debug output
+    # (version banner, communicator lines at NCCL_DEBUG=INFO) goes to stderr
+    if os.environ.get("NCCL_DEBUG") and not os.environ.get("NCCL_DEBUG_FILE"):
+        os.environ["NCCL_DEBUG_FILE"] = "/dev/stderr"
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)

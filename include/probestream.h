@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define PS_ABI_VERSION 7
+#define PS_ABI_VERSION 8
 
 /* status codes */
 #define PS_OK 0
@@ -248,7 +248,13 @@ int ps_import_tiles(int kind, const void *payloads, int64_t payload_stride,
  *     them into last_sent and stamps last_sent_seq for every entry.
  *   ps_peer_signal: stores (value or *value_dev) + add into each *flags[i]
  *     with system-scope release semantics after a system fence;
- *     ps_peer_wait: spins until every flags[i] >= that value (acquire).
+ *     ps_peer_wait: spins until every flags[i] >= that value (acquire); with
+ *     a non-null error word (host-mapped pinned int32) and timeout_ns > 0 the
+ *     spin is bounded: on expiry it stores (flag index + 1) into *error and
+ *     returns, so a dead peer cannot hang the survivors inside a kernel or a
+ *     graph replay.  ps_peer_status returns PS_ERR_CUDA (with the message in
+ *     ps_last_error) once *error is set, PS_OK otherwise; it reads host
+ *     memory only and does not synchronise.
  *   ps_ipc_export / ps_ipc_open: CUDA IPC handle (ps_ipc_handle_bytes bytes)
  *     and offset for any device pointer; opening maps it in this process
  *     (cached per allocation). */
@@ -266,7 +272,8 @@ int ps_export_tiles_peer(int kind, const void *source, int64_t probe_count,
 int ps_peer_signal(int64_t *const *flags, int32_t nflags, int64_t value,
                    const int64_t *value_dev, int64_t add, void *stream);
 int ps_peer_wait(const int64_t *flags, int32_t nflags, int64_t value, const int64_t *value_dev,
-                 int64_t add, void *stream);
+                 int64_t add, int32_t *error, int64_t timeout_ns, void *stream);
+int ps_peer_status(const int32_t *error);
 size_t ps_ipc_handle_bytes(void);
 int ps_ipc_export(const void *ptr, uint8_t *handle, int64_t *offset);
 int ps_ipc_open(const uint8_t *handle, int64_t offset, void **ptr);

@@ -16,7 +16,7 @@ from pathlib import Path
 from .errors import LayoutMismatchError, NativeLibraryError, SlotOverflowError
 
 LIB_PATH = Path(os.environ.get("PROBESTREAM_LIB", Path(__file__).resolve().parent / "libprobestream.so"))
-ABI_VERSION = 7
+ABI_VERSION = 8
 
 PS_OK = 0
 PS_ERR_VALUE = -1
@@ -115,7 +115,8 @@ _SIGNATURES = {
     "ps_export_tiles_peer": (_int, [_int, _vp, _i64, _i64, _vp, _vp, _i64, _i64, _i64, _i64, _vp,
                                     _i64, _vp, _vp, _i64, _vp, _vp]),
     "ps_peer_signal": (_int, [_vp, _i32, _i64, _vp, _i64, _vp]),
-    "ps_peer_wait": (_int, [_vp, _i32, _i64, _vp, _i64, _vp]),
+    "ps_peer_wait": (_int, [_vp, _i32, _i64, _vp, _i64, _vp, _i64, _vp]),
+    "ps_peer_status": (_int, [_vp]),
     "ps_ipc_handle_bytes": (_sz, []),
     "ps_ipc_export": (_int, [_vp, _vp, _vp]),
     "ps_ipc_open": (_int, [_vp, _i64, _vp]),

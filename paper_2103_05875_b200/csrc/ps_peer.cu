@@ -68,11 +68,34 @@ __global__ void peer_signal_kernel(int64_t *const *flags, int n, int64_t value,
     for (int i = threadIdx.x; i < n; i += blockDim.x) st_release_sys(flags[i], v);
 }
 
+__device__ __forceinline__ uint64_t global_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Bounded acquire spin.  A peer that never signals (crashed rank, lost
+// process) would otherwise hang every GPU inside this kernel -- inside graph
+// replays too, where no host watchdog sees it.  After timeout_ns the waiter
+// records (flag index + 1) in *error (host-mapped pinned memory, read by
+// ps_peer_status without a synchronisation) and returns; the host raises
+// PS_ERR_CUDA at its next check.
 __global__ void peer_wait_kernel(const int64_t *flags, int n, int64_t value,
-                                 const int64_t *value_dev, int64_t add) {
+                                 const int64_t *value_dev, int64_t add, int32_t *error,
+                                 int64_t timeout_ns) {
     const int64_t v = (value_dev ? *value_dev : value) + add;
-    for (int i = threadIdx.x; i < n; i += blockDim.x)
-        while (ld_acquire_sys(flags + i) < v) __nanosleep(64);
+    const uint64_t t0 = global_ns();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        uint32_t spins = 0;
+        while (ld_acquire_sys(flags + i) < v) {
+            __nanosleep(64);
+            if (error && timeout_ns > 0 && (++spins & 1023) == 0 &&
+                int64_t(global_ns() - t0) > timeout_ns) {
+                atomicCAS(error, 0, i + 1);
+                break;
+            }
+        }
+    }
     __threadfence_system();
 }
 
@@ -137,11 +160,22 @@ int ps_peer_signal(int64_t *const *flags, int32_t nflags, int64_t value,
 }
 
 int ps_peer_wait(const int64_t *flags, int32_t nflags, int64_t value, const int64_t *value_dev,
-                 int64_t add, void *stream) {
+                 int64_t add, int32_t *error, int64_t timeout_ns, void *stream) {
     PS_ABI_BEGIN
     if (!flags || nflags < 1) fail(PS_ERR_VALUE, "no flags to wait on");
-    peer_wait_kernel<<<1, 32, 0, as_stream(stream)>>>(flags, nflags, value, value_dev, add);
+    peer_wait_kernel<<<1, 32, 0, as_stream(stream)>>>(flags, nflags, value, value_dev, add, error,
+                                                      timeout_ns);
     check_launch("peer_wait_kernel");
+    PS_ABI_END
+}
+
+int ps_peer_status(const int32_t *error) {
+    PS_ABI_BEGIN
+    if (!error) fail(PS_ERR_VALUE, "null error word");
+    const int32_t e = *reinterpret_cast<const volatile int32_t *>(error);
+    if (e != 0)
+        fail(PS_ERR_CUDA, "peer exchange timed out: rank flag " + std::to_string(e - 1) +
+                              " was never signalled (a peer rank stopped or crashed)");
     PS_ABI_END
 }
 

@@ -45,6 +45,36 @@ from .server import CHAIN_PRIORITY, DEFAULT_GOP, RESERVE_SMS, KindOutput
 from .volume import AtlasKind, ProbeAtlas
 
 
+def _peer_timeout_ns() -> int:
+    return int(float(os.environ.get("PS_PEER_TIMEOUT_S", "30")) * 1e9)
+
+
+_PEER_ERR: dict = {}
+
+
+def peer_error_word(device) -> torch.Tensor:
+    """The host-mapped pinned int32 that the bounded peer waits of this
+    process report a timeout into (one per device; 0 = healthy)."""
+    idx = torch.device(device).index
+    w = _PEER_ERR.get(idx)
+    if w is None:
+        w = _PEER_ERR[idx] = torch.zeros(1, dtype=torch.int32, pin_memory=True)
+    return w
+
+
+def check_peers() -> None:
+    """Raise (RuntimeError, PS_ERR_CUDA) if any peer wait of this process gave
+    up on a rank that never signalled.  Reads pinned host memory only."""
+    for w in _PEER_ERR.values():
+        N.call("ps_peer_status", w.data_ptr())
+
+
+def peer_wait(flags_ptr: int, nflags: int, seq: int, seq_dev_ptr, device, stream) -> None:
+    """ps_peer_wait bounded by PS_PEER_TIMEOUT_S (default 30 s)."""
+    N.call("ps_peer_wait", flags_ptr, nflags, int(seq), seq_dev_ptr, 1,
+           peer_error_word(device).data_ptr(), _peer_timeout_ns(), stream)
+
+
 def _env_flag(name: str, default: bool) -> bool:
     v = os.environ.get(name)
     return default if v is None else v not in ("0", "false", "no", "")
@@ -276,7 +306,7 @@ class DistKindStream:
         self._mark(f"{tag}.detect", 1)
         self._mark(f"{tag}.exchange_bits", 0)
         N.call("ps_peer_signal", self.sig_bits.data_ptr(), world, int(seq), D.ptr(seq_dev), 1, st)
-        N.call("ps_peer_wait", self.flags.data_ptr(), world, int(seq), D.ptr(seq_dev), 1, st)
+        peer_wait(self.flags.data_ptr(), world, seq, D.ptr(seq_dev), dev, st)
         self._mark(f"{tag}.exchange_bits", 1)
         self._mark(f"{tag}.select", 0)
         select_device(self.bits2[k], pvs_bits, vol, self.last_sent_seq, seq, self.budget,
@@ -297,8 +327,7 @@ class DistKindStream:
         self._mark(f"{tag}.gather", 0)
         N.call("ps_peer_signal", self.sig_export.data_ptr(), 1, int(seq), D.ptr(seq_dev), 1, st)
         if self.is_encoder:
-            N.call("ps_peer_wait", self.flags[1].data_ptr(), world, int(seq), D.ptr(seq_dev), 1,
-                   st)
+            peer_wait(self.flags[1].data_ptr(), world, seq, D.ptr(seq_dev), dev, st)
         self._mark(f"{tag}.gather", 1)
         if self.is_encoder:
             key = self.frame_count % self.gop_length == 0
@@ -511,6 +540,7 @@ class DistributedFrame:
 
     def tick(self, frame=None, lights=None, pvs_bits=None):
         frame = self.seq if frame is None else frame
+        check_peers()
         main = torch.cuda.current_stream(self.device)
         if self.overlap:
             buf = self.updater.frames_done % 2
@@ -551,6 +581,7 @@ class DistributedFrame:
         main = torch.cuda.current_stream(self.device)
         for ev in self._pending:
             main.wait_event(ev)
+        check_peers()
 
     def output_stream(self, kind: str):
         return self.streams[kind] if self.overlap else torch.cuda.current_stream(self.device)

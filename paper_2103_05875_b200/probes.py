@@ -330,7 +330,9 @@ class ProbeUpdater:
             N.call("ps_trace_blend", ctypes.byref(params), stream)
         seq = sp["state"][0:1]
         N.call("ps_peer_signal", sp["sig"].data_ptr(), world, 0, seq.data_ptr(), 1, stream)
-        N.call("ps_peer_wait", sp["flags"].data_ptr(), world, 0, seq.data_ptr(), 1, stream)
+        from .distributed import peer_wait
+
+        peer_wait(sp["flags"].data_ptr(), world, 0, seq.data_ptr(), self.device, stream)
         params = self._params(hysteresis, passes=6, shadow_maps=sp["maps2"][k])
         N.call("ps_trace_blend", ctypes.byref(params), stream)
 

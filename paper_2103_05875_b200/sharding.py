@@ -2,12 +2,15 @@
 
 Probe id = i + nx*(j + ny*k) (volume.py:72-74), so a z-slab is a contiguous
 ascending id range: rank r traces, blends and change-detects its slab only
-(scene replicated).  The only exchange the path has is the change bitmap
-(16 KB at 131,072 probes), all-gathered over NCCL so every rank runs the
-same global selection and slot assignment (twin-replay determinism,
-test_packing.py:235-240); then each rank exports the core tiles of its own
-selected probes and the encoder rank (0) gathers them into the single update
-atlas it packs (the "single encoder stream" of the north star).
+(scene replicated).  The path has two exchanges per texture kind, both over
+peer memory by default (distributed.py, csrc/ps_peer.cu): the change bitmap
+(16 KB at 131,072 probes), ORed by every rank's detect kernel straight into
+every rank's bitmap, so all ranks run the same global selection and slot
+assignment (twin-replay determinism, test_packing.py:235-240); and the
+selected cores, which each rank's export kernel writes straight into the
+encoder rank's (0) update atlas, the single one it packs (the "single
+encoder stream" of the north star).  PS_PEER=0 selects the NCCL path
+(all-reduce of the bitmaps, send/recv of per-rank payloads).
 """
 
 from __future__ import annotations
