@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define PS_ABI_VERSION 8
+#define PS_ABI_VERSION 9
 
 /* status codes */
 #define PS_OK 0
@@ -203,6 +203,21 @@ int ps_assign_slots(const int64_t *selected, const int64_t *n_dev, int64_t n_hos
                     int32_t *slot_probe, int64_t *last_selected, int64_t *meta,
                     int64_t *entries, int64_t *entry_count, uint32_t *status_dev,
                     void *workspace, size_t workspace_bytes, void *stream);
+
+/* The same state machine straight from a selection BITMAP (bit p = probe p
+ * selected; ANDed with pvs_bits when non-NULL), for slot_count >=
+ * probe_count, where no eviction is reachable: two single-pass kernels
+ * (decoupled look-back scans) instead of ps_assign_slots' id-list chain.
+ * Writes probe_slot / slot_probe / last_selected / meta exactly as
+ * ps_assign_slots, entries + entry_count, plan int64[8] (the per-call plan:
+ * selected, new, taken-free, 0, 0, old used, tick) and, when non-NULL,
+ * *sel_count.  PS_ERR_VALUE when slot_count < probe_count. */
+size_t ps_assign_bits_workspace_bytes(int64_t probe_count, int64_t slot_count);
+int ps_assign_slots_bits(const uint32_t *sel_bits, const uint32_t *pvs_bits, int64_t probe_count,
+                         int64_t slot_count, int32_t *probe_slot, int32_t *slot_probe,
+                         int64_t *last_selected, int64_t *meta, int64_t *entries,
+                         int64_t *entry_count, int64_t *plan, int64_t *sel_count,
+                         void *workspace, size_t workspace_bytes, void *stream);
 
 /* Copy each entry's stripped core (block[1:-1,1:-1]) into its slot region of
  * update_texels (packing.py:335-337).  Optional commit: when

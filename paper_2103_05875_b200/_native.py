@@ -16,7 +16,7 @@ from pathlib import Path
 from .errors import LayoutMismatchError, NativeLibraryError, SlotOverflowError
 
 LIB_PATH = Path(os.environ.get("PROBESTREAM_LIB", Path(__file__).resolve().parent / "libprobestream.so"))
-ABI_VERSION = 8
+ABI_VERSION = 9
 
 PS_OK = 0
 PS_ERR_VALUE = -1
@@ -101,6 +101,9 @@ _SIGNATURES = {
     "ps_select": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _int, _i64, _int, _vp, _vp, _vp, _sz,
                          _vp]),
     "ps_assign_workspace_bytes": (_sz, [_i64, _i64]),
+    "ps_assign_bits_workspace_bytes": (_sz, [_i64, _i64]),
+    "ps_assign_slots_bits": (_int, [_vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                    _vp, _vp, _sz, _vp]),
     "ps_assign_slots": (_int, [_vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp,
                                _vp, _vp, _sz, _vp]),
     "ps_build_update": (_int, [_int, _vp, _i64, _i64, _vp, _vp, _i64, _i64, _vp, _i64, _vp,

@@ -220,10 +220,21 @@ __global__ void __launch_bounds__(256) shadow_map_kernel(ps_trace_params prm) {
 // grid of sms - reserve CTAs leaves whole SMs free (a grid of 256-thread CTAs
 // would be spread over every SM and leave only fragments, too small for NCCL's
 // kernels).  The kernel is per-warp, so the block size is free.
+// CLAIM > 0: chunks are claimed per CTA in blocks of CLAIM consecutive tasks
+// (one probe tile x CLAIM consecutive directions of the Morton-ordered ray
+// set): the CTA's warps trace neighbouring directions from the same origins
+// at the same time, so their node fetches share the SM's L1.  A CTA-shared
+// 64-bit word holds (block << 32 | next); the warp that draws next == CLAIM
+// fetches the CTA's next block from the global counter.
 template <int SHADOW, int LEAFV, int MINB, int PROBE_PARALLEL, int WIDTH, int TPB = THREADS,
-          int STATS = 0>
+          int STATS = 0, int CLAIM = 0>
 __global__ void __launch_bounds__(TPB, TPB == THREADS ? MINB : (TPB == 1024 ? 1 : 2))
     trace_kernel(ps_trace_params prm) {
+    __shared__ unsigned long long s_claim;
+    if (CLAIM > 0) {
+        if (threadIdx.x == 0) s_claim = CLAIM;  // block 0 "exhausted": first claim fetches
+        __syncthreads();
+    }
     const float4 *nodes = reinterpret_cast<const float4 *>(prm.nodes);
     const float4 *tris = reinterpret_cast<const float4 *>(prm.tris);
     const float4 *dirs = reinterpret_cast<const float4 *>(prm.ray_dirs);
@@ -257,7 +268,26 @@ __global__ void __launch_bounds__(TPB, TPB == THREADS ? MINB : (TPB == 1024 ? 1 
     float4 *records = reinterpret_cast<float4 *>(prm.records);
     while (true) {
         uint32_t task = 0;
-        if (lane == 0) task = atomicAdd(prm.work_counter, 1u);
+        if (lane == 0) {
+            if (CLAIM > 0) {
+                while (true) {
+                    const unsigned long long old = atomicAdd(&s_claim, 1ull);
+                    const uint32_t idx = uint32_t(old);
+                    if (idx < uint32_t(CLAIM)) {
+                        task = uint32_t(old >> 32) * CLAIM + idx;
+                        break;
+                    }
+                    if (idx == uint32_t(CLAIM)) {
+                        const uint32_t nb = atomicAdd(prm.work_counter, 1u);
+                        atomicExch(&s_claim, (unsigned long long)nb << 32);
+                    } else {
+                        __nanosleep(64);
+                    }
+                }
+            } else {
+                task = atomicAdd(prm.work_counter, 1u);
+            }
+        }
         task = __shfl_sync(0xffffffffu, task, 0);
         if (int64_t(task) >= total_chunks) break;
         int64_t q;
@@ -734,7 +764,7 @@ void launch_trace_t(const ps_trace_params &p, int sms, cudaStream_t s, bool sm_s
 
 // two 640-thread CTAs per SM (40 warps at <= 48 registers) on all but the
 // reserved SMs
-template <int SHADOW, int LEAFV, int PP, int WIDTH>
+template <int SHADOW, int LEAFV, int PP, int WIDTH, int CLAIM = 0>
 void launch_trace_640(const ps_trace_params &p, int sms, cudaStream_t s) {
     static const int carve = [] {  // tuning knob: L1 / shared-memory carveout (percent)
         const char *e = getenv("PS_L1_CARVE");
@@ -742,12 +772,12 @@ void launch_trace_640(const ps_trace_params &p, int sms, cudaStream_t s) {
     }();
     static bool set = false;
     if (carve >= 0 && !set) {
-        check_cuda(cudaFuncSetAttribute(trace_kernel<SHADOW, LEAFV, 1, PP, WIDTH, 640>,
+        check_cuda(cudaFuncSetAttribute(trace_kernel<SHADOW, LEAFV, 1, PP, WIDTH, 640, 0, CLAIM>,
                                         cudaFuncAttributePreferredSharedMemoryCarveout, carve),
                    "carveout");
         set = true;
     }
-    trace_kernel<SHADOW, LEAFV, 1, PP, WIDTH, 640><<<2 * sms, 640, 0, s>>>(p);
+    trace_kernel<SHADOW, LEAFV, 1, PP, WIDTH, 640, 0, CLAIM><<<2 * sms, 640, 0, s>>>(p);
 }
 
 template <int SHADOW, int MINB>
@@ -787,12 +817,22 @@ void launch_trace_s(const ps_trace_params &p, int variant, int sms, cudaStream_t
             case 11: launch_trace_t<SHADOW, 1, 4, 0, 5>(p, sms, s, big); break;
             case 12: launch_trace_t<SHADOW, 1, 1, 0, 5>(p, sms, s, big); break;
             // fp16 boxes, octant tests, two 256-bit loads per node
-            case 64: launch_trace_640<SHADOW, 0, 4, 3>(p, sms, s); break;
+            case 64: launch_trace_640<SHADOW, 0, 4, 19>(p, sms, s); break;  // 2x4x4 tiles
+            case 86: launch_trace_640<SHADOW, 0, 4, 3>(p, sms, s); break;
             case 70: launch_trace_640<SHADOW, 0, 12, 18>(p, sms, s); break;  // word selects
             case 71: launch_trace_t<SHADOW, 0, 1, 12, 3>(p, sms, s, true); break;  // 1024 x 1
             case 72: launch_trace_640<SHADOW, 1, 12, 3>(p, sms, s); break;  // leaf pairs
-            case 65: launch_trace_640<SHADOW, 0, 2, 3>(p, sms, s); break;
-            default: launch_trace_640<SHADOW, 0, 12, 3>(p, sms, s); break;
+            case 65: launch_trace_640<SHADOW, 0, 2, 19>(p, sms, s); break;  // 4x4x2 tiles
+            case 87: launch_trace_640<SHADOW, 0, 2, 3>(p, sms, s); break;
+            // CTA-level claiming: one tile x CLAIM neighbouring directions
+            case 80: launch_trace_640<SHADOW, 0, 12, 3, 16>(p, sms, s); break;
+            case 81: launch_trace_640<SHADOW, 0, 12, 3, 32>(p, sms, s); break;
+            case 82: launch_trace_640<SHADOW, 0, 12, 3, 64>(p, sms, s); break;
+            case 83: launch_trace_640<SHADOW, 0, 12, 3, 256>(p, sms, s); break;
+            // speculative while-while traversal (parked leaves, warp vote)
+            case 84: launch_trace_640<SHADOW, 0, 12, 19>(p, sms, s); break;
+            case 85: launch_trace_640<SHADOW, 0, 12, 3>(p, sms, s); break;  // plain loop
+            default: launch_trace_640<SHADOW, 0, 12, 19>(p, sms, s); break;
         }
         return;
     }
@@ -942,8 +982,10 @@ int ps_trace_blend(const ps_trace_params *params, void *stream) {
             shadow_map_kernel<17><<<blocks, 256, 0, s>>>(p);
         else if (p.bvh_width == 8)
             shadow_map_kernel<16><<<blocks, 256, 0, s>>>(p);
-        else if (p.bvh_width == 5)
+        else if (p.bvh_width == 5 && getenv("PS_SHADOW_PLAIN"))
             shadow_map_kernel<3><<<blocks, 256, 0, s>>>(p);
+        else if (p.bvh_width == 5)  // speculative while-while traversal (traverse_spec)
+            shadow_map_kernel<19><<<blocks, 256, 0, s>>>(p);
         else if (p.bvh_width == 4)
             shadow_map_kernel<6><<<blocks, 256, 0, s>>>(p);  // octant-specialised BVH4 tests
         else

@@ -477,10 +477,100 @@ __device__ int traverse8(const float4 *__restrict__ nodes, const float4 *__restr
     }
 }
 
+// fp16-box BVH4 node test (node4ho_hits) dispatched on the ray octant
+__device__ __forceinline__ void node4ho_switch(const float4 *nodes, int node, int oct, float ix,
+                                               float iy, float iz, float oix, float oiy, float oiz,
+                                               float tmax, float d[4], int c[4]) {
+#define PS_OCTS_CASE(o) \
+    case o: node4ho_hits<o>(nodes, node, ix, iy, iz, oix, oiy, oiz, tmax, d, c); break;
+    switch (oct) {
+        PS_OCTS_CASE(0) PS_OCTS_CASE(1) PS_OCTS_CASE(2) PS_OCTS_CASE(3)
+        PS_OCTS_CASE(4) PS_OCTS_CASE(5) PS_OCTS_CASE(6)
+        default: node4ho_hits<7>(nodes, node, ix, iy, iz, oix, oiy, oiz, tmax, d, c);
+    }
+#undef PS_OCTS_CASE
+}
+
+// Speculative while-while traversal (Aila & Laine 2009) over the fp16-box
+// BVH4: a lane that reaches a leaf parks it and keeps walking inner nodes
+// until every lane still in the loop holds a leaf (warp vote), then the
+// warp tests the parked leaves together -- node tests and triangle tests
+// run in converged phases instead of interleaving partial warps.  Same
+// nearest hit as traverse<..., 3>: a parked leaf is tested later than in the
+// plain loop, so pops cull against a t_best that can only be larger (stale),
+// never smaller -- no subtree holding the nearest hit is skipped.
+constexpr int TRAV_DONE = -1;  // leaf refs are ~(first << 3 | count), count >= 1: <= -2
+
+template <bool ANY_HIT>
+__device__ int traverse_spec(const float4 *__restrict__ nodes, const float4 *__restrict__ tris,
+                             const Ray &r, float tmax, float &t_best) {
+    const float sx = fabsf(r.dx) < 1e-12f ? copysignf(1e-12f, r.dx) : r.dx;
+    const float sy = fabsf(r.dy) < 1e-12f ? copysignf(1e-12f, r.dy) : r.dy;
+    const float sz = fabsf(r.dz) < 1e-12f ? copysignf(1e-12f, r.dz) : r.dz;
+    const int oct = (sx < 0.0f ? 1 : 0) | (sy < 0.0f ? 2 : 0) | (sz < 0.0f ? 4 : 0);
+    const float ix = 1.0f / sx, iy = 1.0f / sy, iz = 1.0f / sz;
+    const float oix = r.ox * ix, oiy = r.oy * iy, oiz = r.oz * iz;
+    int2 stack[STACK];
+    int sp = 0;
+    int node = 0, leaf = 0;  // leaf: parked leaf ref (0 = none)
+    int hit_slot = -1;
+    t_best = tmax;
+    auto pop = [&]() -> int {
+        while (sp > 0) {
+            const int2 e = stack[--sp];
+            if (__int_as_float(e.y) <= t_best) return e.x;
+        }
+        return TRAV_DONE;
+    };
+    while (node != TRAV_DONE || leaf != 0) {
+        // ---- inner nodes until every lane holds a leaf (or is done) -------------------
+        while (node >= 0) {
+            float d[4];
+            int c[4];
+            node4ho_switch(nodes, node, oct, ix, iy, iz, oix, oiy, oiz, t_best, d, c);
+            if (d[0] != INFINITY) {
+                if (d[3] != INFINITY) stack[sp++] = make_int2(c[3], __float_as_int(d[3]));
+                if (d[2] != INFINITY) stack[sp++] = make_int2(c[2], __float_as_int(d[2]));
+                if (d[1] != INFINITY) stack[sp++] = make_int2(c[1], __float_as_int(d[1]));
+                node = c[0];
+            } else {
+                node = pop();
+            }
+            if (node < TRAV_DONE && leaf == 0) {  // park the leaf, keep walking
+                leaf = node;
+                node = pop();
+            }
+            if (__all_sync(__activemask(), leaf != 0)) break;
+        }
+        // ---- parked (and directly reached) leaves ----------------------------------------
+        while (leaf != 0) {
+            const int ref = ~leaf;
+            const int first = ref >> 3, cnt = ref & 7;
+            for (int k = 0; k < cnt; ++k) {
+                const float t = tri_hit(r, __ldg(tris + 3 * (first + k)),
+                                        __ldg(tris + 3 * (first + k) + 1),
+                                        __ldg(tris + 3 * (first + k) + 2));
+                if (t < t_best) {
+                    t_best = t;
+                    hit_slot = first + k;
+                    if (ANY_HIT) return hit_slot;
+                }
+            }
+            leaf = 0;
+            if (node < TRAV_DONE) {  // the walk stopped on another leaf
+                leaf = node;
+                node = pop();
+            }
+        }
+    }
+    return hit_slot;
+}
+
 template <bool ANY_HIT, int LEAFV = 0, int WIDTH = 2, int STATS = 0>
 __device__ int traverse(const float4 *__restrict__ nodes, const float4 *__restrict__ tris,
                         const Ray &r, float tmax, float &t_best) {
     if constexpr (WIDTH == 16) return traverse8<ANY_HIT, STATS>(nodes, tris, r, tmax, t_best);
+    if constexpr (WIDTH == 19) return traverse_spec<ANY_HIT>(nodes, tris, r, tmax, t_best);
     unsigned long long st_nodes = 0, st_leaves = 0, st_tris = 0;
     // reciprocal direction; tiny components replaced so the slabs stay finite
     const float sx = fabsf(r.dx) < 1e-12f ? copysignf(1e-12f, r.dx) : r.dx;

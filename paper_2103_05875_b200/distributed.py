@@ -308,15 +308,8 @@ class DistKindStream:
         N.call("ps_peer_signal", self.sig_bits.data_ptr(), world, int(seq), D.ptr(seq_dev), 1, st)
         peer_wait(self.flags.data_ptr(), world, seq, D.ptr(seq_dev), dev, st)
         self._mark(f"{tag}.exchange_bits", 1)
-        self._mark(f"{tag}.select", 0)
-        select_device(self.bits2[k], pvs_bits, vol, self.last_sent_seq, seq, self.budget,
-                      out_ids=self.sel_ids, out_count=self.sel_count,
-                      workspace_slot=self.ws_select, ordered=False, active=self.active)
+        entries, count = self._select_assign(self.bits2[k], pvs_bits, seq)
         self.bits2[k].zero_()  # ready for frame + 2 (peers write it only after our next flag)
-        self._mark(f"{tag}.select", 1)
-        self._mark(f"{tag}.assign", 0)
-        entries, count = self.layout.assign_device(self.sel_ids, self.sel_count)
-        self._mark(f"{tag}.assign", 1)
         self._mark(f"{tag}.export", 0)
         N.call("ps_export_tiles_peer", self.kind.native, src.texels.data_ptr(), vol.probe_count,
                src.probes_per_row, entries.data_ptr(), count.data_ptr(), self.layout.slot_count,
@@ -337,6 +330,26 @@ class DistKindStream:
             pack_delta(self.update_texels, self.kind, prev, planes_out=cur,
                        residual=self.residual, skip=self.skip, key_dev=key_dev)
             self._mark(f"{tag}.pack_delta", 1)
+
+    def _select_assign(self, bits, pvs_bits, seq: int):
+        """Global selection + slot assignment, replicated on every rank.
+        Without a budget the selection is the candidate bitmap itself and the
+        slot cache assigns straight from it (ps_assign_slots_bits)."""
+        tag = self.kind.value
+        if self.budget is None and self.layout.slot_count >= self.volume.probe_count:
+            self._mark(f"{tag}.assign", 0)
+            out = self.layout.assign_bits_device(bits, pvs_bits)
+            self._mark(f"{tag}.assign", 1)
+            return out
+        self._mark(f"{tag}.select", 0)
+        select_device(bits, pvs_bits, self.volume, self.last_sent_seq, seq, self.budget,
+                      out_ids=self.sel_ids, out_count=self.sel_count,
+                      workspace_slot=self.ws_select, ordered=False, active=self.active)
+        self._mark(f"{tag}.select", 1)
+        self._mark(f"{tag}.assign", 0)
+        out = self.layout.assign_device(self.sel_ids, self.sel_count)
+        self._mark(f"{tag}.assign", 1)
+        return out
 
     def _tick_peer(self, rendered: ProbeAtlas, seq: int, pvs_bits=None):
         graphed = self.graphs is not None and self.frame_count >= 1 and self.timers is None
@@ -422,14 +435,7 @@ class DistKindStream:
             self._mark(f"{tag}.detect", 1)
 
         def seg_select_export():
-            self._mark(f"{tag}.select", 0)
-            select_device(self.bits, pvs_bits, self.volume, self.last_sent_seq, seq, self.budget,
-                          out_ids=self.sel_ids, out_count=self.sel_count,
-                          workspace_slot=self.ws_select, ordered=False, active=self.active)
-            self._mark(f"{tag}.select", 1)
-            self._mark(f"{tag}.assign", 0)
-            entries, count = self.layout.assign_device(self.sel_ids, self.sel_count)
-            self._mark(f"{tag}.assign", 1)
+            entries, count = self._select_assign(self.bits, pvs_bits, seq)
             self._mark(f"{tag}.export", 0)
             N.call("ps_export_tiles", self.kind.native, rendered.texels.data_ptr(),
                    self.volume.probe_count, rendered.probes_per_row, entries.data_ptr(),

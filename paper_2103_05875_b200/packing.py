@@ -350,6 +350,31 @@ class UpdateAtlasLayout:
                D.stream_ptr(self.device))
         return self._entries, self._entry_count
 
+    def assign_bits_device(self, sel_bits: torch.Tensor, pvs_bits: torch.Tensor | None = None):
+        """Stream-ordered assign of the probes whose bit is set in ``sel_bits``
+        (int32 words over the layout's probe capacity, ANDed with ``pvs_bits``
+        when given) -- the same state machine as ``assign`` in two kernels
+        (ps_assign_slots_bits), for layouts with a slot per probe
+        (slot_count >= probe capacity: no eviction is reachable).  Returns
+        (entries, entry_count) device tensors; no host synchronisation."""
+        n = self._cap
+        if n == 0:
+            raise ValueError("layout has no probe capacity; pass probe_count")
+        if self.slot_count < n:
+            raise ValueError("assign_bits_device needs slot_count >= probe capacity; "
+                             "use assign_device")
+        if getattr(self, "_ws_bits", None) is None:
+            lib = N.lib()
+            self._ws_bits = D.workspace(lib.ps_assign_bits_workspace_bytes(n, self.slot_count),
+                                        self.device)
+            self._plan = torch.zeros(8, dtype=torch.int64, device=self.device)
+        N.call("ps_assign_slots_bits", sel_bits.data_ptr(), D.ptr(pvs_bits), n, self.slot_count,
+               self._probe_slot.data_ptr(), self._slot_probe.data_ptr(),
+               self._last_selected.data_ptr(), self._meta.data_ptr(), self._entries.data_ptr(),
+               self._entry_count.data_ptr(), self._plan.data_ptr(), None,
+               self._ws_bits.data_ptr(), self._ws_bits.numel(), D.stream_ptr(self.device))
+        return self._entries, self._entry_count
+
     def raise_pending(self) -> None:
         st = int(self._status.item()) if self._status is not None else 0
         if st:

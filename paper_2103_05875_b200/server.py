@@ -156,14 +156,22 @@ class KindStream:
                               bits=self.bits, with_ids=False, workspace_slot=self.ws_detect,
                               active=self.active)
         self._mark(f"{tag}.detect", 1)
-        self._mark(f"{tag}.select", 0)
-        select_device(self.bits, pvs_bits, self.volume, self.last_sent_seq, seq, self.budget,
-                      out_ids=self.sel_ids, out_count=self.sel_count,
-                      workspace_slot=self.ws_select, ordered=False, active=self.active)
-        self._mark(f"{tag}.select", 1)
-        self._mark(f"{tag}.assign", 0)
-        entries, count = self.layout.assign_device(self.sel_ids, self.sel_count)
-        self._mark(f"{tag}.assign", 1)
+        if self.budget is None and self.layout.slot_count >= self.volume.probe_count:
+            # no budget: the selection is the candidate set (changed & pvs &
+            # active, detect applied active), so it stays a bitmap and the
+            # slot cache assigns straight from it (ps_assign_slots_bits)
+            self._mark(f"{tag}.assign", 0)
+            entries, count = self.layout.assign_bits_device(self.bits, pvs_bits)
+            self._mark(f"{tag}.assign", 1)
+        else:
+            self._mark(f"{tag}.select", 0)
+            select_device(self.bits, pvs_bits, self.volume, self.last_sent_seq, seq, self.budget,
+                          out_ids=self.sel_ids, out_count=self.sel_count,
+                          workspace_slot=self.ws_select, ordered=False, active=self.active)
+            self._mark(f"{tag}.select", 1)
+            self._mark(f"{tag}.assign", 0)
+            entries, count = self.layout.assign_device(self.sel_ids, self.sel_count)
+            self._mark(f"{tag}.assign", 1)
         self._mark(f"{tag}.build", 0)
         N.call("ps_build_update", self.kind.native, rendered.texels.data_ptr(),
                self.volume.probe_count, rendered.probes_per_row, entries.data_ptr(),

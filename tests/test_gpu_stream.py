@@ -349,3 +349,54 @@ def test_slot_random_sequences_vs_oracle(ps, slots, n):
         sel = rng.choice(n, size=k, replace=False)
         assert dev_layout.assign(torch.from_numpy(sel).to(DEV)) == ref.assign(sel), step
     assert dev_layout.probe_slot == ref.probe_slot
+
+
+def _bits_of(ids, n):
+    words = np.zeros((n + 31) // 32, np.uint32)
+    for p in ids:
+        words[p >> 5] |= np.uint32(1) << np.uint32(p & 31)
+    return torch.from_numpy(words.view(np.int32)).to(DEV)
+
+
+@pytest.mark.parametrize("n,slots", [(1, 1), (37, 37), (5000, 5000), (20000, 24000),
+                                     (131072, 131072)])
+def test_assign_bits_vs_oracle(ps, n, slots):
+    """ps_assign_slots_bits (bitmap in, two look-back kernels) == the reference
+    slot cache (packing.py:283-305) == ps_assign_slots on the same sequence:
+    entries, probe_slot, slot_probe, last_selected and the tick, with and
+    without a PVS mask, across tile boundaries (8192 probes per tile)."""
+    _, packing, _, _ = ps
+    rng = np.random.default_rng(n + slots)
+    a = packing.UpdateAtlasLayout(slots, 8, probe_count=n)
+    b = packing.UpdateAtlasLayout(slots, 8, probe_count=n)
+    ref = so.SlotCache(slots, 8)
+    steps = 6 if n < 100000 else 3
+    for step in range(steps):
+        frac = [1.0, 0.3, 0.0, 0.9, 0.01, 1.0][step]
+        sel = np.flatnonzero(rng.random(n) < frac)
+        pvs = None
+        if step == 3:
+            pv = np.flatnonzero(rng.random(n) < 0.5)
+            pvs = _bits_of(pv, n)
+            sel_eff = np.intersect1d(sel, pv)
+        else:
+            sel_eff = sel
+        entries, count = a.assign_bits_device(_bits_of(sel, n), pvs)
+        got = [tuple(r) for r in entries[: int(count.item())].cpu().tolist()]
+        want = ref.assign(sel_eff)
+        assert got == [tuple(map(int, e)) for e in want], step
+        assert b.assign(torch.from_numpy(sel_eff).to(DEV)) == got, step
+        assert torch.equal(a._probe_slot, b._probe_slot)
+        assert torch.equal(a._slot_probe, b._slot_probe)
+        assert torch.equal(a._last_selected, b._last_selected)
+        assert torch.equal(a._meta[:2], b._meta[:2])
+        plan = a._plan.cpu().tolist()
+        assert plan[0] == len(sel_eff) and plan[6] == step + 1
+    assert a.probe_slot == ref.probe_slot
+
+
+def test_assign_bits_needs_a_slot_per_probe(ps):
+    _, packing, _, _ = ps
+    layout = packing.UpdateAtlasLayout(10, 8, probe_count=20)
+    with pytest.raises(ValueError):
+        layout.assign_bits_device(_bits_of([1, 2], 20))
