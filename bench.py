@@ -305,7 +305,8 @@ def run_ours(args, rank, world, local):
             "slabs": ([[int(b), int(e)] for b, e in slabs] if slabs and world > 1 else None),
             "rank_trace_blend_ms": rank_trace if world > 1 else None,
             "launch": "eager" if args.eager else "CUDA graphs (trace+blend, one chain per kind)",
-            "exchange": (("peer memory (CUDA IPC over NVLink)" if getattr(server.impl, "peer", False)
+            "exchange": (("peer memory (CUDA IPC over NVLink)"
+                          if getattr(getattr(server.impl, "color", None), "peer", False)
                           else "NCCL") if world > 1 else None),
             "peer_ranks_mapped": peer_ranks,
         },
