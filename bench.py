@@ -140,6 +140,21 @@ def profile_metric(prefix: str, key: str):
     return None
 
 
+def trace_issue_profile():
+    """Warp instructions per C4 trace launch and the capture they come from
+    (profiles/trace_accounting_*.json, newest round first), or None."""
+    for p in sorted((ROOT / "profiles").glob("trace_accounting_r*.json"), reverse=True):
+        try:
+            d = json.loads(p.read_text())
+            return {"warp_inst_per_launch": d["totals"]["warp_inst"],
+                    "thread_inst_per_ray": d["per_ray"]["thread_inst"],
+                    "simt_efficiency": d["simt_efficiency"], "source": f"profiles/{p.name}",
+                    "kernel": d["kernel"]}
+        except Exception:
+            continue
+    return None
+
+
 def profile_traffic(prefix: str):
     """DRAM bytes (read + write) per launch, summed over the kernels whose name
     starts with `prefix` (one launch per texture kind), from the committed
@@ -157,6 +172,33 @@ def profile_traffic(prefix: str):
 
 
 # --------------------------------------------------------------------------------------------
+
+
+def trace_roofline(trace_ms, rays_total, world, clocks) -> dict:
+    """The trace is issue-bound (no HBM / tensor roofline): its bound is the
+    SM issue rate, 148 SMs x 4 schedulers x 1 warp instruction per clock.
+    achieved = the warp instructions one launch executes (ncu capture of the
+    same kernel, profiles/trace_accounting_*.json; divided by the ranks for a
+    slab) / the live CUDA-event time of the launch."""
+    out = {"kernel": "trace_kernel (probe rays, this rank's slab; CUDA events, pass alone)",
+           "ms": round(trace_ms, 4),
+           "rays_per_s": round(rays_total / world / (trace_ms / 1e3), 1),
+           "bound": "issue"}
+    prof = trace_issue_profile()
+    mhz = (clocks.summary() or {}).get("sm_mhz") or 1965
+    if prof:
+        import torch
+
+        sms = torch.cuda.get_device_properties(0).multi_processor_count
+        peak = sms * 4 * mhz * 1e6  # warp instructions / s
+        achieved = prof["warp_inst_per_launch"] / world / (trace_ms / 1e3)
+        out.update({"achieved": round(achieved / 1e9, 1), "peak": round(peak / 1e9, 1),
+                    "unit": "G warp-inst/s", "frac": round(achieved / peak, 4),
+                    "warp_inst_per_launch": int(prof["warp_inst_per_launch"] / world),
+                    "thread_inst_per_ray": prof["thread_inst_per_ray"],
+                    "simt_efficiency": prof["simt_efficiency"],
+                    "profile": prof["source"], "profiled_kernel": prof["kernel"]})
+    return out
 
 
 def build_scene(name):
@@ -327,17 +369,7 @@ def run_ours(args, rank, world, local):
             "traffic": traffic,
             "algorithmic_bytes_per_launch": pk,
         },
-        "roofline_trace": {
-            "kernel": "trace_kernel (probe rays, this rank's slab; CUDA events, pass alone)",
-            "ms": round(passes["trace"], 4),
-            "rays_per_s": round(rays_total / world / (passes["trace"] / 1e3), 1),
-            "l1_data_pipe_frac": profile_metric("trace_kernel", "l1_pct"),
-            "sm_frac": profile_metric("trace_kernel", "sm_pct"),
-            "note": "BVH traversal on SIMT cores has no dense roofline: bound by L1 "
-                    "data-pipe wavefronts of divergent node fetches (fractions from "
-                    "profiles/ncu_summary.json); 10.7 inner nodes, 1.07 leaves, 2.1 "
-                    "triangle tests per ray (tools/trav_stats.py)",
-        },
+        "roofline_trace": trace_roofline(passes["trace"], rays_total, world, clocks),
         "roofline_blend": {
             "bound": "tensor",
             "kernel": "blend_tc_kernel (tcgen05.mma kind::tf32, this rank's slab)",
@@ -377,11 +409,81 @@ def run_ours(args, rank, world, local):
         "gpu_launches_per_step": launches_per_step,
         "kernels": kernel_names,
     }
+    if world == 1:
+        # the reference-facing drop-in (numpy in / numpy out), not in the step
+        out["dropin_numpy"] = dropin_numpy(dims)
     if world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(sc, vol, rays, args.cpu_sample, args.shadows)
+        parts = out["cpu_baseline"]["detail"].get("stages_parts_s", {})
+        for kind in ("color", "visibility"):
+            if kind in parts and kind in out["dropin_numpy"]:
+                ref_ms = 1e3 * sum(v for k, v in parts[kind].items() if k != "delta")
+                out["dropin_numpy"][kind]["reference_ms"] = round(ref_ms, 1)
+                out["dropin_numpy"][kind]["speedup"] = round(
+                    ref_ms / out["dropin_numpy"][kind]["ms"], 1)
     print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def _reference_package():
+    """The reference ``probestream`` from $PROBESTREAM_REF or baseline/_ref
+    (the offline install that travels to the GPU box), or None."""
+    import importlib
+
+    for c in (os.environ.get("PROBESTREAM_REF"), str(ROOT / "baseline" / "_ref")):
+        if c and (Path(c) / "probestream" / "__init__.py").exists():
+            if c not in sys.path:
+                sys.path.insert(0, c)
+            try:
+                mod = importlib.import_module("probestream")
+                importlib.import_module("probestream.volume")
+                return mod
+            except Exception:
+                return None
+    return None
+
+
+def dropin_numpy(dims, reps: int = 3) -> dict:
+    """The INTEGRATION.md §1 swap as a reference caller sees it: numpy atlases
+    in the reference's own ProbeVolume / ProbeAtlas objects (baseline/_ref;
+    this package's mirrors when absent) through this package's
+    detect_changed -> select_for_client -> build_update_atlas -> pack_texels,
+    every probe changed, at the bench volume.  Wall time per kind (best of
+    ``reps``), host <-> device staging of the numpy arrays included."""
+    import numpy as np
+    import torch
+
+    from paper_2103_05875_b200 import packing, selection
+    from paper_2103_05875_b200 import volume as V_ours
+
+    ref = _reference_package()
+    V = ref.volume if ref is not None else V_ours
+    n = dims[0] * dims[1] * dims[2]
+    vol = V.ProbeVolume(tuple(dims))
+    rng = np.random.default_rng(0)
+    out = {"objects": "reference probestream (baseline/_ref)" if ref is not None
+           else "package mirrors (reference not importable)", "probes": n}
+    for K in (V.AtlasKind.COLOR, V.AtlasKind.VISIBILITY):
+        a = V.ProbeAtlas(K, n)
+        dt = a.texels.dtype
+        cur = rng.integers(0, 2**16, size=a.texels.shape, dtype=dt)
+        rendered, last = V.ProbeAtlas(K, n, a.probes_per_row, cur), V.ProbeAtlas(
+            K, n, a.probes_per_row, cur ^ dt.type(1))
+        best = None
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            changed = selection.detect_changed(rendered, last, vol)
+            sel = selection.select_for_client(changed, changed, vol, np.zeros(n, np.int64), 1)
+            layout = packing.UpdateAtlasLayout(n, K.core_side)
+            upd, entries = packing.build_update_atlas(sel, layout, rendered)
+            planes = packing.pack_texels(upd, K)
+            t = time.perf_counter() - t0
+            best = t if best is None else min(best, t)
+        assert len(entries) == n and isinstance(planes.data, np.ndarray)
+        out[K.value] = {"ms": round(best * 1e3, 2), "selected": len(sel)}
+    return out
 
 
 def cpu_baseline(sc, vol, rays, sample, shadows="map"):

@@ -10,6 +10,8 @@
 // rows, and every byte is read once and written once (HBM-bound).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+#include <algorithm>
 #include <mutex>
 #include <string>
 
@@ -401,6 +403,158 @@ __global__ void __launch_bounds__(TILE_X *TILE_Y)
     }
 }
 
+// Visibility planes with misaligned rows, as a flat byte array per plane: a
+// thread owns one 16-byte-aligned word of every plane (the same flat offset
+// in all three), so every plane / residual store and previous-plane load is
+// one aligned 16-byte access -- no funnel shifts, no partial stores.  Needs
+// planes whose size h * pw is a multiple of 16 (update atlases: h is a
+// multiple of 16).  A word covers plane columns [x0, x0 + 16) of one row,
+// or the tail of row r and the head of row r + 1.
+//
+// The word's stream window: plane column x needs stream byte 3x + e, i.e.
+// texel (3x + e) >> 2, byte ((3x + e) & 3) ^ 1 of the little-endian texel
+// word (stream order R.hi R.lo G.hi G.lo).  With c = 3 * x0 mod 16 the 16
+// texels from (3 * x0 - c) / 4 (one aligned 64-byte window) hold every stream
+// byte of the word, and c is the same for every word of a row, so the byte
+// gather is a compile-time PRMT pattern chosen by a row-uniform switch on c.
+template <int C, int E, int J>
+__device__ __forceinline__ uint32_t vis_word(const uint32_t (&t)[16]) {
+    // output bytes i = 4J + p, p = 0..3 -> stream byte k = C + 3i + E
+    constexpr int k0 = C + 3 * (4 * J) + E;
+    constexpr int ta = k0 >> 2;
+    // selectors for the first permute over (t[ta], t[ta + 1]) and the second
+    // over (that result, t[ta + 2]); bytes of t[ta + 2] come in through the second
+    constexpr auto tex = [](int p) { return (C + 3 * (4 * J + p) + E) >> 2; };
+    constexpr auto byt = [](int p) { return ((C + 3 * (4 * J + p) + E) & 3) ^ 1; };
+    constexpr uint32_t s1 = ((tex(0) - ta < 2 ? (tex(0) - ta) * 4 + byt(0) : 0) << 0) |
+                            ((tex(1) - ta < 2 ? (tex(1) - ta) * 4 + byt(1) : 0) << 4) |
+                            ((tex(2) - ta < 2 ? (tex(2) - ta) * 4 + byt(2) : 0) << 8) |
+                            ((tex(3) - ta < 2 ? (tex(3) - ta) * 4 + byt(3) : 0) << 12);
+    constexpr uint32_t s2 = ((tex(0) - ta < 2 ? 0 : 4 + byt(0)) << 0) |
+                            ((tex(1) - ta < 2 ? 1 : 4 + byt(1)) << 4) |
+                            ((tex(2) - ta < 2 ? 2 : 4 + byt(2)) << 8) |
+                            ((tex(3) - ta < 2 ? 3 : 4 + byt(3)) << 12);
+    const uint32_t w01 = __byte_perm(t[ta], t[ta + 1 < 16 ? ta + 1 : 15], s1);
+    if constexpr (tex(3) - ta < 2) return w01;
+    else return __byte_perm(w01, t[ta + 2 < 16 ? ta + 2 : 15], s2);
+}
+
+template <int C>
+__device__ __forceinline__ void vis_words(const uint32_t (&t)[16], uint32_t (&o)[3][4]) {
+#define PS_VW(E, J) o[E][J] = vis_word<C, E, J>(t);
+    PS_VW(0, 0) PS_VW(0, 1) PS_VW(0, 2) PS_VW(0, 3)
+    PS_VW(1, 0) PS_VW(1, 1) PS_VW(1, 2) PS_VW(1, 3)
+    PS_VW(2, 0) PS_VW(2, 1) PS_VW(2, 2) PS_VW(2, 3)
+#undef PS_VW
+}
+
+// the 16 plane bytes (3 planes) of row r, columns [x0, x0 + 16); x0 may be
+// negative (the head of a straddling word), texels outside the row read as 0
+__device__ __forceinline__ void vis_segment(const PackArgs &a, int64_t r, int64_t x0,
+                                            uint32_t (&o)[3][4]) {
+    const int64_t s0 = 3 * x0;
+    const int c = int(((s0 % 16) + 16) % 16);
+    const int64_t t0 = (s0 - c) / 4;  // multiple of 4 texels
+    const uint8_t *row = a.texels + r * a.row_stride_b;
+    uint32_t t[16];
+    if (a.vec_in && t0 >= 0 && t0 + 16 <= a.w) {
+        const uint4 *p = reinterpret_cast<const uint4 *>(row + t0 * 4);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const uint4 q = __ldg(p + i);
+            t[4 * i] = q.x;
+            t[4 * i + 1] = q.y;
+            t[4 * i + 2] = q.z;
+            t[4 * i + 3] = q.w;
+        }
+    } else {
+        const uint32_t *p = reinterpret_cast<const uint32_t *>(row);
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+            t[i] = (t0 + i >= 0 && t0 + i < a.w) ? __ldg(p + t0 + i) : 0u;
+    }
+    switch (c) {
+#define PS_VC(C) case C: vis_words<C>(t, o); break;
+        PS_VC(0) PS_VC(1) PS_VC(2) PS_VC(3) PS_VC(4) PS_VC(5) PS_VC(6) PS_VC(7)
+        PS_VC(8) PS_VC(9) PS_VC(10) PS_VC(11) PS_VC(12) PS_VC(13) PS_VC(14)
+        default: vis_words<15>(t, o);
+#undef PS_VC
+    }
+}
+
+// bytes [lo, hi) of a 16-byte word as a 4 x 32-bit lane mask
+__device__ __forceinline__ uint32_t byte_mask_word(int j, int lo, int hi) {
+    uint32_t m = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) m |= (4 * j + b >= lo && 4 * j + b < hi) ? (0xFFu << (8 * b)) : 0u;
+    return m;
+}
+
+__global__ void __launch_bounds__(256) pack_delta_vis_flat_kernel(PackArgs a) {
+    const bool key = a.key_dev && *a.key_dev;
+    const uint8_t *prev = key ? nullptr : a.prev;
+    const int64_t T = a.h * a.pw;  // bytes per plane, multiple of 16
+    const int64_t nwords = T / 16;
+    const int64_t nby = (a.h + TILE_Y - 1) / TILE_Y;
+    for (int64_t W = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; W < nwords;
+         W += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t f0 = 16 * W;
+        const int64_t r = f0 / a.pw, x0 = f0 - r * a.pw;
+        const int n1 = int(a.pw - x0 < 16 ? a.pw - x0 : 16);  // bytes in row r
+        uint32_t o[3][4];
+        vis_segment(a, r, x0, o);
+        if (n1 < 16) {  // the word runs into row r + 1: its columns [0, 16 - n1)
+            uint32_t o2[3][4];
+            vis_segment(a, r + 1, -int64_t(n1), o2);  // byte i <- column i - n1
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t m = byte_mask_word(j, 0, n1);
+#pragma unroll
+                for (int e = 0; e < 3; ++e) o[e][j] = (o[e][j] & m) | (o2[e][j] & ~m);
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < 3; ++e) {
+            const int64_t off = e * T + f0;
+            uint4 *dst = reinterpret_cast<uint4 *>(a.cur + off);
+            *dst = make_uint4(o[e][0], o[e][1], o[e][2], o[e][3]);
+            if (!a.skip && !a.residual) continue;
+            uint32_t d[4] = {o[e][0], o[e][1], o[e][2], o[e][3]};
+            if (prev) {
+                const uint4 pv = __ldg(reinterpret_cast<const uint4 *>(prev + off));
+                const uint32_t pw4[4] = {pv.x, pv.y, pv.z, pv.w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) d[j] = o[e][j] ^ pw4[j];
+                if (a.residual)
+                    *reinterpret_cast<uint4 *>(a.residual + off) =
+                        make_uint4(__vsub4(o[e][0], pw4[0]), __vsub4(o[e][1], pw4[1]),
+                                   __vsub4(o[e][2], pw4[2]), __vsub4(o[e][3], pw4[3]));
+            } else if (a.residual) {
+                *reinterpret_cast<uint4 *>(a.residual + off) =
+                    make_uint4(o[e][0], o[e][1], o[e][2], o[e][3]);
+            }
+            if (!a.skip) continue;
+            // SKIP (pre-set to 1 when prev exists): a changed byte clears its block;
+            // key frames clear every block the word touches
+            auto clear = [&](int64_t rr, int64_t xa, int lo, int hi) {
+                // bytes [lo, hi) of the word are row rr, columns xa + (b - lo)
+                const int64_t bxa = xa / 16, bxb = (xa + (hi - lo) - 1) / 16;
+                for (int64_t bx = bxa; bx <= bxb; ++bx) {
+                    const int blo = lo + int(bx * 16 - xa > 0 ? bx * 16 - xa : 0);
+                    const int bhi = lo + int((bx + 1) * 16 - xa < hi - lo ? (bx + 1) * 16 - xa
+                                                                          : hi - lo);
+                    bool dirty = !prev;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) dirty |= (d[j] & byte_mask_word(j, blo, bhi)) != 0u;
+                    if (dirty) a.skip[(int64_t(e) * nby + rr / TILE_Y) * a.nseg + bx] = 0;
+                }
+            };
+            clear(r, x0, 0, n1);
+            if (n1 < 16 && r + 1 < a.h) clear(r + 1, 0, n1, 16);
+        }
+    }
+}
+
 // Generic temporal delta over already-packed planes (elements of 1 or 2 B).
 template <int EB>
 __global__ void __launch_bounds__(TILE_X *TILE_Y)
@@ -495,9 +649,20 @@ int launch_pack_delta(int kind, const void *texels, int64_t h, int64_t w, int64_
     const bool rows_misaligned = kind == PS_KIND_VISIBILITY && !a.vec_out && a.vec_in &&
                                  aligned16(planes_cur) && (!planes_prev || aligned16(planes_prev)) &&
                                  (!residual || aligned16(residual));
-    if (kind == PS_KIND_COLOR)
+    static const bool funnel = getenv("PS_PACK_FUNNEL") != nullptr;  // tuning: old path
+    const bool flat = rows_misaligned && !funnel && (h * a.pw) % 16 == 0 && a.vec_in;
+    if (kind == PS_KIND_COLOR) {
         pack_delta_kernel<PS_KIND_COLOR><<<grid, block, 0, stream>>>(a);
-    else if (rows_misaligned)
+    } else if (flat) {
+        if (skip) {  // SKIP starts at 1 (block identical) and changed bytes clear it
+            const int64_t nby = ceil_div(h, TILE_Y);
+            check_cuda(cudaMemsetAsync(skip, 1, size_t(3 * nby * a.nseg), stream), "memset skip");
+        }
+        const int64_t words = h * a.pw / 16;
+        const unsigned blocks = unsigned(std::max<int64_t>(
+            1, std::min<int64_t>(ceil_div(words, 256), int64_t(sm_count()) * 16)));
+        pack_delta_vis_flat_kernel<<<blocks, 256, 0, stream>>>(a);
+    } else if (rows_misaligned)
         pack_delta_vis_unaligned_kernel<<<grid, block, 0, stream>>>(a);
     else
         pack_delta_kernel<PS_KIND_VISIBILITY><<<grid, block, 0, stream>>>(a);

@@ -831,6 +831,9 @@ void launch_trace_s(const ps_trace_params &p, int variant, int sms, cudaStream_t
             case 83: launch_trace_640<SHADOW, 0, 12, 3, 256>(p, sms, s); break;
             // speculative while-while traversal (parked leaves, warp vote)
             case 84: launch_trace_640<SHADOW, 0, 12, 19>(p, sms, s); break;
+            case 88: launch_trace_640<SHADOW, 0, 12, 20>(p, sms, s); break;  // word selects
+            case 89: launch_trace_640<SHADOW, 0, 12, 21>(p, sms, s); break;  // vote >= 3/4
+            case 91: launch_trace_640<SHADOW, 0, 12, 22>(p, sms, s); break;  // vote >= 1/2
             case 85: launch_trace_640<SHADOW, 0, 12, 3>(p, sms, s); break;  // plain loop
             default: launch_trace_640<SHADOW, 0, 12, 19>(p, sms, s); break;
         }

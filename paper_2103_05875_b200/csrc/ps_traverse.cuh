@@ -501,7 +501,10 @@ __device__ __forceinline__ void node4ho_switch(const float4 *nodes, int node, in
 // never smaller -- no subtree holding the nearest hit is skipped.
 constexpr int TRAV_DONE = -1;  // leaf refs are ~(first << 3 | count), count >= 1: <= -2
 
-template <bool ANY_HIT>
+// SEL: node test with per-axis word selects (node4hs_hits) instead of the
+// octant switch; VOTE: leave the node phase when all (0), >= 3/4 (1) or >= 1/2
+// (2) of the lanes still walking hold a parked leaf
+template <bool ANY_HIT, int SEL = 0, int VOTE = 0>
 __device__ int traverse_spec(const float4 *__restrict__ nodes, const float4 *__restrict__ tris,
                              const Ray &r, float tmax, float &t_best) {
     const float sx = fabsf(r.dx) < 1e-12f ? copysignf(1e-12f, r.dx) : r.dx;
@@ -527,7 +530,11 @@ __device__ int traverse_spec(const float4 *__restrict__ nodes, const float4 *__r
         while (node >= 0) {
             float d[4];
             int c[4];
-            node4ho_switch(nodes, node, oct, ix, iy, iz, oix, oiy, oiz, t_best, d, c);
+            if (SEL)
+                node4hs_hits(nodes, node, ix, iy, iz, oix, oiy, oiz, t_best, oct & 1, oct & 2,
+                             oct & 4, d, c);
+            else
+                node4ho_switch(nodes, node, oct, ix, iy, iz, oix, oiy, oiz, t_best, d, c);
             if (d[0] != INFINITY) {
                 if (d[3] != INFINITY) stack[sp++] = make_int2(c[3], __float_as_int(d[3]));
                 if (d[2] != INFINITY) stack[sp++] = make_int2(c[2], __float_as_int(d[2]));
@@ -540,7 +547,13 @@ __device__ int traverse_spec(const float4 *__restrict__ nodes, const float4 *__r
                 leaf = node;
                 node = pop();
             }
-            if (__all_sync(__activemask(), leaf != 0)) break;
+            if (VOTE == 0) {
+                if (__all_sync(__activemask(), leaf != 0)) break;
+            } else {
+                const unsigned m = __activemask();
+                const int parked = __popc(__ballot_sync(m, leaf != 0));
+                if (parked * (VOTE == 1 ? 4 : 2) >= __popc(m) * (VOTE == 1 ? 3 : 1)) break;
+            }
         }
         // ---- parked (and directly reached) leaves ----------------------------------------
         while (leaf != 0) {
@@ -571,6 +584,9 @@ __device__ int traverse(const float4 *__restrict__ nodes, const float4 *__restri
                         const Ray &r, float tmax, float &t_best) {
     if constexpr (WIDTH == 16) return traverse8<ANY_HIT, STATS>(nodes, tris, r, tmax, t_best);
     if constexpr (WIDTH == 19) return traverse_spec<ANY_HIT>(nodes, tris, r, tmax, t_best);
+    if constexpr (WIDTH == 20) return traverse_spec<ANY_HIT, 1>(nodes, tris, r, tmax, t_best);
+    if constexpr (WIDTH == 21) return traverse_spec<ANY_HIT, 0, 1>(nodes, tris, r, tmax, t_best);
+    if constexpr (WIDTH == 22) return traverse_spec<ANY_HIT, 0, 2>(nodes, tris, r, tmax, t_best);
     unsigned long long st_nodes = 0, st_leaves = 0, st_tris = 0;
     // reciprocal direction; tiny components replaced so the slabs stay finite
     const float sx = fabsf(r.dx) < 1e-12f ? copysignf(1e-12f, r.dx) : r.dx;

@@ -150,6 +150,38 @@ def test_pack_delta_matches_pack_then_delta(ps, kind, slots):
     assert not skip0.cpu().numpy().any()
 
 
+@pytest.mark.parametrize("slots", [17, 363, 4096, 16384])
+def test_pack_delta_sparse_skip_unaligned_rows(ps, slots):
+    """Visibility planes with rows that are not 16-byte aligned (the flat
+    16-byte-word kernel): a handful of changed texels, so the SKIP map is
+    mostly 1 and every cleared block is pinned -- including blocks reached
+    only through a word that straddles two plane rows."""
+    _, _, _, delta = ps
+    rng = np.random.default_rng(slots + 7)
+    spr = math.ceil(math.sqrt(slots))
+    rows = math.ceil(slots / spr)
+    shape = (rows * 16, spr * 16, 2)
+    prev_tex = rng.integers(0, 2**16, size=shape, dtype=np.uint16)
+    cur_tex = prev_tex.copy()
+    h, w = shape[0], shape[1]
+    pw = (4 * w + 2) // 3
+    # texels at the ends of rows (straddling words) plus random ones
+    for r in rng.choice(h, size=min(h, 12), replace=False):
+        cur_tex[r, w - 1, rng.integers(0, 2)] ^= np.uint16(1 << int(rng.integers(0, 16)))
+        cur_tex[r, 0, rng.integers(0, 2)] ^= np.uint16(1 << int(rng.integers(0, 16)))
+    for _ in range(20):
+        cur_tex[rng.integers(0, h), rng.integers(0, w), rng.integers(0, 2)] ^= np.uint16(0x8000)
+    prev_planes = so.pack_texels(prev_tex, "visibility")
+    want_planes = so.pack_texels(cur_tex, "visibility")
+    want_res, want_skip = so.temporal_delta(want_planes, prev_planes)
+    assert (pw * 1) % 16 != 0 and want_skip.mean() > 0.5
+    planes, res, skip = delta.pack_delta(torch.from_numpy(cur_tex).to(DEV), "visibility",
+                                         torch.from_numpy(prev_planes).to(DEV))
+    assert np.array_equal(planes.cpu().numpy(), want_planes)
+    assert np.array_equal(res.cpu().numpy(), want_res)
+    assert np.array_equal(skip.cpu().numpy(), want_skip)
+
+
 # --- detect -----------------------------------------------------------------------------
 
 
