@@ -48,7 +48,10 @@ def load_reference():
     """The reference ``probestream`` package from $PROBESTREAM_REF or
     ``baseline/_ref``, or None (never reads /root/reference at run time)."""
     if "probestream" in sys.modules:
-        return sys.modules["probestream"]
+        mod = sys.modules["probestream"]
+        for sub in ("volume", "selection", "packing"):
+            importlib.import_module(f"probestream.{sub}")
+        return mod
     cands = [os.environ.get("PROBESTREAM_REF"), str(ROOT / "baseline" / "_ref")]
     for c in cands:
         if c and (Path(c) / "probestream" / "__init__.py").exists():

@@ -408,8 +408,8 @@ __global__ void __launch_bounds__(TILE_X *TILE_Y)
 // in all three), so every plane / residual store and previous-plane load is
 // one aligned 16-byte access -- no funnel shifts, no partial stores.  Needs
 // planes whose size h * pw is a multiple of 16 (update atlases: h is a
-// multiple of 16).  A word covers plane columns [x0, x0 + 16) of one row,
-// or the tail of row r and the head of row r + 1.
+// multiple of 16) at least 16 bytes wide.  A word covers plane columns
+// [x0, x0 + 16) of one row, or the tail of row r and the head of row r + 1.
 //
 // The word's stream window: plane column x needs stream byte 3x + e, i.e.
 // texel (3x + e) >> 2, byte ((3x + e) & 3) ^ 1 of the little-endian texel
@@ -419,24 +419,23 @@ __global__ void __launch_bounds__(TILE_X *TILE_Y)
 // gather is a compile-time PRMT pattern chosen by a row-uniform switch on c.
 template <int C, int E, int J>
 __device__ __forceinline__ uint32_t vis_word(const uint32_t (&t)[16]) {
-    // output bytes i = 4J + p, p = 0..3 -> stream byte k = C + 3i + E
-    constexpr int k0 = C + 3 * (4 * J) + E;
-    constexpr int ta = k0 >> 2;
-    // selectors for the first permute over (t[ta], t[ta + 1]) and the second
-    // over (that result, t[ta + 2]); bytes of t[ta + 2] come in through the second
+    // output bytes i = 4J + p, p = 0..3 <- stream byte k = C + 3i + E, i.e. byte
+    // (k & 3) ^ 1 of texel k >> 2; the four bytes span up to four texels
+    // ta..ta+3, gathered by up to three permutes: (t[ta], t[ta+1]), then the
+    // result with t[ta+2], then with t[ta+3]
     constexpr auto tex = [](int p) { return (C + 3 * (4 * J + p) + E) >> 2; };
     constexpr auto byt = [](int p) { return ((C + 3 * (4 * J + p) + E) & 3) ^ 1; };
-    constexpr uint32_t s1 = ((tex(0) - ta < 2 ? (tex(0) - ta) * 4 + byt(0) : 0) << 0) |
-                            ((tex(1) - ta < 2 ? (tex(1) - ta) * 4 + byt(1) : 0) << 4) |
-                            ((tex(2) - ta < 2 ? (tex(2) - ta) * 4 + byt(2) : 0) << 8) |
-                            ((tex(3) - ta < 2 ? (tex(3) - ta) * 4 + byt(3) : 0) << 12);
-    constexpr uint32_t s2 = ((tex(0) - ta < 2 ? 0 : 4 + byt(0)) << 0) |
-                            ((tex(1) - ta < 2 ? 1 : 4 + byt(1)) << 4) |
-                            ((tex(2) - ta < 2 ? 2 : 4 + byt(2)) << 8) |
-                            ((tex(3) - ta < 2 ? 3 : 4 + byt(3)) << 12);
-    const uint32_t w01 = __byte_perm(t[ta], t[ta + 1 < 16 ? ta + 1 : 15], s1);
-    if constexpr (tex(3) - ta < 2) return w01;
-    else return __byte_perm(w01, t[ta + 2 < 16 ? ta + 2 : 15], s2);
+    constexpr int ta = tex(0);
+    constexpr auto sel1 = [](int p) { return tex(p) - tex(0) < 2 ? (tex(p) - tex(0)) * 4 + byt(p) : 0; };
+    constexpr auto sel2 = [](int p) { return tex(p) - tex(0) == 2 ? 4 + byt(p) : p; };
+    constexpr auto sel3 = [](int p) { return tex(p) - tex(0) == 3 ? 4 + byt(p) : p; };
+    constexpr uint32_t s1 = sel1(0) | (sel1(1) << 4) | (sel1(2) << 8) | (sel1(3) << 12);
+    constexpr uint32_t s2 = sel2(0) | (sel2(1) << 4) | (sel2(2) << 8) | (sel2(3) << 12);
+    constexpr uint32_t s3 = sel3(0) | (sel3(1) << 4) | (sel3(2) << 8) | (sel3(3) << 12);
+    uint32_t v = __byte_perm(t[ta], t[ta + 1 < 16 ? ta + 1 : 15], s1);
+    if constexpr (tex(3) - ta >= 2) v = __byte_perm(v, t[ta + 2 < 16 ? ta + 2 : 15], s2);
+    if constexpr (tex(3) - ta >= 3) v = __byte_perm(v, t[ta + 3 < 16 ? ta + 3 : 15], s3);
+    return v;
 }
 
 template <int C>
@@ -450,15 +449,15 @@ __device__ __forceinline__ void vis_words(const uint32_t (&t)[16], uint32_t (&o)
 
 // the 16 plane bytes (3 planes) of row r, columns [x0, x0 + 16); x0 may be
 // negative (the head of a straddling word), texels outside the row read as 0
-__device__ __forceinline__ void vis_segment(const PackArgs &a, int64_t r, int64_t x0,
+__device__ __forceinline__ void vis_segment(const PackArgs &a, int r, int x0,
                                             uint32_t (&o)[3][4]) {
-    const int64_t s0 = 3 * x0;
-    const int c = int(((s0 % 16) + 16) % 16);
-    const int64_t t0 = (s0 - c) / 4;  // multiple of 4 texels
-    const uint8_t *row = a.texels + r * a.row_stride_b;
+    const int s0 = 3 * x0;
+    const int c = s0 & 15;         // 3 * x0 mod 16, also for negative x0
+    const int t0 = (s0 - c) >> 2;  // multiple of 4 texels (16 bytes)
+    const uint8_t *row = a.texels + int64_t(r) * a.row_stride_b;
     uint32_t t[16];
-    if (a.vec_in && t0 >= 0 && t0 + 16 <= a.w) {
-        const uint4 *p = reinterpret_cast<const uint4 *>(row + t0 * 4);
+    if (t0 >= 0 && t0 + 16 <= int(a.w)) {  // rows are 16-byte aligned (vec_in)
+        const uint4 *p = reinterpret_cast<const uint4 *>(row + 4 * t0);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const uint4 q = __ldg(p + i);
@@ -471,7 +470,7 @@ __device__ __forceinline__ void vis_segment(const PackArgs &a, int64_t r, int64_
         const uint32_t *p = reinterpret_cast<const uint32_t *>(row);
 #pragma unroll
         for (int i = 0; i < 16; ++i)
-            t[i] = (t0 + i >= 0 && t0 + i < a.w) ? __ldg(p + t0 + i) : 0u;
+            t[i] = (t0 + i >= 0 && t0 + i < int(a.w)) ? __ldg(p + t0 + i) : 0u;
     }
     switch (c) {
 #define PS_VC(C) case C: vis_words<C>(t, o); break;
@@ -493,19 +492,21 @@ __device__ __forceinline__ uint32_t byte_mask_word(int j, int lo, int hi) {
 __global__ void __launch_bounds__(256) pack_delta_vis_flat_kernel(PackArgs a) {
     const bool key = a.key_dev && *a.key_dev;
     const uint8_t *prev = key ? nullptr : a.prev;
-    const int64_t T = a.h * a.pw;  // bytes per plane, multiple of 16
-    const int64_t nwords = T / 16;
-    const int64_t nby = (a.h + TILE_Y - 1) / TILE_Y;
-    for (int64_t W = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; W < nwords;
-         W += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t f0 = 16 * W;
-        const int64_t r = f0 / a.pw, x0 = f0 - r * a.pw;
-        const int n1 = int(a.pw - x0 < 16 ? a.pw - x0 : 16);  // bytes in row r
+    // 32-bit offsets: the launcher routes planes of >= 2^31 bytes elsewhere
+    const uint32_t pw = uint32_t(a.pw), h = uint32_t(a.h);
+    const uint32_t T = h * pw;  // bytes per plane, multiple of 16
+    const uint32_t nwords = T / 16;
+    const uint32_t nby = (h + TILE_Y - 1) / TILE_Y, nseg = uint32_t(a.nseg);
+    for (uint32_t W = blockIdx.x * blockDim.x + threadIdx.x; W < nwords;
+         W += gridDim.x * blockDim.x) {
+        const uint32_t f0 = 16 * W;
+        const uint32_t r = f0 / pw, x0 = f0 - r * pw;
+        const int n1 = int(pw - x0 < 16 ? pw - x0 : 16);  // bytes in row r
         uint32_t o[3][4];
-        vis_segment(a, r, x0, o);
+        vis_segment(a, int(r), int(x0), o);
         if (n1 < 16) {  // the word runs into row r + 1: its columns [0, 16 - n1)
             uint32_t o2[3][4];
-            vis_segment(a, r + 1, -int64_t(n1), o2);  // byte i <- column i - n1
+            vis_segment(a, int(r) + 1, -n1, o2);  // byte i <- column i - n1
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const uint32_t m = byte_mask_word(j, 0, n1);
@@ -515,9 +516,8 @@ __global__ void __launch_bounds__(256) pack_delta_vis_flat_kernel(PackArgs a) {
         }
 #pragma unroll
         for (int e = 0; e < 3; ++e) {
-            const int64_t off = e * T + f0;
-            uint4 *dst = reinterpret_cast<uint4 *>(a.cur + off);
-            *dst = make_uint4(o[e][0], o[e][1], o[e][2], o[e][3]);
+            const size_t off = size_t(e) * T + f0;
+            *reinterpret_cast<uint4 *>(a.cur + off) = make_uint4(o[e][0], o[e][1], o[e][2], o[e][3]);
             if (!a.skip && !a.residual) continue;
             uint32_t d[4] = {o[e][0], o[e][1], o[e][2], o[e][3]};
             if (prev) {
@@ -534,23 +534,24 @@ __global__ void __launch_bounds__(256) pack_delta_vis_flat_kernel(PackArgs a) {
                     make_uint4(o[e][0], o[e][1], o[e][2], o[e][3]);
             }
             if (!a.skip) continue;
-            // SKIP (pre-set to 1 when prev exists): a changed byte clears its block;
-            // key frames clear every block the word touches
-            auto clear = [&](int64_t rr, int64_t xa, int lo, int hi) {
-                // bytes [lo, hi) of the word are row rr, columns xa + (b - lo)
-                const int64_t bxa = xa / 16, bxb = (xa + (hi - lo) - 1) / 16;
-                for (int64_t bx = bxa; bx <= bxb; ++bx) {
-                    const int blo = lo + int(bx * 16 - xa > 0 ? bx * 16 - xa : 0);
-                    const int bhi = lo + int((bx + 1) * 16 - xa < hi - lo ? (bx + 1) * 16 - xa
-                                                                          : hi - lo);
+            // SKIP (preset to 1): a changed byte clears its codec block; key frames
+            // clear every block the word touches.  Bytes [lo, hi) of the word are
+            // row rr, columns xa + (b - lo); they meet at most two blocks.
+            auto clear = [&](uint32_t rr, uint32_t xa, int lo, int hi) {
+                const uint32_t bxa = xa >> 4, bxb = (xa + uint32_t(hi - lo) - 1) >> 4;
+                uint8_t *sk = a.skip + (size_t(e) * nby + (rr >> 4)) * nseg;
+                for (uint32_t bx = bxa; bx <= bxb; ++bx) {
+                    const int blo = lo + int(bx * 16 > xa ? bx * 16 - xa : 0);
+                    const int bhi = lo + int((bx + 1) * 16 - xa < uint32_t(hi - lo)
+                                                 ? (bx + 1) * 16 - xa : uint32_t(hi - lo));
                     bool dirty = !prev;
 #pragma unroll
                     for (int j = 0; j < 4; ++j) dirty |= (d[j] & byte_mask_word(j, blo, bhi)) != 0u;
-                    if (dirty) a.skip[(int64_t(e) * nby + rr / TILE_Y) * a.nseg + bx] = 0;
+                    if (dirty) sk[bx] = 0;
                 }
             };
             clear(r, x0, 0, n1);
-            if (n1 < 16 && r + 1 < a.h) clear(r + 1, 0, n1, 16);
+            if (n1 < 16) clear(r + 1, 0, n1, 16);
         }
     }
 }
@@ -650,7 +651,8 @@ int launch_pack_delta(int kind, const void *texels, int64_t h, int64_t w, int64_
                                  aligned16(planes_cur) && (!planes_prev || aligned16(planes_prev)) &&
                                  (!residual || aligned16(residual));
     static const bool funnel = getenv("PS_PACK_FUNNEL") != nullptr;  // tuning: old path
-    const bool flat = rows_misaligned && !funnel && (h * a.pw) % 16 == 0 && a.vec_in;
+    const bool flat = rows_misaligned && !funnel && (h * a.pw) % 16 == 0 && a.pw >= 16 && a.vec_in &&
+                      3 * h * a.pw < (int64_t(1) << 31);
     if (kind == PS_KIND_COLOR) {
         pack_delta_kernel<PS_KIND_COLOR><<<grid, block, 0, stream>>>(a);
     } else if (flat) {

@@ -409,7 +409,8 @@ class UpdateAtlasLayout:
         entries, count = self.assign_device(ids)
         self.raise_pending()
         n = int(count.item())
-        return [tuple(r) for r in entries[:n].cpu().tolist()]
+        e = entries[:n].cpu()
+        return list(zip(e[:, 0].tolist(), e[:, 1].tolist()))
 
     # dict views for API parity with the reference attributes
     @property
@@ -479,8 +480,8 @@ def build_update_atlas(selected, layout: UpdateAtlasLayout, source, update_texel
         if ids.numel() and (int(ids.min()) < 0 or int(ids.max()) >= n):
             raise IndexError("selected probe outside the source atlas")
     else:
-        host = np.asarray(list(selected) if not isinstance(selected, np.ndarray) else selected,
-                          dtype=np.int64).reshape(-1)
+        host = np.asarray(selected if isinstance(selected, (np.ndarray, list, tuple))
+                          else list(selected), dtype=np.int64).reshape(-1)
         uniq = np.unique(host)
         if len(uniq) > layout.slot_count:
             raise SlotOverflowError(f"{len(uniq)} probes selected for {layout.slot_count} "
@@ -494,7 +495,8 @@ def build_update_atlas(selected, layout: UpdateAtlasLayout, source, update_texel
            count.data_ptr(), layout.slot_count, layout.slots_per_row, upd.data_ptr(),
            shape[1], None, None, 0, None, D.stream_ptr(dev))
     k = int(count.item())
-    ent = [tuple(r) for r in entries[:k].cpu().tolist()]
+    e = entries[:k].cpu()
+    ent = list(zip(e[:, 0].tolist(), e[:, 1].tolist()))  # [(slot, probe), ...] by slot
     if out_np is not None:
         out_np[...] = D.to_numpy(upd)
         return out_np, ent
