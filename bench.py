@@ -124,10 +124,17 @@ def load_peaks():
     return 6650.0, "fallback"
 
 
+def ncu_summary_path() -> Path:
+    """The newest committed ncu summary (profiles/ncu_summary_r*.json, else
+    the round-1 profiles/ncu_summary.json)."""
+    rounds = sorted((ROOT / "profiles").glob("ncu_summary_r*.json"))
+    return rounds[-1] if rounds else ROOT / "profiles" / "ncu_summary.json"
+
+
 def profile_metric(prefix: str, key: str):
     """A fraction (pct / 100) for the first kernel starting with `prefix` in the
     committed ncu summary, or None."""
-    p = ROOT / "profiles" / "ncu_summary.json"
+    p = ncu_summary_path()
     if not p.exists():
         return None
     try:
@@ -158,8 +165,8 @@ def trace_issue_profile():
 def profile_traffic(prefix: str):
     """DRAM bytes (read + write) per launch, summed over the kernels whose name
     starts with `prefix` (one launch per texture kind), from the committed
-    ncu summary (profiles/ncu_summary.json); None if absent."""
-    p = ROOT / "profiles" / "ncu_summary.json"
+    ncu summary (profiles/ncu_summary_r*.json); None if absent."""
+    p = ncu_summary_path()
     if not p.exists():
         return None
     try:

@@ -301,7 +301,7 @@ __device__ __forceinline__ void issue_mma(const float *st, uint32_t tmem, int c)
     mma_tf32(tmem + COL_C, a_c, b_cl, ID_C, 1u);
 }
 
-__global__ void __launch_bounds__(THREADS, 2) blend_tc_kernel(ps_trace_params prm) {
+__global__ void __launch_bounds__(THREADS, 2) blend_tc_kernel(ps_trace_params prm, int rotate) {
     extern __shared__ unsigned char smem_raw[];
     float *stages = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~uintptr_t(1023));
@@ -314,6 +314,10 @@ __global__ void __launch_bounds__(THREADS, 2) blend_tc_kernel(ps_trace_params pr
     const int64_t left = int64_t(prm.probe_end) - p0;
     const int nq = int(left < P ? left : P);
     const int64_t pl0 = p0 - prm.probe_begin;
+    // rotate: CTA b walks its k-steps from (b mod NK), so the CTAs in flight read
+    // different weight-image k-steps instead of all the same L2 lines at once
+    const int kr = rotate ? int(blockIdx.x % unsigned(NK)) : 0;
+    auto kstep = [&](int c) { return c + kr < NK ? c + kr : c + kr - NK; };
 
     if (tid == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -347,14 +351,15 @@ __global__ void __launch_bounds__(THREADS, 2) blend_tc_kernel(ps_trace_params pr
         const int q = tid >> 2, j = tid & 3;
 #pragma unroll
         for (int c = 0; c < RING - 1; ++c) {
-            if (c < NK) issue_raw(ring + c * RAW, records, R, q, nq, c, j);
+            if (c < NK) issue_raw(ring + c * RAW, records, R, q, nq, kstep(c), j);
             cp_async_commit();
         }
 #pragma unroll 1
         for (int c = 0; c < NK; ++c) {
             const int s = c % STAGES, u = c / STAGES;
             if (c + RING - 1 < NK)
-                issue_raw(ring + ((c + RING - 1) % RING) * RAW, records, R, q, nq, c + RING - 1, j);
+                issue_raw(ring + ((c + RING - 1) % RING) * RAW, records, R, q, nq,
+                          kstep(c + RING - 1), j);
             cp_async_commit();
             cp_async_wait<RING - 1>();  // k-step c's records have landed
             const Rec2 rv = read_raw(ring + (c % RING) * RAW, q, nq, j);
@@ -393,8 +398,8 @@ __global__ void __launch_bounds__(THREADS, 2) blend_tc_kernel(ps_trace_params pr
                 if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
                 // the k-step's five operand images are contiguous in the weight image
                 mbar_expect_tx(&a_full[s], A_LOAD_BYTES);
-                bulk_g2s(stages + s * STAGE, prm.w_image + size_t(c) * A_FLOATS, A_LOAD_BYTES,
-                         &a_full[s]);
+                bulk_g2s(stages + s * STAGE, prm.w_image + size_t(kstep(c)) * A_FLOATS,
+                         A_LOAD_BYTES, &a_full[s]);
             }
         }
         __syncwarp();
@@ -572,7 +577,9 @@ void launch_blend_tc(const ps_trace_params &p, int64_t nloc, cudaStream_t s) {
                    "cudaFuncSetAttribute(blend_tc)");
         attr = true;
     }
-    tc::blend_tc_kernel<<<unsigned(ceil_div(nloc, tc::P)), tc::THREADS, tc::SMEM_BYTES, s>>>(p);
+    static const int rotate = getenv("PS_BLEND_ROTATE") ? atoi(getenv("PS_BLEND_ROTATE")) : 0;
+    tc::blend_tc_kernel<<<unsigned(ceil_div(nloc, tc::P)), tc::THREADS, tc::SMEM_BYTES, s>>>(
+        p, rotate);
     check_launch("blend_tc_kernel");
 }
 

@@ -7,6 +7,9 @@
 #include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "ps_common.cuh"
 
 namespace ps {
@@ -220,6 +223,77 @@ __global__ void __launch_bounds__(256, SIDE == 18 ? 3 : 4)
         });
         if (lane == 0 && last_sent_seq) last_sent_seq[p] = current_seq;
     }
+}
+
+// Build through shared memory: each warp keeps BUILD_DEPTH blocks in flight
+// with 8-byte cp.async copies (a block row is 4 * SIDE bytes at an 8-byte
+// aligned offset: 5 / 9 copies per row), so a warp's loads no longer live in
+// registers and an SM keeps ~4x more bytes in flight than the register
+// version (whose 24 resident warps held one block each).  Once a block has
+// landed the warp writes its core to the slot and commits the whole block.
+constexpr int BUILD_DEPTH = 4;
+
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+                 "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit_group() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int SIDE>
+__global__ void __launch_bounds__(256)
+    build_async_kernel(const uint32_t *src, int64_t src_w, int64_t ppr, const int64_t *entries,
+                       const int64_t *entry_count, int64_t slots_per_row, uint32_t *dst,
+                       int64_t dst_w, uint32_t *last_sent, int64_t *last_sent_seq,
+                       int64_t current_seq, const int64_t *seq_dev) {
+    constexpr int CORE = SIDE - 2, HALF = SIDE / 2, PAIRS = SIDE * HALF, WORDS = SIDE * SIDE;
+    __shared__ __align__(16) uint2 ring[8][BUILD_DEPTH][PAIRS];
+    const int64_t count = *entry_count;
+    if (seq_dev) current_seq = *seq_dev;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    uint2(*my)[PAIRS] = ring[wib];
+    auto issue = [&](int64_t e, int slot) {
+        if (e < count) {
+            const int64_t p = entries[2 * e + 1];
+            const uint2 *sb = reinterpret_cast<const uint2 *>(src + (p / ppr) * SIDE * src_w +
+                                                              (p % ppr) * SIDE);
+            const int64_t wp = src_w / 2;  // row stride in pairs (src_w is even: ppr * SIDE)
+            for (int k = lane; k < PAIRS; k += 32) cp_async8(&my[slot][k], sb + (k / HALF) * wp + k % HALF);
+        }
+        cp_async_commit_group();
+    };
+#pragma unroll
+    for (int d = 0; d < BUILD_DEPTH - 1; ++d) issue(warp + d * nwarps, d);
+    int slot = 0;
+    for (int64_t e = warp; e < count; e += nwarps) {
+        issue(e + (BUILD_DEPTH - 1) * nwarps, (slot + BUILD_DEPTH - 1) % BUILD_DEPTH);
+        cp_async_wait_group<BUILD_DEPTH - 1>();
+        __syncwarp();
+        const int64_t s_ = entries[2 * e], p = entries[2 * e + 1];
+        const uint32_t *blk = reinterpret_cast<const uint32_t *>(my[slot]);
+        const int64_t y0 = (p / ppr) * SIDE, x0 = (p % ppr) * SIDE;
+        const int64_t sy = (s_ / slots_per_row) * CORE, sx = (s_ % slots_per_row) * CORE;
+        for (int k = lane; k < CORE * CORE; k += 32) {
+            const int r = k / CORE, c = k % CORE;
+            dst[(sy + r) * dst_w + sx + c] = blk[(r + 1) * SIDE + c + 1];
+        }
+        if (last_sent) {
+            uint2 *ls = reinterpret_cast<uint2 *>(last_sent + y0 * src_w + x0);
+            const int64_t wp = src_w / 2;
+            for (int k = lane; k < PAIRS; k += 32) ls[(k / HALF) * wp + k % HALF] = my[slot][k];
+        }
+        if (lane == 0 && last_sent_seq) last_sent_seq[p] = current_seq;
+        __syncwarp();  // the slot is refilled by the next iteration's issue
+        slot = (slot + 1) % BUILD_DEPTH;
+        (void)WORDS;
+    }
+    cp_async_wait_group<0>();
 }
 
 // slab-sharded build: export own probes' cores into a per-rank payload
@@ -566,6 +640,27 @@ int ps_build_update(int kind, const void *source, int64_t probe_count, int64_t p
     const int64_t src_w = probes_per_row * side;
     const unsigned blocks = unsigned(std::max<int64_t>(
         1, std::min<int64_t>(ceil_div(max_entries, 8), int64_t(sm_count()) * 16)));
+    // tuning knob: the cp.async variant measured equal (visibility) or slower
+    // (colour 0.056 -> 0.062 ms at C4), so the register version is the default
+    static const bool async_build = getenv("PS_BUILD_ASYNC") != nullptr;
+    if (async_build) {
+        const unsigned ab = unsigned(std::max<int64_t>(
+            1, std::min<int64_t>(ceil_div(max_entries, 8 * BUILD_DEPTH), int64_t(sm_count()) * 8)));
+        if (kind == PS_KIND_COLOR)
+            build_async_kernel<10><<<ab, 256, 0, s>>>(
+                static_cast<const uint32_t *>(source), src_w, probes_per_row, entries,
+                entry_count, slots_per_row, static_cast<uint32_t *>(update_texels),
+                update_row_stride, static_cast<uint32_t *>(last_sent), last_sent_seq,
+                current_seq, current_seq_dev);
+        else
+            build_async_kernel<18><<<ab, 256, 0, s>>>(
+                static_cast<const uint32_t *>(source), src_w, probes_per_row, entries,
+                entry_count, slots_per_row, static_cast<uint32_t *>(update_texels),
+                update_row_stride, static_cast<uint32_t *>(last_sent), last_sent_seq,
+                current_seq, current_seq_dev);
+        check_launch("build_async_kernel");
+        return PS_OK;
+    }
     if (kind == PS_KIND_COLOR)
         build_kernel<10><<<blocks, 256, 0, s>>>(
             static_cast<const uint32_t *>(source), src_w, probes_per_row, entries, entry_count,
