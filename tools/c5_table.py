@@ -17,8 +17,8 @@ def main():
           "delta 768 / 2,048 B per selected probe) over the staged chain time; `pack_delta` is "
           "the kernel alone over the whole update atlas it rewrites every frame, against the "
           "measured 6,546.6 GB/s.  Visibility planes of N < 131,072 have rows that are not "
-          "16-byte aligned (update atlas 4,096 texels wide and less) and take the funnel-shift "
-          "kernel.\n")
+          "16-byte aligned (update atlas 4,096 texels wide and less) and take the flat-word "
+          "kernel (round 2; the funnel-shift kernel before it).\n")
     print("| N | p changed | active | colour chain ms | vis chain ms | colour graphed ms | "
           "vis graphed ms | colour alg GB/s (frac) | vis alg GB/s (frac) | pack_delta frac c / v "
           "| graphed chains Hz (c+v) |")
