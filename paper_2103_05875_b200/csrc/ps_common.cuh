@@ -72,6 +72,33 @@ struct Carver {
 
 
 #ifdef __CUDACC__
+// Division by a run-time constant d >= 1 for dividends n < 2^31 as a
+// multiply-high, an add and a shift (Granlund-Montgomery): s = ceil(log2 d),
+// m = floor(2^32 (2^s - d) / d) + 1, n / d = (umulhi(n, m) + n) >> s.  Set up
+// once per thread; replaces the ~15-instruction reciprocal sequence (or the
+// 64-bit software division) of every per-ray / per-entry index split.
+struct FastDiv {
+    uint32_t d, m, s;
+    __device__ __forceinline__ explicit FastDiv(uint32_t d_) : d(d_) {
+        s = 0;
+        while ((1ull << s) < d) ++s;
+        m = uint32_t((((1ull << s) - d) << 32) / d + 1);
+    }
+    __device__ __forceinline__ uint32_t div(uint32_t n) const {
+        return (__umulhi(n, m) + n) >> s;
+    }
+};
+
+// (row, column) origin of block `id` in a grid of `per_row` blocks of `side`
+// texels: ids and grids are < 2^31, so one 32-bit division instead of a
+// 64-bit software divide and modulo
+__device__ __forceinline__ void block_origin(int64_t id, int64_t per_row, int side, int64_t &y,
+                                             int64_t &x) {
+    const uint32_t i = uint32_t(id), n = uint32_t(per_row), r = i / n;
+    y = int64_t(r) * side;
+    x = int64_t(i - r * n) * side;
+}
+
 // One warp moves probe block (y0, x0) -- SIDE x SIDE words of a rendered
 // atlas, row stride src_w -- handing each interior (core) word to `core(r, c,
 // v)` and, if last_sent is set, committing the whole block there.  Every load

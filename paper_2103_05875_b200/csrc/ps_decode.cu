@@ -215,8 +215,10 @@ __global__ void __launch_bounds__(256)
     const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
     for (int64_t e = warp; e < count; e += nwarps) {
         const int64_t slot = entries[2 * e], p = entries[2 * e + 1];
-        const int64_t sy = (slot / slots_per_row) * CORE, sx = (slot % slots_per_row) * CORE;
-        const int64_t y0 = (p / ppr) * SIDE, x0 = (p % ppr) * SIDE;
+        int64_t sy, sx;
+        block_origin(slot, slots_per_row, CORE, sy, sx);
+        int64_t y0, x0;
+        block_origin(p, ppr, SIDE, y0, x0);
         for (int k = lane; k < SIDE * SIDE; k += 32) {
             const int r = k / SIDE, c = k % SIDE;
             const int n = CORE;

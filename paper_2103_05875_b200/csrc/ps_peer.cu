@@ -43,8 +43,10 @@ __global__ void __launch_bounds__(256)
         const int64_t slot = entries[2 * e], p = entries[2 * e + 1];
         if (lane == 0 && last_sent_seq) last_sent_seq[p] = current_seq;  // replicated stamp
         if (p < probe_begin || p >= probe_end) continue;
-        const int64_t y0 = (p / ppr) * SIDE, x0 = (p % ppr) * SIDE;
-        const int64_t sy = (slot / slots_per_row) * CORE, sx = (slot % slots_per_row) * CORE;
+        int64_t y0, x0;
+        block_origin(p, ppr, SIDE, y0, x0);
+        int64_t sy, sx;
+        block_origin(slot, slots_per_row, CORE, sy, sx);
         warp_copy_block<SIDE>(src, src_w, y0, x0, lane, last_sent, [&](int r, int c, uint32_t v) {
             dst[(sy + r) * dst_w + sx + c] = v;  // encoder's atlas, maybe remote
         });

@@ -214,10 +214,15 @@ __global__ void __launch_bounds__(256, SIDE == 18 ? 3 : 4)
     const int lane = threadIdx.x & 31;
     const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    // probe ids and slots are < 2^31: 32-bit divisions (a 64-bit division is a
+    // ~70-instruction software sequence, four of them per entry dominated the
+    // kernel's instruction count)
+    const uint32_t ppr32 = uint32_t(ppr), spr32 = uint32_t(slots_per_row);
     for (int64_t e = warp; e < count; e += nwarps) {
-        const int64_t slot = entries[2 * e], p = entries[2 * e + 1];
-        const int64_t y0 = (p / ppr) * SIDE, x0 = (p % ppr) * SIDE;
-        const int64_t sy = (slot / slots_per_row) * CORE, sx = (slot % slots_per_row) * CORE;
+        const uint32_t slot = uint32_t(entries[2 * e]), p = uint32_t(entries[2 * e + 1]);
+        const uint32_t py = p / ppr32, sy_ = slot / spr32;
+        const int64_t y0 = int64_t(py) * SIDE, x0 = int64_t(p - py * ppr32) * SIDE;
+        const int64_t sy = int64_t(sy_) * CORE, sx = int64_t(slot - sy_ * spr32) * CORE;
         warp_copy_block<SIDE>(src, src_w, y0, x0, lane, last_sent, [&](int r, int c, uint32_t v) {
             dst[(sy + r) * dst_w + sx + c] = v;
         });
@@ -277,8 +282,10 @@ __global__ void __launch_bounds__(256)
         __syncwarp();
         const int64_t s_ = entries[2 * e], p = entries[2 * e + 1];
         const uint32_t *blk = reinterpret_cast<const uint32_t *>(my[slot]);
-        const int64_t y0 = (p / ppr) * SIDE, x0 = (p % ppr) * SIDE;
-        const int64_t sy = (s_ / slots_per_row) * CORE, sx = (s_ % slots_per_row) * CORE;
+        int64_t y0, x0;
+        block_origin(p, ppr, SIDE, y0, x0);
+        int64_t sy, sx;
+        block_origin(s_, slots_per_row, CORE, sy, sx);
         for (int k = lane; k < CORE * CORE; k += 32) {
             const int r = k / CORE, c = k % CORE;
             dst[(sy + r) * dst_w + sx + c] = blk[(r + 1) * SIDE + c + 1];
@@ -313,7 +320,8 @@ __global__ void __launch_bounds__(256)
         const int64_t p = entries[2 * e + 1];
         if (lane == 0 && last_sent_seq) last_sent_seq[p] = current_seq;  // replicated stamp
         if (p < probe_begin || p >= probe_end) continue;
-        const int64_t y0 = (p / ppr) * SIDE, x0 = (p % ppr) * SIDE;
+        int64_t y0, x0;
+        block_origin(p, ppr, SIDE, y0, x0);
         uint32_t *dst = payload + (p - probe_begin) * (CORE * CORE);
         warp_copy_block<SIDE>(src, src_w, y0, x0, lane, last_sent,
                               [&](int r, int c, uint32_t v) { dst[r * CORE + c] = v; });
@@ -338,7 +346,8 @@ __global__ void __launch_bounds__(256)
         int r = 0;
         while (r + 1 < world && p >= s_begin[r + 1]) ++r;
         const uint32_t *srcp = payloads + (int64_t(r) * payload_stride + (p - s_begin[r])) * (CORE * CORE);
-        const int64_t sy = (slot / slots_per_row) * CORE, sx = (slot % slots_per_row) * CORE;
+        int64_t sy, sx;
+        block_origin(slot, slots_per_row, CORE, sy, sx);
 #pragma unroll 4
         for (int k = lane; k < CORE * CORE; k += 32) {
             const int rr = k / CORE, cc = k % CORE;
@@ -442,7 +451,8 @@ __global__ void guard_kernel(uint32_t *atlas, int64_t w, int64_t ppr, int64_t pr
         else if (r == SIDE - 1) { sr = N; sc = SIDE - 1 - c; }
         else if (c == 0) { sr = SIDE - 1 - r; sc = 1; }
         else { sr = SIDE - 1 - r; sc = N; }
-        const int64_t y0 = (p / ppr) * SIDE, x0 = (p % ppr) * SIDE;
+        int64_t y0, x0;
+        block_origin(p, ppr, SIDE, y0, x0);
         atlas[(y0 + r) * w + x0 + c] = atlas[(y0 + sr) * w + x0 + sc];
     }
 }

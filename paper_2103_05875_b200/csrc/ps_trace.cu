@@ -169,16 +169,38 @@ __global__ void __launch_bounds__(256) shadow_map_kernel(ps_trace_params prm) {
     // directions from the light) when the whole map is traced and S allows it;
     // otherwise consecutive texels of a row
     const bool blocked = prm.shadow_texel_begin == 0 && total == all && S % 8 == 0;
+    // index splits by run-time constants as multiply-high divisions (all < 2^31
+    // for maps up to 30 lights x 6 x 3,344^2; larger maps take 64-bit divides)
+    const bool fast = all < (int64_t(1) << 31);
+    const FastDiv div_light{uint32_t(fast ? per_light : 1)}, div_face{uint32_t(S * S)},
+        div_s{uint32_t(S)}, div_bs{uint32_t(S >= 8 ? S / 8 : 1)};
     for (int64_t wi = prm.shadow_texel_begin + blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
          wi < total; wi += int64_t(gridDim.x) * blockDim.x) {
-        const int l = int(wi / per_light);
-        const int rem = int(wi - int64_t(l) * per_light);
-        const int f = rem / (S * S);
-        int j = (rem / S) % S, i = rem % S;
-        if (blocked) {
-            const int r2 = rem - f * S * S, blk = r2 >> 5, ln = r2 & 31;
-            i = (blk % (S / 8)) * 8 + (ln & 7);
-            j = (blk / (S / 8)) * 4 + (ln >> 3);
+        int l, rem, f, i, j;
+        if (fast) {
+            l = int(div_light.div(uint32_t(wi)));
+            rem = int(uint32_t(wi) - uint32_t(l) * div_light.d);
+            f = int(div_face.div(uint32_t(rem)));
+            const uint32_t r2 = uint32_t(rem) - uint32_t(f) * div_face.d;
+            const uint32_t row = div_s.div(r2);
+            j = int(row);
+            i = int(r2 - row * div_s.d);
+            if (blocked) {
+                const uint32_t blk = r2 >> 5, ln = r2 & 31, by = div_bs.div(blk);
+                i = int(blk - by * div_bs.d) * 8 + int(ln & 7);
+                j = int(by) * 4 + int(ln >> 3);
+            }
+        } else {
+            l = int(wi / per_light);
+            rem = int(wi - int64_t(l) * per_light);
+            f = rem / (S * S);
+            j = (rem / S) % S;
+            i = rem % S;
+            if (blocked) {
+                const int r2 = rem - f * S * S, blk = r2 >> 5, ln = r2 & 31;
+                i = (blk % (S / 8)) * 8 + (ln & 7);
+                j = (blk / (S / 8)) * 4 + (ln >> 3);
+            }
         }
         const int64_t idx = int64_t(l) * per_light + int64_t(f) * S * S + int64_t(j) * S + i;
         const int a = f >> 1;
@@ -266,6 +288,10 @@ __global__ void __launch_bounds__(TPB, TPB == THREADS ? MINB : (TPB == 1024 ? 1 
                                : PROBE_PARALLEL ? probe_groups * R : nloc * chunks_per_probe;
     const int lane = threadIdx.x & 31;
     float4 *records = reinterpret_cast<float4 *>(prm.records);
+    // run-time divisors of the tiled chunk decode (task -> tile, direction ->
+    // probe i, j, k): multiply-high divisions instead of per-ray divisions
+    const FastDiv div_dg{uint32_t(dgroups > 0 ? dgroups : 1)},
+        div_tx{uint32_t(tiles_x > 0 ? tiles_x : 1)}, div_ty{uint32_t(tiles_y > 0 ? tiles_y : 1)};
     while (true) {
         uint32_t task = 0;
         if (lane == 0) {
@@ -292,22 +318,25 @@ __global__ void __launch_bounds__(TPB, TPB == THREADS ? MINB : (TPB == 1024 ? 1 
         if (int64_t(task) >= total_chunks) break;
         int64_t q;
         int r;
+        int64_t i = 0, j = 0, k = 0;  // grid coordinates (TILED: from the tile)
         if (TILED) {
-            int64_t t;
+            uint32_t t;
             if (PROBE_PARALLEL == 7) {  // direction-major: all tiles for one direction
                 r = int(int64_t(task) / tiles);
-                t = int64_t(task) - int64_t(r) * tiles;
+                t = uint32_t(int64_t(task) - int64_t(r) * tiles);
             } else {
-                t = int64_t(task) / dgroups;
-                r = int(int64_t(task) - t * dgroups) * DD + lane / (TX * TY * TZ);
+                t = div_dg.div(task);
+                r = int(task - t * div_dg.d) * DD + lane / (TX * TY * TZ);
                 if (r >= R) continue;
             }
             const int pl = lane % (TX * TY * TZ);
-            const int64_t tx = t % tiles_x, ty = (t / tiles_x) % tiles_y, tz = t / (tiles_x * tiles_y);
-            const int64_t pi = tx * TX + (pl % TX), pj = ty * TY + ((pl / TX) % TY);
-            const int64_t pk = k0 + tz * TZ + pl / (TX * TY);
-            const int64_t pp = pi + prm.nx * (pj + prm.ny * pk);
-            if (pi >= prm.nx || pj >= prm.ny || pp < prm.probe_begin || pp >= prm.probe_end) continue;
+            const uint32_t txy = div_tx.div(t), tz = div_ty.div(txy);
+            const uint32_t tx = t - txy * div_tx.d, ty = txy - tz * div_ty.d;
+            i = int64_t(tx) * TX + (pl % TX);
+            j = int64_t(ty) * TY + ((pl / TX) % TY);
+            k = k0 + int64_t(tz) * TZ + pl / (TX * TY);
+            const int64_t pp = i + prm.nx * (j + prm.ny * k);
+            if (i >= prm.nx || j >= prm.ny || pp < prm.probe_begin || pp >= prm.probe_end) continue;
             q = pp - prm.probe_begin;
         } else if (PROBE_PARALLEL) {
             const int64_t g = int64_t(task) / R;
@@ -319,8 +348,12 @@ __global__ void __launch_bounds__(TPB, TPB == THREADS ? MINB : (TPB == 1024 ? 1 
             r = int(int64_t(task) - q * chunks_per_probe) * 32 + lane;
             if (r >= R) continue;
         }
-        const int64_t p = prm.probe_begin + q;
-        const int64_t i = p % prm.nx, j = (p / prm.nx) % prm.ny, k = p / (int64_t(prm.nx) * prm.ny);
+        if (!TILED) {
+            const int64_t p = prm.probe_begin + q;
+            i = p % prm.nx;
+            j = (p / prm.nx) % prm.ny;
+            k = p / (int64_t(prm.nx) * prm.ny);
+        }
         Ray ray;
         // origin + spacing * (i, j, k) in double, rounded once (no FMA
         // contraction, as numpy evaluates volume.py:138)
