@@ -54,7 +54,10 @@ def _compile(src: Path, force: bool) -> tuple[Path, str]:
     if not force and not _stale(src, obj):
         return obj, ""
     if src.suffix == ".cu":
-        cmd = [_nvcc(), *ARCH, *NVCC_FLAGS, f"-I{INCLUDE}", f"-I{CSRC}", "-c", str(src), "-o", str(obj)]
+        # PS_NVCC_EXTRA: extra nvcc flags for tuning builds (e.g. -DPS_BLEND_STAGES=6)
+        extra = os.environ.get("PS_NVCC_EXTRA", "").split()
+        cmd = [_nvcc(), *ARCH, *NVCC_FLAGS, *extra, f"-I{INCLUDE}", f"-I{CSRC}", "-c", str(src),
+               "-o", str(obj)]
     else:
         cmd = ["g++", *CXX_FLAGS, f"-I{INCLUDE}", "-I/usr/local/cuda/include", "-c", str(src),
                "-o", str(obj)]

@@ -82,7 +82,10 @@ constexpr uint32_t COL_D0 = 0, COL_D1 = BD_ROWS, COL_C = 2 * BD_ROWS, TMEM_COLS 
 static_assert(COL_C + BC_ROWS <= TMEM_COLS, "accumulators must fit the TMEM allocation");
 static_assert(P * 64 + P * 256 + XBUF <= STAGES * STAGE + RING * RAW,
               "epilogue staging must fit the stages and the ring");
-static_assert(2 * (SMEM_BYTES + 1024) + 1024 <= 233472, "two CTAs per SM");
+#ifndef PS_BLEND_CTAS
+#define PS_BLEND_CTAS 2  // CTAs per SM (tuning: 1 allows deeper stage / ring pipelines)
+#endif
+static_assert(PS_BLEND_CTAS * (SMEM_BYTES + 1024) + 1024 <= 233472, "CTAs per SM vs shared memory");
 
 // canonical K-major, no-swizzle operand image: 8-row x 16-byte core matrices,
 // row groups 128 B apart (SBO), the two 4-wide k halves rows*16 B apart (LBO);
@@ -301,7 +304,8 @@ __device__ __forceinline__ void issue_mma(const float *st, uint32_t tmem, int c)
     mma_tf32(tmem + COL_C, a_c, b_cl, ID_C, 1u);
 }
 
-__global__ void __launch_bounds__(THREADS, 2) blend_tc_kernel(ps_trace_params prm, int rotate) {
+__global__ void __launch_bounds__(THREADS, PS_BLEND_CTAS)
+    blend_tc_kernel(ps_trace_params prm, int rotate) {
     extern __shared__ unsigned char smem_raw[];
     float *stages = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~uintptr_t(1023));
