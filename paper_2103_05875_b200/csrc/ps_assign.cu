@@ -48,22 +48,33 @@ __device__ __forceinline__ void st_rel(uint64_t *p, uint64_t v) {
     asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// exclusive prefix of this tile (thread 0 only); values are packed pairs
-// (hi << 31 | lo) that add without carrying between the halves (< 2^31 each)
+// exclusive prefix of this tile, computed by warp 0 (every lane must call):
+// the tile publishes its aggregate, then the warp reads up to 32 predecessors'
+// status words at once and sums back to the nearest published prefix -- one
+// L2 round trip per 32 tiles instead of one per tile.  Values are packed pairs
+// (hi << 31 | lo) that add without carrying between the halves (< 2^31 each).
 __device__ uint64_t look_back(uint64_t *status, int64_t tile, uint64_t agg) {
+    const int lane = threadIdx.x & 31;
     if (tile == 0) {
-        st_rel(status, FLAG_PREFIX | agg);
+        if (lane == 0) st_rel(status, FLAG_PREFIX | agg);
         return 0;
     }
-    st_rel(status + tile, FLAG_AGG | agg);
+    if (lane == 0) st_rel(status + tile, FLAG_AGG | agg);
     uint64_t excl = 0;
-    for (int64_t j = tile - 1;; --j) {
-        uint64_t v;
-        while (((v = ld_acq(status + j)) >> 62) == 0) __nanosleep(32);
-        excl += v & VAL_MASK;
-        if ((v >> 62) == 2) break;
+    for (int64_t base = tile - 1;; base -= 32) {
+        const int64_t j = base - lane;
+        uint64_t v = FLAG_PREFIX;  // before tile 0: an empty prefix
+        if (j >= 0)
+            while (((v = ld_acq(status + j)) >> 62) == 0) __nanosleep(32);
+        const unsigned pre = __ballot_sync(0xffffffffu, (v >> 62) == 2);
+        const int stop = pre ? __ffs(pre) - 1 : 31;  // nearest published prefix
+        uint64_t x = lane <= stop ? (v & VAL_MASK) : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        excl += x;
+        if (pre) break;
     }
-    st_rel(status + tile, FLAG_PREFIX | (excl + agg));
+    if (lane == 0) st_rel(status + tile, FLAG_PREFIX | (excl + agg));
     return excl;
 }
 
@@ -128,10 +139,10 @@ __global__ void __launch_bounds__(AS_THREADS)
                                 __reduce_add_sync(0xffffffffu, __popc(neww)));
     uint64_t tile_total;
     const uint64_t woff = warp_offsets(mine, s_warp, tile_total);
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {
         const uint64_t excl = look_back(status, tile, tile_total);
-        s_base = excl;
-        if (tile == ntiles - 1) {  // totals: plan (ps_select.cu plan_kernel layout) + meta
+        if (threadIdx.x == 0) s_base = excl;
+        if (threadIdx.x == 0 && tile == ntiles - 1) {  // totals: plan (plan_kernel layout) + meta
             const uint64_t all = excl + tile_total;
             const int64_t sc = int64_t(all >> 31), nc = int64_t(all & 0x7fffffffu);
             plan[0] = sc;
@@ -194,10 +205,12 @@ __global__ void __launch_bounds__(AS_THREADS)
     const uint64_t mine = __reduce_add_sync(0xffffffffu, __popc(emask));
     uint64_t tile_total;
     const uint64_t woff = warp_offsets(mine, s_warp, tile_total);
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {
         const uint64_t excl = look_back(status, tile, tile_total);
-        s_base = excl;
-        if (tile == ntiles - 1) *entry_count = int64_t(excl + tile_total);
+        if (threadIdx.x == 0) {
+            s_base = excl;
+            if (tile == ntiles - 1) *entry_count = int64_t(excl + tile_total);
+        }
     }
     __syncthreads();
     int64_t rank = int64_t(s_base + woff);

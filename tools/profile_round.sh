@@ -17,7 +17,7 @@ launches)
     tail -2 $OUT/ncu_launch.log ;;
 full)
     ncu --set full --clock-control none --import-source on \
-        -k regex:"trace_kernel|blend|shadow_map|pack_delta|detect_kernel|build_kernel|bind_kernel|entries_kernel" \
+        -k regex:"trace_kernel|blend|shadow_map|pack_delta|detect_kernel|build_kernel|build_multi|bind_kernel|entries_kernel" \
         -s 13 -c 13 -o $OUT/full_c4 $CMD > $OUT/ncu_full.log 2>&1 || true
     tail -2 $OUT/ncu_full.log ;;
 esac
