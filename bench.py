@@ -577,7 +577,7 @@ def run_reference(args, rank, world, local):
 def main():
     # keep rank 0's stdout to the single JSON line: NCCL's debug output
     # (version banner, communicator lines at NCCL_DEBUG=INFO) goes to stderr
-    if os.environ.get("NCCL_DEBUG") and not os.environ.get("NCCL_DEBUG_FILE"):
+    if not os.environ.get("NCCL_DEBUG_FILE"):
         os.environ["NCCL_DEBUG_FILE"] = "/dev/stderr"
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)

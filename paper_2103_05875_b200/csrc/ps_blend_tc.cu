@@ -412,6 +412,15 @@ __global__ void __launch_bounds__(THREADS, PS_BLEND_CTAS)
     mbar_wait(&done, 0);
     tc_fence_after();
 
+#ifdef PS_BLEND_NO_EPILOGUE  // tuning: time the main loop alone
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                     "r"(TMEM_COLS));
+    }
+    return;
+#endif
     // ---- epilogue: TMEM -> state + quantised cores (staged in the freed stages) -----------
     uint32_t *s_ccore = reinterpret_cast<uint32_t *>(stages);  // [P][64]
     uint32_t *s_vcore = s_ccore + P * 64;                      // [P][256]

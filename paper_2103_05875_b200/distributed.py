@@ -80,11 +80,25 @@ def _env_flag(name: str, default: bool) -> bool:
     return default if v is None else v not in ("0", "false", "no", "")
 
 
-def slab_range(volume, rank: int, world: int):
-    """[begin, end) of rank's z-slab: whole k-planes, balanced."""
+def _encoder_share() -> float:
+    return float(os.environ.get("PS_ENCODER_SHARE", "1.0"))
+
+
+def slab_range(volume, rank: int, world: int, encoder_share: float | None = None):
+    """[begin, end) of rank's z-slab.  encoder_share = 1: whole k-planes,
+    equal.  < 1: rank 0 (the encoder, which also packs the whole update
+    atlas) gets that fraction of an equal share and the others split the rest,
+    cut at rows of nx probes (PS_ENCODER_SHARE)."""
     nx, ny, nz = volume.dims
     plane = nx * ny
-    return (nz * rank) // world * plane, (nz * (rank + 1)) // world * plane
+    share = _encoder_share() if encoder_share is None else encoder_share
+    if world == 1 or share >= 1.0:
+        return (nz * rank) // world * plane, (nz * (rank + 1)) // world * plane
+    rows = ny * nz
+    weights = [share] + [1.0] * (world - 1)
+    total = sum(weights)
+    cut = lambda r: int(round(rows * sum(weights[:r]) / total))
+    return cut(rank) * nx, cut(rank + 1) * nx
 
 
 def ranges_from_cost(n_units: int, unit: int, world: int, unit_cost) -> list:
