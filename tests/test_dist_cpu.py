@@ -149,3 +149,26 @@ def test_cost_balanced_ranges():
     assert [(e - b) // plane for b, e in r] == [1] * 8
     r = ranges_from_cost(8, plane, 4, [1.0] * 7 + [100.0])
     assert r[-1] == (7 * plane, 8 * plane) and min(e - b for b, e in r) >= plane
+
+
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
+@pytest.mark.parametrize("share", [1.0, 0.88, 0.5])
+def test_slab_ranges_partition_the_volume(world, share):
+    """Slabs tile [0, n) in rank order, at whole rows of nx probes (whole
+    k-planes at share 1), with the encoder's reduced share when asked."""
+    from paper_2103_05875_b200.distributed import slab_range
+
+    class V:
+        dims = (64, 32, 64)
+
+    n = 64 * 32 * 64
+    r = [slab_range(V, k, world, share) for k in range(world)]
+    assert r[0][0] == 0 and r[-1][1] == n
+    assert all(a[1] == b[0] for a, b in zip(r, r[1:]))
+    assert all(b % 64 == 0 and e % 64 == 0 and e > b for b, e in r)
+    if share == 1.0:
+        assert all(b % (64 * 32) == 0 for b, _ in r)
+    else:
+        sizes = [e - b for b, e in r]
+        assert sizes[0] < min(sizes[1:])
+        assert abs(sizes[0] / (sum(sizes[1:]) / (world - 1)) - share) < 0.05
