@@ -304,6 +304,32 @@ __device__ __forceinline__ void issue_mma(const float *st, uint32_t tmem, int c)
     mma_tf32(tmem + COL_C, a_c, b_cl, ID_C, 1u);
 }
 
+// the guard-banded SIDE x SIDE blocks of probes p0 .. p0 + nq - 1, from their
+// quantised cores staged in shared memory (core[q * CORE_WORDS + i])
+template <int SIDE, int NJ>
+__device__ __forceinline__ void write_blocks(uint32_t *atlas, int ppr, int p0, int nq,
+                                             const uint32_t *core, int core_words, int warp,
+                                             int lane) {
+    static_assert(NJ * 32 >= SIDE * SIDE, "NJ words per lane cover the block");
+    int src[NJ], off[NJ];
+    const int W = ppr * SIDE;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+        const int k = lane + 32 * j;
+        const int r = k / SIDE, c = k - (k / SIDE) * SIDE;
+        src[j] = k < SIDE * SIDE ? guard_source(r, c, SIDE) : -1;
+        off[j] = r * W + c;
+    }
+    for (int q = warp; q < nq; q += THREADS / 32) {
+        const int p = p0 + q, by = p / ppr;
+        uint32_t *blk = atlas + size_t(by) * SIDE * W + size_t(p - by * ppr) * SIDE;
+        const uint32_t *cq = core + q * core_words;
+#pragma unroll
+        for (int j = 0; j < NJ; ++j)
+            if (src[j] >= 0) blk[off[j]] = cq[src[j]];
+    }
+}
+
 __global__ void __launch_bounds__(THREADS, PS_BLEND_CTAS)
     blend_tc_kernel(ps_trace_params prm, int rotate) {
     extern __shared__ unsigned char smem_raw[];
@@ -526,33 +552,13 @@ __global__ void __launch_bounds__(THREADS, PS_BLEND_CTAS)
     __syncthreads();
 
     // ---- atlas blocks with guard bands -------------------------------------------------------
-    {
-        const int ppr = prm.probes_per_row_color;
-        const int W = ppr * 10;
-        const int pb = int(p0);
-        for (int idx = tid; idx < nq * 100; idx += THREADS) {
-            const int qq = idx / 100, k = idx - qq * 100;
-            const int r = k / 10, c = k - r * 10;
-            const int p = pb + qq;
-            const int by = p / ppr;
-            const int y0 = by * 10, x0 = (p - by * ppr) * 10;
-            prm.color_atlas[size_t(y0 + r) * W + x0 + c] = s_ccore[qq * 64 + guard_source(r, c, 10)];
-        }
-    }
-    {
-        const int ppr = prm.probes_per_row_vis;
-        const int W = ppr * 18;
-        const int pb = int(p0);
-        uint32_t *vis = reinterpret_cast<uint32_t *>(prm.vis_atlas);
-        for (int idx = tid; idx < nq * 324; idx += THREADS) {
-            const int qq = idx / 324, k = idx - qq * 324;
-            const int r = k / 18, c = k - r * 18;
-            const int p = pb + qq;
-            const int by = p / ppr;
-            const int y0 = by * 18, x0 = (p - by * ppr) * 18;
-            vis[size_t(y0 + r) * W + x0 + c] = s_vcore[qq * 256 + guard_source(r, c, 18)];
-        }
-    }
+    // a warp writes whole probe blocks: one block-origin division per probe,
+    // and each lane's guard-band source indices (its words k = lane + 32 j of
+    // the 10 x 10 / 18 x 18 block) computed once, not per word
+    write_blocks<10, 4>(prm.color_atlas, prm.probes_per_row_color, int(p0), nq, s_ccore, 64, warp,
+                        lane);
+    write_blocks<18, 11>(reinterpret_cast<uint32_t *>(prm.vis_atlas), prm.probes_per_row_vis,
+                         int(p0), nq, s_vcore, 256, warp, lane);
     if (warp == 0) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
