@@ -43,6 +43,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <type_traits>
 
 #include "ps_common.cuh"
 #include "ps_guard.cuh"
@@ -490,64 +491,72 @@ __global__ void __launch_bounds__(THREADS, PS_BLEND_CTAS)
     }
     // colour: TMEM lanes 0-63 hold W_hi*B (+ W_hi*B_lo) of the 64 texels, lanes
     // 64-127 the W_lo*B_hi terms of the same texels; warp half h owns probes
-    // h*16..h*16+15.  Warps of lane quarters 2-3 hand their partials over
-    // through shared memory to the warps of quarters 0-1, which finish.
-    float *xbuf = reinterpret_cast<float *>(s_vcore + P * 256);  // [half][ch][t][i]
+    // h*16..h*16+15.  A warp can only read its own TMEM lane quarter, so the
+    // hi warps (quarters 0-1) and the lo warps (quarters 2-3) trade halves
+    // through shared memory: the hi warps finish probes 0-7 of the half, the
+    // lo warps probes 8-15 -- every warp finishes 8 probes of 32 texels.
+    float *xbuf = reinterpret_cast<float *>(s_vcore + P * 256);  // [half][hi|lo][ch][t][8]
     const int q0c = half * (P / 2);
     static_assert(P / 2 == 16, "one 16-column TMEM load per channel");
     const uint32_t cbase = lane_base + COL_C;
-    if (sub >= 2) {
-        const int t = (sub - 2) * 32 + lane;
-        float v[16];
+    const bool hi_warp = sub < 2;
+    const int tcol = (sub & 1) * 32 + lane;  // this lane's colour texel (both roles)
+    float own[3][16];
 #pragma unroll
-        for (int ch = 0; ch < 3; ++ch) {
-            tmem_ld16(cbase + ch * P + q0c, v);
+    for (int ch = 0; ch < 3; ++ch) tmem_ld16(cbase + ch * P + q0c, own[ch]);
+    // own[] is indexed with compile-time offsets only (a run-time offset would
+    // put the array in local memory): the two roles are two instantiations
+    auto give_half = [&](auto GIVE) {  // hi warps give probes 8-15, lo warps 0-7
+        constexpr int give = decltype(GIVE)::value;
+        float *xo = xbuf + ((half * 2 + (give ? 0 : 1)) * 3) * 64 * 8;
 #pragma unroll
-            for (int i = 0; i < 16; ++i) xbuf[((half * 3 + ch) * 64 + t) * 16 + i] = v[i];
-        }
-    }
-    float old[16][3];
-    float cr[16], cg[16], cb[16];
-    const int tc_ = sub * 32 + lane;
-    const float inv_c = sub < 2 ? __ldg(prm.inv_wsum + tc_) : 0.f;
+        for (int ch = 0; ch < 3; ++ch)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) xo[(ch * 64 + tcol) * 8 + i] = own[ch][give + i];
+    };
+    if (hi_warp)
+        give_half(std::integral_constant<int, 8>());
+    else
+        give_half(std::integral_constant<int, 0>());
+    const int keep = hi_warp ? 0 : 8;  // probes this warp finishes: q0c + keep + 0..7
+    const float inv_c = __ldg(prm.inv_wsum + tcol);
     const bool need_old_c = inv_c == 0.f || h != 0.f;
-    if (sub < 2) {
+    float old[8][3];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            const float *st = prm.irradiance + ((pl0 + q0c + i) * 64 + tc_) * 3;
-            const bool ld = need_old_c && q0c + i < nq;
+    for (int i = 0; i < 8; ++i) {
+        const int qq = q0c + keep + i;
+        const float *st = prm.irradiance + ((pl0 + qq) * 64 + tcol) * 3;
+        const bool ld = need_old_c && qq < nq;
 #pragma unroll
-            for (int ch = 0; ch < 3; ++ch) old[i][ch] = ld ? __ldcs(st + ch) : 0.f;
-        }
-        tmem_ld16(cbase + q0c, cr);
-        tmem_ld16(cbase + P + q0c, cg);
-        tmem_ld16(cbase + 2 * P + q0c, cb);
+        for (int ch = 0; ch < 3; ++ch) old[i][ch] = ld ? __ldcs(st + ch) : 0.f;
     }
-    __syncthreads();  // the lo partials are in xbuf
-    if (sub < 2) {
-        const int t = tc_;
-        const float *xr = xbuf + ((half * 3 + 0) * 64 + t) * 16;
-        const float *xg = xbuf + ((half * 3 + 1) * 64 + t) * 16;
-        const float *xb = xbuf + ((half * 3 + 2) * 64 + t) * 16;
+    __syncthreads();  // both halves are in xbuf
+    auto finish = [&](auto KEEP) {
+        constexpr int kp = decltype(KEEP)::value;
+        const float *xi = xbuf + ((half * 2 + (kp ? 0 : 1)) * 3) * 64 * 8;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            const int qq = q0c + i;
+        for (int i = 0; i < 8; ++i) {
+            const int qq = q0c + kp + i;
             if (qq >= nq) break;
-            float *st = prm.irradiance + ((pl0 + qq) * 64 + t) * 3;
-            const float acc[3] = {cr[i] + xr[i], cg[i] + xg[i], cb[i] + xb[i]};
+            float *st = prm.irradiance + ((pl0 + qq) * 64 + tcol) * 3;
             uint32_t texel = 0;
 #pragma unroll
             for (int ch = 0; ch < 3; ++ch) {
-                float v = acc[ch] * inv_c;
+                const float acc = own[ch][kp + i] + xi[(ch * 64 + tcol) * 8 + i];
+                float v = acc * inv_c;
                 if (inv_c == 0.f) v = old[i][ch];  // no ray sees this texel: keep the state
                 else if (h != 0.f) v = fmaf(h, old[i][ch] - v, v);
                 __stcs(st + ch, v);
                 const float x = fminf(fmaxf(v * qs, 0.0f), 1.0f);
                 texel |= __float2uint_rn(x * 1023.0f) << (10 * ch);
             }
-            s_ccore[qq * 64 + t] = texel;
+            s_ccore[qq * 64 + tcol] = texel;
         }
-    }
+    };
+    if (hi_warp)
+        finish(std::integral_constant<int, 0>());
+    else
+        finish(std::integral_constant<int, 8>());
     tc_fence_before();
     __syncthreads();
 
