@@ -276,8 +276,12 @@ def run_ours(args, rank, world, local):
     ms = start.elapsed_time(end) / args.steps
     # probes selected (= entries written) in the last timed frame, per kind:
     # the full-volume update means every probe, every frame
-    selected = {k: (int(o.entry_count.item()) if o is not None else None)
+    selected = {k: (int(o.entry_count.item()) if o is not None else -1)
                 for k, o in zip(("color", "visibility"), outs)}
+    if world > 1:  # each kind's outputs live on its encoder rank
+        t = torch.tensor([selected["color"], selected["visibility"]], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        selected = {"color": int(t[0]), "visibility": int(t[1])}
     ms_max = ms
     if world > 1:
         t = torch.tensor([ms], device=dev)
@@ -291,6 +295,11 @@ def run_ours(args, rank, world, local):
         t = torch.tensor([e2e_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
+        # host I/O of the whole job: every rank's H2D, each encoder rank's D2H
+        b = torch.tensor([e2e["h2d_bytes_per_step"], e2e["d2h_bytes_per_step"]], device=dev,
+                         dtype=torch.int64)
+        dist.all_reduce(b, op=dist.ReduceOp.SUM)
+        e2e["h2d_bytes_per_step"], e2e["d2h_bytes_per_step"] = int(b[0]), int(b[1])
 
     e2e_enc = server.run_e2e_encoded(args.steps, args.warmup + 2 * args.steps + 40,
                                      frame_lights) if world == 1 else {}
@@ -358,6 +367,8 @@ def run_ours(args, rank, world, local):
                           if getattr(getattr(server.impl, "color", None), "peer", False)
                           else "NCCL") if world > 1 else None),
             "peer_ranks_mapped": peer_ranks,
+            "encoder_ranks": (dict(zip(("color", "visibility"), server.impl.encoders))
+                              if world > 1 else None),
         },
         "selected_last_frame": selected,
         "grays_per_s": round(rays_total / (ms_max / 1e3) / 1e9, 4),
@@ -367,7 +378,8 @@ def run_ours(args, rank, world, local):
         "packed_atlas_gbs": round(achieved, 1) if achieved else None,
         "roofline": {
             "bound": "hbm",
-            "kernel": "pack_delta_kernel (colour + visibility)",
+            "kernel": "pack_delta_kernel (colour + visibility)" if world == 1 else
+                      "pack_delta_kernel (the kinds rank 0 encodes: colour)",
             "achieved": round(achieved, 1) if achieved else None,
             "peak": peak,
             "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}, burst copy)",
@@ -579,6 +591,16 @@ def main():
     # (version banner, communicator lines at NCCL_DEBUG=INFO) goes to stderr
     if not os.environ.get("NCCL_DEBUG_FILE"):
         os.environ["NCCL_DEBUG_FILE"] = "/dev/stderr"
+    # NCCL_DEBUG=VERSION prints its banner to stdout whatever NCCL_DEBUG_FILE
+    # says: log the version to stderr instead (INFO / TRACE lines go to the file)
+    if os.environ.get("NCCL_DEBUG", "").upper() == "VERSION":
+        os.environ["NCCL_DEBUG"] = "WARN"
+        try:
+            import torch
+
+            log("NCCL version", ".".join(map(str, torch.cuda.nccl.version())))
+        except Exception:
+            pass
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=40)

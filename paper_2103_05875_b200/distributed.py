@@ -492,7 +492,7 @@ class DistKindStream:
 class DistributedFrame:
     """One client session's hot path sharded over the process group."""
 
-    def __init__(self, volume, scene, rays_per_probe, device, rank, world, encoder=0,
+    def __init__(self, volume, scene, rays_per_probe, device, rank, world, encoder=None,
                  color_threshold=0.0, visibility_threshold=0.0, slot_count=None, budget=None,
                  gop_length=DEFAULT_GOP, overlap: bool = True, graphs: bool = False,
                  balance: bool = _env_flag("PS_BALANCE", False),
@@ -535,12 +535,24 @@ class DistributedFrame:
         self._buf_done = [[], []]
         self._pending = []
         ppr = self.updater.color.probes_per_row
-        kw = dict(encoder=encoder, slot_count=slot_count, gop_length=gop_length, budget=budget,
+        # encoder ranks per kind: colour and visibility are separate encoder
+        # streams, so by default they are packed on different ranks (colour on
+        # rank 0, visibility on rank 1): the encoder-serial pack of the whole
+        # update atlas, which the other ranks never do, is split over two ranks.
+        # encoder=r puts both on rank r; PS_SPLIT_ENCODERS=0 the same for r = 0.
+        if encoder is None:
+            split = _env_flag("PS_SPLIT_ENCODERS", True) and world > 1
+            encoder = (0, 1 if split else 0)
+        elif isinstance(encoder, int):
+            encoder = (encoder, encoder)
+        self.encoders = tuple(int(e) for e in encoder)
+        kw = dict(slot_count=slot_count, gop_length=gop_length, budget=budget,
                   probes_per_row=ppr, peer=peer)
         self.color = DistKindStream(AtlasKind.COLOR, volume, device, rank, world, self.ranges,
-                                    threshold=color_threshold, **kw)
+                                    encoder=self.encoders[0], threshold=color_threshold, **kw)
         self.visibility = DistKindStream(AtlasKind.VISIBILITY, volume, device, rank, world,
-                                         self.ranges, threshold=visibility_threshold, **kw)
+                                         self.ranges, encoder=self.encoders[1],
+                                         threshold=visibility_threshold, **kw)
         self.seq = 0
         self.timers = None
         self.enable_graphs(graphs)

@@ -40,15 +40,21 @@ def main():
     kw = dict(irradiance_scale=2.0, shadows="map", shadow_map_size=128, gop_length=args.gop)
     frame = DistributedFrame(vol, sc, rays, dev, rank, world, graphs=args.graphs, peer=not args.nccl,
                              **kw)
-    single = ProbeStreamServer(vol, sc, rays, device=dev, **kw) if rank == 0 else None
+    # each kind is checked on its encoder rank (colour on rank 0, visibility on
+    # rank 1 by default), against a single-GPU server on that rank
+    enc = frame.encoders
+    single = ProbeStreamServer(vol, sc, rays, device=dev, **kw) if rank in enc else None
     ok = True
     for f in range(args.frames):
         lights = S.moving_light(sc, f).lights
         outs = frame.tick(f, lights)
-        if rank == 0:
+        if single is not None:
             ref = single.tick(f, lights)
             torch.cuda.synchronize()
-            for name, a, b in zip(("color", "visibility"), outs, ref):
+            for name, a, b, e in zip(("color", "visibility"), outs, ref, enc):
+                if e != rank:
+                    assert a is None, "outputs on a rank that does not encode the kind"
+                    continue
                 n = int(b.entry_count.item())
                 same = (int(a.entry_count.item()) == n
                         and torch.equal(a.entries[:n], b.entries[:n])
@@ -56,7 +62,8 @@ def main():
                         and torch.equal(a.skip, b.skip)
                         and (b.key or torch.equal(a.residual.view(torch.uint8),
                                                   b.residual.view(torch.uint8))))
-                print(f"frame {f} {name}: entries {n} bit-identical={same}", flush=True)
+                print(f"frame {f} {name} (rank {rank}): entries {n} bit-identical={same}",
+                      flush=True)
                 ok &= same
     flag = torch.tensor([1 if ok else 0], device=dev)
     dist.all_reduce(flag, op=dist.ReduceOp.MIN)
