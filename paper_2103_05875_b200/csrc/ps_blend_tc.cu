@@ -334,8 +334,11 @@ __device__ __forceinline__ void write_blocks(uint32_t *atlas, int ppr, int p0, i
 __global__ void __launch_bounds__(THREADS, PS_BLEND_CTAS)
     blend_tc_kernel(ps_trace_params prm, int rotate) {
     extern __shared__ unsigned char smem_raw[];
-    float *stages = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                              ~uintptr_t(1023));
+    // 1024-byte aligned by offsetting the shared array itself (an integer round
+    // trip through uintptr_t would lose the shared address space and turn every
+    // ring read, operand-image write and epilogue staging access into a
+    // generic 64-bit LD / ST instead of LDS / STS)
+    float *stages = reinterpret_cast<float *>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
     __shared__ __align__(8) uint64_t a_full[STAGES], b_full[STAGES], empty[STAGES], done;
     __shared__ uint32_t s_tmem;
 
