@@ -431,6 +431,12 @@ __global__ void __launch_bounds__(THREADS, PS_BLEND_CTAS)
                 const int s = c % STAGES, u = c / STAGES;
                 if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
                 // the k-step's five operand images are contiguous in the weight image
+#ifdef PS_BLEND_NO_WEIGHT_TRAFFIC  // tuning only (wrong results): weights loaded once
+                if (c >= STAGES) {
+                    mbar_arrive(&a_full[s]);
+                    continue;
+                }
+#endif
                 mbar_expect_tx(&a_full[s], A_LOAD_BYTES);
                 bulk_g2s(stages + s * STAGE, prm.w_image + size_t(kstep(c)) * A_FLOATS,
                          A_LOAD_BYTES, &a_full[s]);
