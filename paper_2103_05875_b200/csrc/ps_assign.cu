@@ -13,7 +13,7 @@
 // id list (ids -> bits -> compaction -> plan -> bind -> stamp -> entry bits ->
 // compaction); here the selection stays a bitmap:
 //
-//   bind_kernel    (one pass over the selection words): per 1024-probe warp
+//   bind_kernel    (one pass over the selection words): per 128-probe warp
 //                  span, coalesced probe_slot reads -> ballot masks of new
 //                  probes; warp / block / cross-tile (look-back) prefix of
 //                  (selected, new) counts; then new ids, both slot maps and
@@ -33,8 +33,17 @@ namespace {
 
 constexpr int AS_THREADS = 256;                 // 8 warps
 constexpr int AS_WARPS = AS_THREADS / 32;
-constexpr int64_t AS_SPAN = 1024;               // probes (or slots) per warp
-constexpr int64_t AS_TILE = AS_SPAN * AS_WARPS;  // 8192 per CTA tile
+// bitmap words per warp (PS_AS_SPAN_WORDS, tuning): 4 words = 128 probes per
+// warp puts 128 CTAs on the GPU at C4 instead of 16 with 1,024-probe spans
+// (C5 N=131,072 graphed chains, spans of 32 / 8 / 4 words: colour 0.134 /
+// 0.129 / 0.125 ms, visibility 0.293 / 0.287 / 0.284 ms)
+#ifndef PS_AS_SPAN_WORDS
+#define PS_AS_SPAN_WORDS 4
+#endif
+constexpr int SPAN_WORDS = PS_AS_SPAN_WORDS;
+static_assert(SPAN_WORDS >= 1 && SPAN_WORDS <= 32, "span words");
+constexpr int64_t AS_SPAN = 32 * SPAN_WORDS;    // probes (or slots) per warp
+constexpr int64_t AS_TILE = AS_SPAN * AS_WARPS;  // 1,024 per CTA tile
 
 constexpr uint64_t FLAG_AGG = 1ull << 62, FLAG_PREFIX = 2ull << 62;
 constexpr uint64_t VAL_MASK = (1ull << 62) - 1;
@@ -118,7 +127,7 @@ __global__ void __launch_bounds__(AS_THREADS)
     const int64_t words = (n + 31) / 32;
     // lane b holds word b of this warp's span: selection and new-probe masks
     uint32_t selw = 0, neww = 0;
-    {
+    if (lane < SPAN_WORDS) {
         const int64_t w = span0 / 32 + lane;
         if (w < words) {
             selw = sel_bits[w];
@@ -126,8 +135,8 @@ __global__ void __launch_bounds__(AS_THREADS)
             if (w == words - 1 && (n & 31)) selw &= (1u << (n & 31)) - 1u;
         }
     }
-#pragma unroll 4
-    for (int b = 0; b < 32; ++b) {
+#pragma unroll
+    for (int b = 0; b < SPAN_WORDS; ++b) {
         const uint32_t sw = __shfl_sync(0xffffffffu, selw, b);
         const int64_t p = span0 + b * 32 + lane;
         const bool sel = (sw >> lane) & 1u;
@@ -159,7 +168,7 @@ __global__ void __launch_bounds__(AS_THREADS)
     }
     __syncthreads();
     int64_t rank = int64_t((s_base + woff) & 0x7fffffffu);  // new probes before this warp
-    for (int b = 0; b < 32; ++b) {
+    for (int b = 0; b < SPAN_WORDS; ++b) {
         const uint32_t nm = __shfl_sync(0xffffffffu, neww, b);
         const uint32_t sm = __shfl_sync(0xffffffffu, selw, b);
         const int64_t p = span0 + b * 32 + lane;
@@ -185,14 +194,14 @@ __global__ void __launch_bounds__(AS_THREADS)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t span0 = tile * AS_TILE + int64_t(warp) * AS_SPAN;
     uint32_t emask = 0;
-    int32_t q[32];
+    int32_t q[SPAN_WORDS];
 #pragma unroll
-    for (int b = 0; b < 32; ++b) {
+    for (int b = 0; b < SPAN_WORDS; ++b) {
         const int64_t s = span0 + b * 32 + lane;
         q[b] = s < slot_count ? slot_probe[s] : -1;
     }
 #pragma unroll
-    for (int b = 0; b < 32; ++b) {
+    for (int b = 0; b < SPAN_WORDS; ++b) {
         bool hit = false;
         if (q[b] >= 0 && q[b] < n) {
             uint32_t w = sel_bits[q[b] >> 5];
@@ -215,7 +224,7 @@ __global__ void __launch_bounds__(AS_THREADS)
     __syncthreads();
     int64_t rank = int64_t(s_base + woff);
 #pragma unroll
-    for (int b = 0; b < 32; ++b) {
+    for (int b = 0; b < SPAN_WORDS; ++b) {
         const uint32_t m = __shfl_sync(0xffffffffu, emask, b);
         if ((m >> lane) & 1u) {
             const int64_t k = rank + __popc(m & ((1u << lane) - 1u));

@@ -867,6 +867,10 @@ void launch_trace_s(const ps_trace_params &p, int variant, int sms, cudaStream_t
             case 88: launch_trace_640<SHADOW, 0, 12, 20>(p, sms, s); break;  // word selects
             case 89: launch_trace_640<SHADOW, 0, 12, 21>(p, sms, s); break;  // vote >= 3/4
             case 91: launch_trace_640<SHADOW, 0, 12, 22>(p, sms, s); break;  // vote >= 1/2
+            case 92: launch_trace_640<SHADOW, 0, 12, 23>(p, sms, s); break;  // half2 slabs
+            // traversal statistics of 84 / 92 (tuning only, ps_trace_stats)
+            case 93: launch_trace_640<SHADOW, 0, 12, 24>(p, sms, s); break;
+            case 94: launch_trace_640<SHADOW, 0, 12, 25>(p, sms, s); break;
             case 85: launch_trace_640<SHADOW, 0, 12, 3>(p, sms, s); break;  // plain loop
             default: launch_trace_640<SHADOW, 0, 12, 19>(p, sms, s); break;
         }

@@ -491,6 +491,93 @@ __device__ __forceinline__ void node4ho_switch(const float4 *nodes, int node, in
 #undef PS_OCTS_CASE
 }
 
+// ---- fp16 slab arithmetic (WIDTH 23) ----------------------------------------------
+// The node test of node4ho_hits in packed half2 arithmetic: one HFMA2 computes
+// a plane's t for two children at once straight from the node's fp16 words
+// (no fp16 -> fp32 conversions), HMNMX2 reduces the slabs.  The result is
+// conservative -- a child the exact slab test accepts is never rejected --
+// so the set of tested triangles only grows and the nearest hit (an fp32
+// triangle test) is unchanged:
+//   t' = rn(b * I + C) with, per axis, near-plane  I_n = rd(|1/d| (1 - 2^-10)),
+//   C_n = rd(-o I_n) and far-plane I_f = ru(|1/d| (1 + 2^-10)), C_f = ru(-o I_f)
+//   (magnitudes; sign of d applied).  For t >= 0 the 2^-10 scaling covers the
+//   final rounding (<= 2^-11 relative), so near t' <= t and far t' >= t.
+// An axis whose constants would leave the fp16 range (|o / d| >~ 6e4) is
+// dropped from the test (I = 0, C = -inf / +inf): also conservative.
+struct HalfSlabs {
+    __half2 i[3];  // (I_near, I_far) per axis
+    __half2 c[3];  // (C_near, C_far)
+};
+
+#ifndef PS_HALF_SLACK
+#define PS_HALF_SLACK (1.0f / 1024.0f)
+#endif
+__device__ __forceinline__ void half_axis(float o, float s, __half2 &I, __half2 &C) {
+    const float mag = fabsf(1.0f / s);
+    const float mn = mag * (1.0f - PS_HALF_SLACK), mf = mag * (1.0f + PS_HALF_SLACK);
+    if (mf < 60000.0f && mf * fabsf(o) < 60000.0f) {
+        const float in_ = copysignf(__half2float(__float2half_rd(mn)), s);
+        const float if_ = copysignf(__half2float(__float2half_ru(mf)), s);
+        I = __halves2half2(__float2half_rn(in_), __float2half_rn(if_));  // exact
+#ifdef PS_HALF_C_RN  // tuning only: not conservative
+        C = __halves2half2(__float2half_rn(-o * in_), __float2half_rn(-o * if_));
+#else
+        C = __halves2half2(__float2half_rd(__fmul_rd(-o, in_)), __float2half_ru(__fmul_ru(-o, if_)));
+#endif
+    } else {
+        I = __floats2half2_rn(0.0f, 0.0f);
+        C = __floats2half2_rn(-INFINITY, INFINITY);
+    }
+}
+
+template <int OCT>
+__device__ __forceinline__ void node4hh_hits(const float4 *nodes, int node, const HalfSlabs &h,
+                                             __half tbh, float d[4], int c[4]) {
+    constexpr bool NX = OCT & 1, NY = OCT & 2, NZ = OCT & 4;
+    const float4 *nd = nodes + 4 * node;
+    float a[8], b[8];
+    ldg256(nd + 0, a);  // lo_x[4] hi_x[4] | lo_y[4] hi_y[4] (halves)
+    ldg256(nd + 2, b);  // lo_z[4] hi_z[4] | child[4]
+    auto hw = [](float w) { return *reinterpret_cast<const __half2 *>(&w); };
+    const __half2 tb2 = __half2half2(tbh);
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {  // children (2j, 2j+1)
+        const __half2 nx = __hfma2(hw(NX ? a[2 + j] : a[j]), __low2half2(h.i[0]), __low2half2(h.c[0]));
+        const __half2 fx = __hfma2(hw(NX ? a[j] : a[2 + j]), __high2half2(h.i[0]), __high2half2(h.c[0]));
+        const __half2 ny = __hfma2(hw(NY ? a[6 + j] : a[4 + j]), __low2half2(h.i[1]), __low2half2(h.c[1]));
+        const __half2 fy = __hfma2(hw(NY ? a[4 + j] : a[6 + j]), __high2half2(h.i[1]), __high2half2(h.c[1]));
+        const __half2 nz = __hfma2_relu(hw(NZ ? b[2 + j] : b[j]), __low2half2(h.i[2]), __low2half2(h.c[2]));
+        const __half2 fz = __hfma2(hw(NZ ? b[j] : b[2 + j]), __high2half2(h.i[2]), __high2half2(h.c[2]));
+        const __half2 tn = __hmax2(__hmax2(nx, ny), nz);
+        const __half2 tf = __hmin2(__hmin2(fx, fy), __hmin2(fz, tb2));
+        const uint32_t m = __hle2_mask(tn, tf);
+        const uint32_t sel = (*reinterpret_cast<const uint32_t *>(&tn) & m) | (0x7C007C00u & ~m);
+        const float2 f = __half22float2(*reinterpret_cast<const __half2 *>(&sel));
+        d[2 * j] = f.x;
+        d[2 * j + 1] = f.y;
+        c[2 * j] = __float_as_int(b[4 + 2 * j]);
+        c[2 * j + 1] = __float_as_int(b[5 + 2 * j]);
+    }
+    cswap(d[0], c[0], d[1], c[1]);
+    cswap(d[2], c[2], d[3], c[3]);
+    cswap(d[0], c[0], d[2], c[2]);
+    cswap(d[1], c[1], d[3], c[3]);
+    cswap(d[1], c[1], d[2], c[2]);
+}
+
+__device__ __forceinline__ void node4hh_switch(const float4 *nodes, int node, int oct,
+                                               const HalfSlabs &h, __half tbh, float d[4],
+                                               int c[4]) {
+#define PS_OCTH_CASE(o) \
+    case o: node4hh_hits<o>(nodes, node, h, tbh, d, c); break;
+    switch (oct) {
+        PS_OCTH_CASE(0) PS_OCTH_CASE(1) PS_OCTH_CASE(2) PS_OCTH_CASE(3)
+        PS_OCTH_CASE(4) PS_OCTH_CASE(5) PS_OCTH_CASE(6)
+        default: node4hh_hits<7>(nodes, node, h, tbh, d, c);
+    }
+#undef PS_OCTH_CASE
+}
+
 // Speculative while-while traversal (Aila & Laine 2009) over the fp16-box
 // BVH4: a lane that reaches a leaf parks it and keeps walking inner nodes
 // until every lane still in the loop holds a leaf (warp vote), then the
@@ -504,7 +591,7 @@ constexpr int TRAV_DONE = -1;  // leaf refs are ~(first << 3 | count), count >= 
 // SEL: node test with per-axis word selects (node4hs_hits) instead of the
 // octant switch; VOTE: leave the node phase when all (0), >= 3/4 (1) or >= 1/2
 // (2) of the lanes still walking hold a parked leaf
-template <bool ANY_HIT, int SEL = 0, int VOTE = 0>
+template <bool ANY_HIT, int SEL = 0, int VOTE = 0, int HALF = 0, int STATS = 0>
 __device__ int traverse_spec(const float4 *__restrict__ nodes, const float4 *__restrict__ tris,
                              const Ray &r, float tmax, float &t_best) {
     const float sx = fabsf(r.dx) < 1e-12f ? copysignf(1e-12f, r.dx) : r.dx;
@@ -513,6 +600,14 @@ __device__ int traverse_spec(const float4 *__restrict__ nodes, const float4 *__r
     const int oct = (sx < 0.0f ? 1 : 0) | (sy < 0.0f ? 2 : 0) | (sz < 0.0f ? 4 : 0);
     const float ix = 1.0f / sx, iy = 1.0f / sy, iz = 1.0f / sz;
     const float oix = r.ox * ix, oiy = r.oy * iy, oiz = r.oz * iz;
+    HalfSlabs hs;
+    if (HALF) {
+        half_axis(r.ox, sx, hs.i[0], hs.c[0]);
+        half_axis(r.oy, sy, hs.i[1], hs.c[1]);
+        half_axis(r.oz, sz, hs.i[2], hs.c[2]);
+    }
+    __half tbh = __float2half_ru(tmax);
+    unsigned long long st_nodes = 0, st_leaves = 0, st_tris = 0;
     int2 stack[STACK];
     int sp = 0;
     int node = 0, leaf = 0;  // leaf: parked leaf ref (0 = none)
@@ -530,7 +625,10 @@ __device__ int traverse_spec(const float4 *__restrict__ nodes, const float4 *__r
         while (node >= 0) {
             float d[4];
             int c[4];
-            if (SEL)
+            if (STATS) ++st_nodes;
+            if (HALF)
+                node4hh_switch(nodes, node, oct, hs, tbh, d, c);
+            else if (SEL)
                 node4hs_hits(nodes, node, ix, iy, iz, oix, oiy, oiz, t_best, oct & 1, oct & 2,
                              oct & 4, d, c);
             else
@@ -559,6 +657,10 @@ __device__ int traverse_spec(const float4 *__restrict__ nodes, const float4 *__r
         while (leaf != 0) {
             const int ref = ~leaf;
             const int first = ref >> 3, cnt = ref & 7;
+            if (STATS) {
+                ++st_leaves;
+                st_tris += cnt;
+            }
             for (int k = 0; k < cnt; ++k) {
                 const float t = tri_hit(r, __ldg(tris + 3 * (first + k)),
                                         __ldg(tris + 3 * (first + k) + 1),
@@ -569,12 +671,19 @@ __device__ int traverse_spec(const float4 *__restrict__ nodes, const float4 *__r
                     if (ANY_HIT) return hit_slot;
                 }
             }
+            if (HALF) tbh = __float2half_ru(t_best);
             leaf = 0;
             if (node < TRAV_DONE) {  // the walk stopped on another leaf
                 leaf = node;
                 node = pop();
             }
         }
+    }
+    if (STATS) {
+        atomicAdd(&g_trav_stats[0], st_nodes);
+        atomicAdd(&g_trav_stats[1], st_leaves);
+        atomicAdd(&g_trav_stats[2], st_tris);
+        atomicAdd(&g_trav_stats[3], 1ull);
     }
     return hit_slot;
 }
@@ -587,6 +696,9 @@ __device__ int traverse(const float4 *__restrict__ nodes, const float4 *__restri
     if constexpr (WIDTH == 20) return traverse_spec<ANY_HIT, 1>(nodes, tris, r, tmax, t_best);
     if constexpr (WIDTH == 21) return traverse_spec<ANY_HIT, 0, 1>(nodes, tris, r, tmax, t_best);
     if constexpr (WIDTH == 22) return traverse_spec<ANY_HIT, 0, 2>(nodes, tris, r, tmax, t_best);
+    if constexpr (WIDTH == 23) return traverse_spec<ANY_HIT, 0, 0, 1>(nodes, tris, r, tmax, t_best);
+    if constexpr (WIDTH == 24) return traverse_spec<ANY_HIT, 0, 0, 0, 1>(nodes, tris, r, tmax, t_best);
+    if constexpr (WIDTH == 25) return traverse_spec<ANY_HIT, 0, 0, 1, 1>(nodes, tris, r, tmax, t_best);
     unsigned long long st_nodes = 0, st_leaves = 0, st_tris = 0;
     // reciprocal direction; tiny components replaced so the slabs stay finite
     const float sx = fabsf(r.dx) < 1e-12f ? copysignf(1e-12f, r.dx) : r.dx;

@@ -41,7 +41,7 @@ from .packing import UpdateAtlasLayout, widened_width
 from .probes import ProbeUpdater
 from .scene import DeviceScene
 from .selection import _threshold_args, detect_changed_device, select_device
-from .server import CHAIN_PRIORITY, DEFAULT_GOP, RESERVE_SMS, KindOutput
+from .server import CHAIN_PRIORITY, DEFAULT_GOP, DIST_RESERVE_SMS, KindOutput
 from .volume import AtlasKind, ProbeAtlas
 
 
@@ -522,7 +522,7 @@ class DistributedFrame:
         self.updater = ProbeUpdater(volume, scene, rays_per_probe=rays_per_probe, device=device,
                                     probe_range=self.ranges[rank],
                                     atlas_buffers=2 if overlap else 1,
-                                    reserve_sms=probe_kwargs.pop("reserve_sms", RESERVE_SMS) if overlap else 0, **probe_kwargs)
+                                    reserve_sms=probe_kwargs.pop("reserve_sms", DIST_RESERVE_SMS) if overlap else 0, **probe_kwargs)
         # shadow maps: each rank traces 1/world of the texels; peer mode stores
         # them into every rank's maps directly, NCCL mode all-gathers them
         if shard_shadows:

@@ -34,11 +34,17 @@ from .volume import AtlasKind, ProbeAtlas, ProbeVolume
 DEFAULT_GOP = 30  # codec.py:46
 # SMs the persistent tracer leaves to the previous frame's stage chains when
 # they overlap (high-priority side streams); tunable via PS_RESERVE_SMS.
-# Measured at C4 (ms/frame, reserve 2 / 4 / 8): N=1 8.31 / 8.26 / 8.38,
-# N=2 - / 4.79 / 4.88, N=4 - / 2.73 / 2.77
-RESERVE_SMS = int(__import__("os").environ.get("PS_RESERVE_SMS", "4"))
+# Measured at C4, round 2 (N=1 ms/frame, reserve 0 / 2 / 4 / 6 / 8): 5.074 /
+# 5.073 / 5.086 / 5.123 / 5.165; the z-slab ranks (distributed.py) keep 4
+# (round 1, N=2 reserve 4 / 8: 4.79 / 4.88, N=4: 2.73 / 2.77)
+RESERVE_SMS = int(__import__("os").environ.get("PS_RESERVE_SMS", "2"))
+DIST_RESERVE_SMS = int(__import__("os").environ.get("PS_RESERVE_SMS", "4"))
 # stream priority of the per-kind stage chains (-1 = high, 0 = as the trace)
 CHAIN_PRIORITY = int(__import__("os").environ.get("PS_CHAIN_PRIORITY", "-1"))
+# optional own stream (at this priority) for stages 1-2, so the trace can
+# outrank the chains (tuning knob; unset = the caller's current stream)
+_MAIN_PRIORITY = __import__("os").environ.get("PS_MAIN_PRIORITY")
+MAIN_PRIORITY = int(_MAIN_PRIORITY) if _MAIN_PRIORITY not in (None, "") else None
 
 
 @dataclass
@@ -266,6 +272,8 @@ class ProbeStreamServer:
                                      threshold=visibility_threshold, gop_length=gop_length,
                                      budget=budget, probes_per_row=ppr, encode=encode,
                                      stream_id=2)
+        self.main_stream = (torch.cuda.Stream(self.device, priority=MAIN_PRIORITY)
+                            if overlap and MAIN_PRIORITY is not None else None)
         self.seq = 0
         self.timers = None
         self.enable_graphs(graphs)
@@ -289,6 +297,16 @@ class ProbeStreamServer:
         With ``overlap`` the outputs are produced on ``self.streams[kind]``;
         call ``join()`` (or wait on those streams) before reading them."""
         frame = self.seq if frame is None else frame
+        if self.main_stream is not None:
+            caller = torch.cuda.current_stream(self.device)
+            self.main_stream.wait_stream(caller)
+            with torch.cuda.stream(self.main_stream):
+                outs = self._tick(frame, lights, pvs_bits)
+            caller.wait_stream(self.main_stream)
+            return outs
+        return self._tick(frame, lights, pvs_bits)
+
+    def _tick(self, frame, lights, pvs_bits):
         main = torch.cuda.current_stream(self.device)
         timing = self.timers is not None
         if self.overlap:

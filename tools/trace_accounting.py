@@ -72,6 +72,8 @@ def raw(report):
             vals[key] = x
         elif h.startswith(STALLS) and h.endswith("_per_issue_active.ratio"):
             stalls[h[len(STALLS):-len("_per_issue_active.ratio")]] = x
+    if "thread_inst" not in vals and "threads_per_inst" in vals:
+        vals["thread_inst"] = vals["threads_per_inst"] * vals["warp_inst"]
     return row[kn], vals, stalls
 
 
@@ -105,12 +107,12 @@ def main():
         "thread_inst": v["thread_inst"] / rays,
         "warp_inst_per_chunk": v["warp_inst"] / chunks,
         "global_ld_inst_per_chunk": v.get("global_ld_inst", 0) / chunks,
-        "global_ld_requests": v["global_ld_requests"] / rays,
-        "global_ld_sectors": v["global_ld_sectors"] / rays,
-        "l1_data_wavefronts": v["l1_data_wavefronts"] / rays,
-        "local_bytes": 32 * (v["local_ld_sectors"] + v["local_st_sectors"]) / rays,
+        "global_ld_requests": v.get("global_ld_requests", 0) / rays,
+        "global_ld_sectors": v.get("global_ld_sectors", 0) / rays,
+        "l1_data_wavefronts": v.get("l1_data_wavefronts", 0) / rays,
+        "local_bytes": 32 * (v.get("local_ld_sectors", 0) + v.get("local_st_sectors", 0)) / rays,
         "local_inst_per_chunk": (v.get("local_ld_inst", 0) + v.get("local_st_inst", 0)) / chunks,
-        "l2_read_bytes": 32 * v["l2_read_sectors"] / rays,
+        "l2_read_bytes": 32 * v.get("l2_read_sectors", 0) / rays,
         "dram_bytes": (v.get("dram_read_bytes", 0) + v.get("dram_write_bytes", 0)) / rays,
     }
     tot = sum(ops.values())
