@@ -8,6 +8,7 @@
 //   visibility : 12 texels (48 B)      -> 16 uint8 per plane  (48 stream bytes)
 // so the SKIP decision of a block is an OR over the 16 threads that own its
 // rows, and every byte is read once and written once (HBM-bound).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cstdlib>
@@ -556,6 +557,107 @@ __global__ void __launch_bounds__(256) pack_delta_vis_flat_kernel(PackArgs a) {
     }
 }
 
+// The flat-word kernel with one thread-block cluster per 16-row band (a
+// codec block row): a band's bytes [16 by pw, 16 (by + 1) pw) of each plane
+// are pw whole 16-byte words, so the band's SKIP row can be reduced on chip:
+// the BAND_CL CTAs of the cluster split the band's words and OR dirty bits
+// (per plane and block column) into the leader CTA's shared memory over
+// DSMEM; the leader writes the SKIP row once -- no SKIP memset launch and no
+// racing byte stores.  Needs h % 16 == 0 (update atlases).
+constexpr int BAND_CL = 4;
+constexpr int BAND_THREADS = 256;
+
+__global__ void __launch_bounds__(BAND_THREADS) pack_delta_vis_band_kernel(PackArgs a) {
+    namespace cg = cooperative_groups;
+    extern __shared__ uint32_t s_dirty[];  // [3][ceil(nseg / 32)], used in the leader
+    cg::cluster_group cl = cg::this_cluster();
+    const uint32_t rank = cl.block_rank();
+    const bool key = a.key_dev && *a.key_dev;
+    const uint8_t *prev = key ? nullptr : a.prev;
+    const uint32_t pw = uint32_t(a.pw), h = uint32_t(a.h);
+    const uint32_t T = h * pw;
+    const uint32_t nseg = uint32_t(a.nseg), nsw = (nseg + 31) / 32;
+    const uint32_t by = blockIdx.x / BAND_CL;
+    const bool track = a.skip && prev;
+    if (rank == 0 && track)
+        for (uint32_t i = threadIdx.x; i < 3 * nsw; i += blockDim.x) s_dirty[i] = 0u;
+    cl.sync();
+    uint32_t *dirty = cl.map_shared_rank(s_dirty, 0);
+    const uint32_t q = (pw + BAND_CL - 1) / BAND_CL;
+    const uint32_t w_end = by * pw + min(pw, (rank + 1) * q);
+    for (uint32_t W = by * pw + rank * q + threadIdx.x; W < w_end; W += blockDim.x) {
+        const uint32_t f0 = 16 * W;
+        const uint32_t r = f0 / pw, x0 = f0 - r * pw;
+        const int n1 = int(pw - x0 < 16 ? pw - x0 : 16);  // bytes in row r
+        // previous planes first: their loads overlap the texel gather
+        const bool need_prev = prev && (a.residual || track);
+        uint4 pv[3];
+#pragma unroll
+        for (int e = 0; e < 3; ++e)
+            pv[e] = need_prev ? __ldg(reinterpret_cast<const uint4 *>(prev + size_t(e) * T + f0))
+                              : make_uint4(0u, 0u, 0u, 0u);
+        uint32_t o[3][4];
+        vis_segment(a, int(r), int(x0), o);
+        if (n1 < 16) {  // the word runs into row r + 1 (same band)
+            uint32_t o2[3][4];
+            vis_segment(a, int(r) + 1, -n1, o2);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t m = byte_mask_word(j, 0, n1);
+#pragma unroll
+                for (int e = 0; e < 3; ++e) o[e][j] = (o[e][j] & m) | (o2[e][j] & ~m);
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < 3; ++e) {
+            const size_t off = size_t(e) * T + f0;
+            *reinterpret_cast<uint4 *>(a.cur + off) = make_uint4(o[e][0], o[e][1], o[e][2], o[e][3]);
+            if (!prev) {
+                if (a.residual)
+                    *reinterpret_cast<uint4 *>(a.residual + off) =
+                        make_uint4(o[e][0], o[e][1], o[e][2], o[e][3]);
+                continue;
+            }
+            if (!need_prev) continue;
+            const uint32_t pw4[4] = {pv[e].x, pv[e].y, pv[e].z, pv[e].w};
+            if (a.residual)
+                *reinterpret_cast<uint4 *>(a.residual + off) =
+                    make_uint4(__vsub4(o[e][0], pw4[0]), __vsub4(o[e][1], pw4[1]),
+                               __vsub4(o[e][2], pw4[2]), __vsub4(o[e][3], pw4[3]));
+            if (!track) continue;
+            uint32_t d[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) d[j] = o[e][j] ^ pw4[j];
+            if ((d[0] | d[1] | d[2] | d[3]) == 0u) continue;
+            // bytes [lo, hi) of the word: columns xa + (b - lo) of one row
+            auto mark = [&](uint32_t xa, int lo, int hi) {
+                const uint32_t bxa = xa >> 4, bxb = (xa + uint32_t(hi - lo) - 1) >> 4;
+                for (uint32_t bx = bxa; bx <= bxb; ++bx) {
+                    const int blo = lo + int(bx * 16 > xa ? bx * 16 - xa : 0);
+                    const int bhi = lo + int((bx + 1) * 16 - xa < uint32_t(hi - lo)
+                                                 ? (bx + 1) * 16 - xa : uint32_t(hi - lo));
+                    bool dv = false;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) dv |= (d[j] & byte_mask_word(j, blo, bhi)) != 0u;
+                    if (dv) atomicOr(dirty + e * nsw + (bx >> 5), 1u << (bx & 31));
+                }
+            };
+            mark(x0, 0, n1);
+            if (n1 < 16) mark(0, n1, 16);
+        }
+    }
+    cl.sync();  // every CTA's dirty bits have landed in the leader
+    if (rank != 0 || !a.skip) return;
+    // SKIP row `by` of every plane: 1 = block identical to the previous frame
+    const uint32_t nby = h / 16;
+    for (uint32_t i = threadIdx.x; i < 3 * nseg; i += blockDim.x) {
+        const uint32_t e = i / nseg, bx = i - e * nseg;
+        const uint8_t sk = track ? uint8_t(((s_dirty[e * nsw + (bx >> 5)] >> (bx & 31)) & 1u) == 0u)
+                                 : uint8_t(0);
+        a.skip[(size_t(e) * nby + by) * nseg + bx] = sk;
+    }
+}
+
 // Generic temporal delta over already-packed planes (elements of 1 or 2 B).
 template <int EB>
 __global__ void __launch_bounds__(TILE_X *TILE_Y)
@@ -653,8 +755,27 @@ int launch_pack_delta(int kind, const void *texels, int64_t h, int64_t w, int64_
     static const bool funnel = getenv("PS_PACK_FUNNEL") != nullptr;  // tuning: old path
     const bool flat = rows_misaligned && !funnel && (h * a.pw) % 16 == 0 && a.pw >= 16 && a.vec_in &&
                       3 * h * a.pw < (int64_t(1) << 31);
+    // one cluster per 16-row band (SKIP reduced on chip) when the bands are
+    // whole; PS_PACK_FLAT selects the grid-stride flat kernel (tuning)
+    static const bool flat_only = getenv("PS_PACK_FLAT") != nullptr;
+    const bool band = !flat_only && h % 16 == 0 && h / 16 * BAND_CL <= 0x7fffffff &&
+                      size_t(3) * size_t(ceil_div(a.nseg, 32)) * 4 <= 48 * 1024;
     if (kind == PS_KIND_COLOR) {
         pack_delta_kernel<PS_KIND_COLOR><<<grid, block, 0, stream>>>(a);
+    } else if (flat && band) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(unsigned(h / 16) * BAND_CL);
+        cfg.blockDim = dim3(BAND_THREADS);
+        cfg.dynamicSmemBytes = size_t(3) * size_t(ceil_div(a.nseg, 32)) * 4;
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = BAND_CL;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        check_cuda(cudaLaunchKernelEx(&cfg, pack_delta_vis_band_kernel, a), "launch band kernel");
     } else if (flat) {
         if (skip) {  // SKIP starts at 1 (block identical) and changed bytes clear it
             const int64_t nby = ceil_div(h, TILE_Y);
