@@ -41,7 +41,7 @@ from .packing import UpdateAtlasLayout, widened_width
 from .probes import ProbeUpdater
 from .scene import DeviceScene
 from .selection import _threshold_args, detect_changed_device, select_device
-from .server import CHAIN_PRIORITY, DEFAULT_GOP, DIST_RESERVE_SMS, KindOutput
+from .server import DEFAULT_GOP, DIST_CHAIN_PRIORITY, DIST_RESERVE_SMS, KindOutput
 from .volume import AtlasKind, ProbeAtlas
 
 
@@ -530,8 +530,8 @@ class DistributedFrame:
                 self.updater.set_shadow_peers(rank, world)
             else:
                 self.updater.shadow_split = (rank, world, None)
-        self.streams = {"color": torch.cuda.Stream(device, priority=CHAIN_PRIORITY),
-                        "visibility": torch.cuda.Stream(device, priority=CHAIN_PRIORITY)}
+        self.streams = {"color": torch.cuda.Stream(device, priority=DIST_CHAIN_PRIORITY),
+                        "visibility": torch.cuda.Stream(device, priority=DIST_CHAIN_PRIORITY)}
         self._buf_done = [[], []]
         self._pending = []
         ppr = self.updater.color.probes_per_row

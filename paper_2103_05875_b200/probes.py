@@ -43,6 +43,7 @@ from __future__ import annotations
 import ctypes
 import functools
 import math
+import os
 
 import numpy as np
 import torch
@@ -116,6 +117,9 @@ def texel_direction_table() -> np.ndarray:
     out[:64, :3] = texel_directions(8).reshape(-1, 3)
     out[64:, :3] = texel_directions(16).reshape(-1, 3)
     return out
+
+
+EARLY_SHADOWS = os.environ.get("PS_EARLY_SHADOWS", "1") != "0"
 
 
 class ProbeUpdater:
@@ -205,6 +209,13 @@ class ProbeUpdater:
 
     def enable_graphs(self, on: bool = True) -> None:
         self.graphs = {} if on else None
+        # early shadow maps (graphed, unsharded): frame f+1's lights copy and
+        # shadow maps replay on a side stream as soon as frame f's trace is
+        # done, so they overlap frame f's blend; the trace of f+1 waits for
+        # them.  PS_EARLY_SHADOWS=0 keeps them inside the frame graph (tuning)
+        self._early = (on and self.shadow_mode == N.PS_SHADOW_MAP and EARLY_SHADOWS)
+        self._shadow_stream = torch.cuda.Stream(self.device) if self._early else None
+        self._trace_done = None
 
     def set_shadow_peers(self, rank: int, world: int, group=None) -> None:
         """Shard the shadow-map pass over the process group through peer
@@ -393,7 +404,7 @@ class ProbeUpdater:
                 s.lights.copy_(self._pinned_lights[k], non_blocking=True)
                 self._issue_peer(self.hysteresis, sl)
             self.graphs[key] = g
-        if g is None:
+        if g is None and not (self._early and sl is None and self.shadow_peer is None):
             # unsharded: one graph; sharded shadow maps: graph (inputs, weights, map
             # slice) -> eager NCCL all-gather -> graph (trace, blend)
             g = [torch.cuda.CUDAGraph()] + ([torch.cuda.CUDAGraph()] if sl is not None else [])
@@ -405,15 +416,61 @@ class ProbeUpdater:
                 with torch.cuda.graph(g[1], capture_error_mode="thread_local"):
                     self._issue_post(self.hysteresis)
             self.graphs[key] = g
-        g[0].replay()
-        if len(g) > 1:
-            self._gather_shadow(sl)
-            g[1].replay()
+        if g is None and self._early and sl is None and self.shadow_peer is None:
+            g = self._capture_early(k)
+            self.graphs[key] = g
+        if isinstance(g, dict):
+            self._replay_early(g)
+        else:
+            g[0].replay()
+            if len(g) > 1:
+                self._gather_shadow(sl)
+                g[1].replay()
         evt = torch.cuda.Event()
         evt.record(torch.cuda.current_stream(self.device))
         self._graph_evt[k] = evt
         self.frames_done += 1
         return self.color, self.visibility
+
+    def _capture_early(self, k: int) -> dict:
+        """Three graphs for pinned parity k: shadow (lights H2D + shadow maps),
+        trace (ray table H2D + weights + trace), blend."""
+        s, h = self.dscene, self.hysteresis
+        g = {"shadow": torch.cuda.CUDAGraph(), "trace": torch.cuda.CUDAGraph(),
+             "blend": torch.cuda.CUDAGraph()}
+        with torch.cuda.graph(g["shadow"], capture_error_mode="thread_local"):
+            s.lights.copy_(self._pinned_lights[k], non_blocking=True)
+            N.call("ps_trace_blend", ctypes.byref(self._params(h, passes=1)),
+                   D.stream_ptr(self.device))
+        with torch.cuda.graph(g["trace"], capture_error_mode="thread_local"):
+            self.ray_dirs.copy_(self._pinned_dirs[k], non_blocking=True)
+            stream = D.stream_ptr(self.device)
+            N.call("ps_blend_weights", self.ray_dirs.data_ptr(), self.rays_per_probe,
+                   self.texdir.data_ptr(), self.sharpness, self.w_color.data_ptr(),
+                   self.w_depth.data_ptr(), self.inv_wsum.data_ptr(), D.ptr(self.w_image), stream)
+            N.call("ps_trace_blend", ctypes.byref(self._params(h, passes=2)), stream)
+        with torch.cuda.graph(g["blend"], capture_error_mode="thread_local"):
+            N.call("ps_trace_blend", ctypes.byref(self._params(h, passes=4)),
+                   D.stream_ptr(self.device))
+        return g
+
+    def _replay_early(self, g: dict) -> None:
+        main = torch.cuda.current_stream(self.device)
+        side = self._shadow_stream
+        # the maps and the lights buffer are free once the last trace is done
+        if self._trace_done is not None:
+            side.wait_event(self._trace_done)
+        else:
+            side.wait_stream(main)
+        with torch.cuda.stream(side):
+            g["shadow"].replay()
+        shadows_done = torch.cuda.Event()
+        shadows_done.record(side)
+        main.wait_event(shadows_done)
+        g["trace"].replay()
+        self._trace_done = torch.cuda.Event()
+        self._trace_done.record(main)
+        g["blend"].replay()
 
     def update(self, frame: int | None = None, lights=None):
         """Trace + blend one frame; returns (colour atlas, visibility atlas)."""

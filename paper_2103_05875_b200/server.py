@@ -39,12 +39,18 @@ DEFAULT_GOP = 30  # codec.py:46
 # (round 1, N=2 reserve 4 / 8: 4.79 / 4.88, N=4: 2.73 / 2.77)
 RESERVE_SMS = int(__import__("os").environ.get("PS_RESERVE_SMS", "2"))
 DIST_RESERVE_SMS = int(__import__("os").environ.get("PS_RESERVE_SMS", "4"))
-# stream priority of the per-kind stage chains (-1 = high, 0 = as the trace)
-CHAIN_PRIORITY = int(__import__("os").environ.get("PS_CHAIN_PRIORITY", "-1"))
-# optional own stream (at this priority) for stages 1-2, so the trace can
-# outrank the chains (tuning knob; unset = the caller's current stream)
-_MAIN_PRIORITY = __import__("os").environ.get("PS_MAIN_PRIORITY")
-MAIN_PRIORITY = int(_MAIN_PRIORITY) if _MAIN_PRIORITY not in (None, "") else None
+# Stream priorities (-1 = high, 0 = default).  One GPU: stages 1-2 run on the
+# server's own high-priority stream and the stage chains at default priority,
+# so after the trace the blend (and the early shadow maps, probes.py) are
+# scheduled ahead of the previous frame's leftover chain kernels (C4 N=1, with
+# early shadow maps: 5.050 ms with the chains high, 5.043 with the trace high).
+# The z-slab ranks (distributed.py) keep their chains high.  PS_MAIN_PRIORITY=
+# "" runs stages 1-2 on the caller's current stream.
+_env = __import__("os").environ
+CHAIN_PRIORITY = int(_env.get("PS_CHAIN_PRIORITY", "0"))
+DIST_CHAIN_PRIORITY = int(_env.get("PS_CHAIN_PRIORITY", "-1"))
+_MAIN_PRIORITY = _env.get("PS_MAIN_PRIORITY", "-1")
+MAIN_PRIORITY = int(_MAIN_PRIORITY) if _MAIN_PRIORITY != "" else None
 
 
 @dataclass
