@@ -362,7 +362,12 @@ def run_ours(args, rank, world, local):
         "run": {
             "slabs": ([[int(b), int(e)] for b, e in slabs] if slabs and world > 1 else None),
             "rank_trace_blend_ms": rank_trace if world > 1 else None,
-            "launch": "eager" if args.eager else "CUDA graphs (trace+blend, one chain per kind)",
+            "launch": "eager" if args.eager else (
+                "CUDA graphs (shadow maps on a side stream overlapping the previous blend; "
+                "trace; blend; one chain per kind)"
+                if getattr(getattr(server.impl, "updater", None), "_early", False)
+                else "CUDA graphs (trace+blend, one chain per kind)"),
+            "reserved_sms": getattr(getattr(server.impl, "updater", None), "reserve_sms", None),
             "exchange": (("peer memory (CUDA IPC over NVLink)"
                           if getattr(getattr(server.impl, "color", None), "peer", False)
                           else "NCCL") if world > 1 else None),

@@ -178,7 +178,9 @@ class SlabServer:
         impl.enable_stage_timers(True)
         for k in range(frames):
             impl.tick(first_frame + k, lights_for(first_frame + k))
-        torch.cuda.synchronize(self.device)
+            # one frame at a time: the next frame's early shadow maps (probes.py)
+            # would otherwise run beside this frame's stage chains
+            torch.cuda.synchronize(self.device)
         t = impl.stage_times_ms()
         impl.enable_stage_timers(False)
         if overlap:

@@ -65,3 +65,42 @@ def test_graphed_server_bit_identical(mods, budget, overlap):
             assert torch.equal(ka.last_sent_seq, kb.last_sent_seq), f
     assert len(graphed.updater.graphs) >= 1
     assert len(graphed.color.graphs) >= 1
+
+
+def test_graphed_server_async_frames_match_eager(mods):
+    """Frames issued back to back without host syncs (the bench's pattern:
+    early shadow maps on their side stream overlapping the previous blend,
+    chains overlapping the next trace): every frame's outputs, snapshotted
+    on the stream that produced them, equal the eager server's."""
+    _, scene, server = mods
+    sc = scene.cornell_box()
+    vol = scene.volume_for(sc, (8, 8, 8))
+    kw = dict(rays_per_probe=64, gop_length=4, irradiance_scale=2.0, shadow_map_size=64)
+    eager = server.ProbeStreamServer(vol, sc, **kw)
+    graphed = server.ProbeStreamServer(vol, sc, graphs=True, **kw)
+    frames = 10
+    snaps = []
+    for f in range(frames):
+        lights = scene.moving_light(sc, f, period=5).lights
+        outs = graphed.tick(f, lights)
+        snap = []
+        for kind, o in zip(("color", "visibility"), outs):
+            with torch.cuda.stream(graphed.output_stream(kind)):
+                n = o.entry_count.clone()
+                snap.append((n, o.entries.clone(), o.planes.clone(), o.residual.clone(),
+                             o.skip.clone()))
+        snaps.append(snap)
+    graphed.join()
+    torch.cuda.synchronize()
+    for f in range(frames):
+        lights = scene.moving_light(sc, f, period=5).lights
+        ref = eager.tick(f, lights)
+        eager.join()
+        torch.cuda.synchronize()
+        for (n, ent, planes, res, skip), b in zip(snaps[f], ref):
+            m = int(b.entry_count.item())
+            assert int(n.item()) == m, f
+            assert torch.equal(ent[:m], b.entries[:m]), f
+            assert _same(planes, b.planes), f
+            assert _same(res, b.residual), f
+            assert _same(skip, b.skip), f
