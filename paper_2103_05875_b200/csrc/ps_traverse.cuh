@@ -96,11 +96,33 @@ __device__ __forceinline__ void cswap(float &da, int &ca, float &db, int &cb) {
 // them instead of seven 16-byte loads; with coherent warps (one ray direction
 // over a probe tile) the lanes share node lines, so fewer load instructions
 // per node are fewer L1 wavefronts
+// PS_TRACE_L1_HINT (tuning): 1 = node loads L1::evict_last and triangle loads
+// L1::evict_first, 2 = node loads evict_last only
+#ifndef PS_TRACE_L1_HINT
+#define PS_TRACE_L1_HINT 0
+#endif
 __device__ __forceinline__ void ldg256(const void *p, float (&v)[8]) {
+#if PS_TRACE_L1_HINT >= 1
+    asm("ld.global.nc.L1::evict_last.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+#else
     asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+#endif
         : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]),
           "=f"(v[7])
         : "l"(p));
+}
+
+// triangle record load (see PS_TRACE_L1_HINT)
+__device__ __forceinline__ float4 ldg_tri(const float4 *p) {
+#if PS_TRACE_L1_HINT == 1
+    float4 v;
+    asm("ld.global.nc.L1::evict_first.v4.f32 {%0, %1, %2, %3}, [%4];"
+        : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+        : "l"(p));
+    return v;
+#else
+    return __ldg(p);
+#endif
 }
 
 __device__ __forceinline__ void node4_hits(const float4 *nodes, int node, float ix, float iy,
@@ -662,9 +684,9 @@ __device__ int traverse_spec(const float4 *__restrict__ nodes, const float4 *__r
                 st_tris += cnt;
             }
             for (int k = 0; k < cnt; ++k) {
-                const float t = tri_hit(r, __ldg(tris + 3 * (first + k)),
-                                        __ldg(tris + 3 * (first + k) + 1),
-                                        __ldg(tris + 3 * (first + k) + 2));
+                const float t = tri_hit(r, ldg_tri(tris + 3 * (first + k)),
+                                        ldg_tri(tris + 3 * (first + k) + 1),
+                                        ldg_tri(tris + 3 * (first + k) + 2));
                 if (t < t_best) {
                     t_best = t;
                     hit_slot = first + k;
