@@ -77,20 +77,26 @@ __device__ __forceinline__ int cube_texel(float vx, float vy, float vz, int S) {
 
 template <int SHADOW, int WIDTH>
 __device__ Shade shade_hit(const ps_trace_params &p, const float4 *nodes, const float4 *tris,
-                           const Ray &ray, int slot, float t);
+                           const Ray &ray, int slot, float t, float3 shift);
 
+// the ray is moved into the BVH frame once; only that copy lives through the
+// traversal, and the hit point goes back to world coordinates by the frame
+// origin, reloaded afterwards (keeps the loop at 48 registers without spills)
 template <int SHADOW, int LEAFV, int WIDTH, int STATS = 0>
 __device__ Shade shade_ray(const ps_trace_params &p, const float4 *nodes, const float4 *tris,
                            const Ray &ray) {
     float t;
-    const int slot = traverse<false, LEAFV, WIDTH, STATS>(nodes, tris, ray, INFINITY, t);
-    return shade_hit<SHADOW, WIDTH>(p, nodes, tris, ray, slot, t);
+    const Ray rt = to_bvh_frame(nodes, ray);
+    const int slot = traverse_impl<false, LEAFV, WIDTH, STATS>(nodes, tris, rt, INFINITY, t);
+    const float4 org = __ldg(nodes - 4);
+    return shade_hit<SHADOW, WIDTH>(p, nodes, tris, rt, slot, t, make_float3(org.x, org.y, org.z));
 }
 
-// radiance + depth of a ray given its nearest hit (slot < 0: miss)
+// radiance + depth of a ray given its nearest hit (slot < 0: miss); the hit
+// point is ray.o + t ray.d + shift in world coordinates
 template <int SHADOW, int WIDTH>
 __device__ Shade shade_hit(const ps_trace_params &p, const float4 *nodes, const float4 *tris,
-                           const Ray &ray, int slot, float t) {
+                           const Ray &ray, int slot, float t, float3 shift) {
     Shade s;
     s.shadow_mask = 0;
     if (slot < 0) {
@@ -112,7 +118,8 @@ __device__ Shade shade_hit(const ps_trace_params &p, const float4 *nodes, const 
         ny = -ny;
         nz = -nz;
     }
-    const float hx = fmaf(ray.dx, t, ray.ox), hy = fmaf(ray.dy, t, ray.oy), hz = fmaf(ray.dz, t, ray.oz);
+    const float hx = fmaf(ray.dx, t, ray.ox) + shift.x, hy = fmaf(ray.dy, t, ray.oy) + shift.y,
+                hz = fmaf(ray.dz, t, ray.oz) + shift.z;
     const float sx = fmaf(nx, p.normal_bias, hx), sy = fmaf(ny, p.normal_bias, hy),
                 sz = fmaf(nz, p.normal_bias, hz);
     float lr = 0.f, lg = 0.f, lb = 0.f;
@@ -413,6 +420,7 @@ __global__ void __launch_bounds__(THREADS, MINB) trace_ww_kernel(ps_trace_params
     bool has_ray = false;
     bool queue_done = false;
     Ray ray{0.f, 0.f, 0.f, 0.f, 0.f, 1.f};
+    Ray rt = ray;  // the ray in the BVH frame (ps_traverse.cuh to_bvh_frame)
     float ix = 0.f, iy = 0.f, iz = 0.f, oix = 0.f, oiy = 0.f, oiz = 0.f, tb = 0.f;
     int hit = -1;
     int node = WW_SENTINEL, leaf = 0, sp = 0;
@@ -422,7 +430,8 @@ __global__ void __launch_bounds__(THREADS, MINB) trace_ww_kernel(ps_trace_params
         // ---- finished rays: shade + write; then refill from the queue ----------------
         const bool idle = node == WW_SENTINEL;
         if (idle && has_ray) {
-            const Shade sh = shade_hit<SHADOW, 2>(prm, nodes, tris, ray, hit, tb);
+            const Shade sh = shade_hit<SHADOW, 2>(prm, nodes, tris, ray, hit, tb,
+                                                  make_float3(0.f, 0.f, 0.f));
             records[ray_id] = make_float4(sh.r, sh.g, sh.b, sh.depth);
             if (prm.ray_records) {
                 float4 *rec = reinterpret_cast<float4 *>(prm.ray_records) + 2 * int64_t(ray_id);
@@ -461,9 +470,10 @@ __global__ void __launch_bounds__(THREADS, MINB) trace_ww_kernel(ps_trace_params
                     ix = 1.0f / sx;
                     iy = 1.0f / sy;
                     iz = 1.0f / sz;
-                    oix = ray.ox * ix;
-                    oiy = ray.oy * iy;
-                    oiz = ray.oz * iz;
+                    rt = to_bvh_frame(nodes, ray);
+                    oix = rt.ox * ix;
+                    oiy = rt.oy * iy;
+                    oiz = rt.oz * iz;
                     tb = INFINITY;
                     hit = -1;
                     node = 0;
@@ -512,13 +522,13 @@ __global__ void __launch_bounds__(THREADS, MINB) trace_ww_kernel(ps_trace_params
                         b1 = __ldg(tris + 3 * (first + k + 1) + 1);
                         b2 = __ldg(tris + 3 * (first + k + 1) + 2);
                     }
-                    float t = tri_hit(ray, a0, a1, a2);
+                    float t = tri_hit(rt, a0, a1, a2);
                     if (t < tb) {
                         tb = t;
                         hit = first + k;
                     }
                     if (two) {
-                        t = tri_hit(ray, b0, b1, b2);
+                        t = tri_hit(rt, b0, b1, b2);
                         if (t < tb) {
                             tb = t;
                             hit = first + k + 1;

@@ -711,8 +711,8 @@ __device__ int traverse_spec(const float4 *__restrict__ nodes, const float4 *__r
 }
 
 template <bool ANY_HIT, int LEAFV = 0, int WIDTH = 2, int STATS = 0>
-__device__ int traverse(const float4 *__restrict__ nodes, const float4 *__restrict__ tris,
-                        const Ray &r, float tmax, float &t_best) {
+__device__ int traverse_impl(const float4 *__restrict__ nodes, const float4 *__restrict__ tris,
+                             const Ray &r, float tmax, float &t_best) {
     if constexpr (WIDTH == 16) return traverse8<ANY_HIT, STATS>(nodes, tris, r, tmax, t_best);
     if constexpr (WIDTH == 19) return traverse_spec<ANY_HIT>(nodes, tris, r, tmax, t_best);
     if constexpr (WIDTH == 20) return traverse_spec<ANY_HIT, 1>(nodes, tris, r, tmax, t_best);
@@ -729,14 +729,14 @@ __device__ int traverse(const float4 *__restrict__ nodes, const float4 *__restri
     const int oct = (sx < 0.0f ? 1 : 0) | (sy < 0.0f ? 2 : 0) | (sz < 0.0f ? 4 : 0);
     if constexpr (WIDTH == 7) {
         switch (oct) {
-            case 0: return traverse<ANY_HIT, LEAFV, 8, STATS>(nodes, tris, r, tmax, t_best);
-            case 1: return traverse<ANY_HIT, LEAFV, 9, STATS>(nodes, tris, r, tmax, t_best);
-            case 2: return traverse<ANY_HIT, LEAFV, 10, STATS>(nodes, tris, r, tmax, t_best);
-            case 3: return traverse<ANY_HIT, LEAFV, 11, STATS>(nodes, tris, r, tmax, t_best);
-            case 4: return traverse<ANY_HIT, LEAFV, 12, STATS>(nodes, tris, r, tmax, t_best);
-            case 5: return traverse<ANY_HIT, LEAFV, 13, STATS>(nodes, tris, r, tmax, t_best);
-            case 6: return traverse<ANY_HIT, LEAFV, 14, STATS>(nodes, tris, r, tmax, t_best);
-            default: return traverse<ANY_HIT, LEAFV, 15, STATS>(nodes, tris, r, tmax, t_best);
+            case 0: return traverse_impl<ANY_HIT, LEAFV, 8, STATS>(nodes, tris, r, tmax, t_best);
+            case 1: return traverse_impl<ANY_HIT, LEAFV, 9, STATS>(nodes, tris, r, tmax, t_best);
+            case 2: return traverse_impl<ANY_HIT, LEAFV, 10, STATS>(nodes, tris, r, tmax, t_best);
+            case 3: return traverse_impl<ANY_HIT, LEAFV, 11, STATS>(nodes, tris, r, tmax, t_best);
+            case 4: return traverse_impl<ANY_HIT, LEAFV, 12, STATS>(nodes, tris, r, tmax, t_best);
+            case 5: return traverse_impl<ANY_HIT, LEAFV, 13, STATS>(nodes, tris, r, tmax, t_best);
+            case 6: return traverse_impl<ANY_HIT, LEAFV, 14, STATS>(nodes, tris, r, tmax, t_best);
+            default: return traverse_impl<ANY_HIT, LEAFV, 15, STATS>(nodes, tris, r, tmax, t_best);
         }
     }
     const float ix = 1.0f / sx, iy = 1.0f / sy, iz = 1.0f / sz;
@@ -910,6 +910,25 @@ __device__ int traverse(const float4 *__restrict__ nodes, const float4 *__restri
     return hit_slot;
 }
 
+
+// BVH frame: the node buffer is preceded by a 64-byte header whose first three
+// floats are the origin the BVH (boxes and triangle records) was built
+// around (scene.py DeviceScene: the scene's centre, so fp16 boxes round
+// outward at half the magnitude); rays are translated into that frame for
+// the traversal only -- hit distances are unchanged, shading stays in world
+// coordinates.
+__device__ __forceinline__ Ray to_bvh_frame(const float4 *nodes, const Ray &r) {
+    const float4 org = __ldg(nodes - 4);
+    return Ray{r.ox - org.x, r.oy - org.y, r.oz - org.z, r.dx, r.dy, r.dz};
+}
+
+template <bool ANY_HIT, int LEAFV = 0, int WIDTH = 2, int STATS = 0>
+__device__ __forceinline__ int traverse(const float4 *__restrict__ nodes,
+                                        const float4 *__restrict__ tris, const Ray &r, float tmax,
+                                        float &t_best) {
+    return traverse_impl<ANY_HIT, LEAFV, WIDTH, STATS>(nodes, tris, to_bvh_frame(nodes, r), tmax,
+                                                       t_best);
+}
 
 }  // namespace trav
 }  // namespace ps
