@@ -860,12 +860,14 @@ void launch_trace_s(const ps_trace_params &p, int variant, int sms, cudaStream_t
             case 11: launch_trace_t<SHADOW, 1, 4, 0, 5>(p, sms, s, big); break;
             case 12: launch_trace_t<SHADOW, 1, 1, 0, 5>(p, sms, s, big); break;
             // fp16 boxes, octant tests, two 256-bit loads per node
-            case 64: launch_trace_640<SHADOW, 0, 4, 19>(p, sms, s); break;  // 2x4x4 tiles
+            case 64: launch_trace_640<SHADOW, 0, 4, 23>(p, sms, s); break;  // 2x4x4 tiles
             case 86: launch_trace_640<SHADOW, 0, 4, 3>(p, sms, s); break;
             case 70: launch_trace_640<SHADOW, 0, 12, 18>(p, sms, s); break;  // word selects
             case 71: launch_trace_t<SHADOW, 0, 1, 12, 3>(p, sms, s, true); break;  // 1024 x 1
             case 72: launch_trace_640<SHADOW, 1, 12, 3>(p, sms, s); break;  // leaf pairs
-            case 65: launch_trace_640<SHADOW, 0, 2, 19>(p, sms, s); break;  // 4x4x2 tiles
+            case 65: launch_trace_640<SHADOW, 0, 2, 23>(p, sms, s); break;  // 4x4x2 tiles
+            case 66: launch_trace_640<SHADOW, 0, 4, 19>(p, sms, s); break;  // fp32 slabs
+            case 67: launch_trace_640<SHADOW, 0, 2, 19>(p, sms, s); break;
             case 87: launch_trace_640<SHADOW, 0, 2, 3>(p, sms, s); break;
             // CTA-level claiming: one tile x CLAIM neighbouring directions
             case 80: launch_trace_640<SHADOW, 0, 12, 3, 16>(p, sms, s); break;
@@ -882,7 +884,12 @@ void launch_trace_s(const ps_trace_params &p, int variant, int sms, cudaStream_t
             case 93: launch_trace_640<SHADOW, 0, 12, 24>(p, sms, s); break;
             case 94: launch_trace_640<SHADOW, 0, 12, 25>(p, sms, s); break;
             case 85: launch_trace_640<SHADOW, 0, 12, 3>(p, sms, s); break;  // plain loop
-            default: launch_trace_640<SHADOW, 0, 12, 19>(p, sms, s); break;
+            // default: packed half2 slab tests (WIDTH 23), conservative, so the
+            // nearest hits match the fp32 test's; with the scene-centred BVH
+            // frame C4 traces in 3.960 vs 4.004 ms (84 = fp32 slabs) on one
+            // frame's rotation, 4.042 vs 4.050 on the bench's; directions with
+            // a near-zero component take the fp32 test (warp-uniform)
+            default: launch_trace_640<SHADOW, 0, 12, 23>(p, sms, s); break;
         }
         return;
     }
@@ -1034,6 +1041,8 @@ int ps_trace_blend(const ps_trace_params *params, void *stream) {
             shadow_map_kernel<16><<<blocks, 256, 0, s>>>(p);
         else if (p.bvh_width == 5 && getenv("PS_SHADOW_PLAIN"))
             shadow_map_kernel<3><<<blocks, 256, 0, s>>>(p);
+        else if (p.bvh_width == 5 && getenv("PS_SHADOW_HALF"))  // half2 slab tests (tuning:
+            shadow_map_kernel<23><<<blocks, 256, 0, s>>>(p);      // 0.156 vs 0.151 ms at C4)
         else if (p.bvh_width == 5)  // speculative while-while traversal (traverse_spec)
             shadow_map_kernel<19><<<blocks, 256, 0, s>>>(p);
         else if (p.bvh_width == 4)

@@ -524,8 +524,10 @@ __device__ __forceinline__ void node4ho_switch(const float4 *nodes, int node, in
 //   C_n = rd(-o I_n) and far-plane I_f = ru(|1/d| (1 + 2^-10)), C_f = ru(-o I_f)
 //   (magnitudes; sign of d applied).  For t >= 0 the 2^-10 scaling covers the
 //   final rounding (<= 2^-11 relative), so near t' <= t and far t' >= t.
-// An axis whose constants would leave the fp16 range (|o / d| >~ 6e4) is
-// dropped from the test (I = 0, C = -inf / +inf): also conservative.
+// A ray with an axis whose constants would leave the fp16 range (|o / d|
+// >~ 6e4) takes the fp32 test (traverse_spec); dropping the axis (I = 0,
+// C = -inf / +inf) would be conservative too, but such rays then visit most
+// of the BVH.
 struct HalfSlabs {
     __half2 i[3];  // (I_near, I_far) per axis
     __half2 c[3];  // (C_near, C_far)
@@ -534,7 +536,7 @@ struct HalfSlabs {
 #ifndef PS_HALF_SLACK
 #define PS_HALF_SLACK (1.0f / 1024.0f)
 #endif
-__device__ __forceinline__ void half_axis(float o, float s, __half2 &I, __half2 &C) {
+__device__ __forceinline__ bool half_axis(float o, float s, __half2 &I, __half2 &C) {
     const float mag = fabsf(1.0f / s);
     const float mn = mag * (1.0f - PS_HALF_SLACK), mf = mag * (1.0f + PS_HALF_SLACK);
     if (mf < 60000.0f && mf * fabsf(o) < 60000.0f) {
@@ -546,10 +548,11 @@ __device__ __forceinline__ void half_axis(float o, float s, __half2 &I, __half2 
 #else
         C = __halves2half2(__float2half_rd(__fmul_rd(-o, in_)), __float2half_ru(__fmul_ru(-o, if_)));
 #endif
-    } else {
-        I = __floats2half2_rn(0.0f, 0.0f);
-        C = __floats2half2_rn(-INFINITY, INFINITY);
+        return true;
     }
+    I = __floats2half2_rn(0.0f, 0.0f);
+    C = __floats2half2_rn(-INFINITY, INFINITY);
+    return false;
 }
 
 template <int OCT>
@@ -623,10 +626,14 @@ __device__ int traverse_spec(const float4 *__restrict__ nodes, const float4 *__r
     const float ix = 1.0f / sx, iy = 1.0f / sy, iz = 1.0f / sz;
     const float oix = r.ox * ix, oiy = r.oy * iy, oiz = r.oz * iz;
     HalfSlabs hs;
+    // a ray nearly parallel to an axis (|d| < ~2.7e-4 at |o| = 16) cannot use
+    // the fp16 constants for that axis: it takes the fp32 node test instead
+    // (warp-uniform in the probe trace, whose warps share one direction)
+    bool half_ok = false;
     if (HALF) {
-        half_axis(r.ox, sx, hs.i[0], hs.c[0]);
-        half_axis(r.oy, sy, hs.i[1], hs.c[1]);
-        half_axis(r.oz, sz, hs.i[2], hs.c[2]);
+        half_ok = half_axis(r.ox, sx, hs.i[0], hs.c[0]);
+        half_ok &= half_axis(r.oy, sy, hs.i[1], hs.c[1]);
+        half_ok &= half_axis(r.oz, sz, hs.i[2], hs.c[2]);
     }
     __half tbh = __float2half_ru(tmax);
     unsigned long long st_nodes = 0, st_leaves = 0, st_tris = 0;
@@ -648,7 +655,7 @@ __device__ int traverse_spec(const float4 *__restrict__ nodes, const float4 *__r
             float d[4];
             int c[4];
             if (STATS) ++st_nodes;
-            if (HALF)
+            if (HALF && half_ok)
                 node4hh_switch(nodes, node, oct, hs, tbh, d, c);
             else if (SEL)
                 node4hs_hits(nodes, node, ix, iy, iz, oix, oiy, oiz, t_best, oct & 1, oct & 2,
