@@ -520,10 +520,11 @@ __device__ __forceinline__ void node4ho_switch(const float4 *nodes, int node, in
 // conservative -- a child the exact slab test accepts is never rejected --
 // so the set of tested triangles only grows and the nearest hit (an fp32
 // triangle test) is unchanged:
-//   t' = rn(b * I + C) with, per axis, near-plane  I_n = rd(|1/d| (1 - 2^-10)),
-//   C_n = rd(-o I_n) and far-plane I_f = ru(|1/d| (1 + 2^-10)), C_f = ru(-o I_f)
-//   (magnitudes; sign of d applied).  For t >= 0 the 2^-10 scaling covers the
-//   final rounding (<= 2^-11 relative), so near t' <= t and far t' >= t.
+//   t' = rn(b * I + C) with, per axis, near-plane  I_n = rd(|1/d| (1 - s)),
+//   C_n = rd(-o I_n) and far-plane I_f = ru(|1/d| (1 + s)), C_f = ru(-o I_f)
+//   (magnitudes; sign of d applied).  For t >= 0 the slack s (PS_HALF_SLACK)
+//   covers the final rounding (<= 2^-11 relative), so near t' <= t and far
+//   t' >= t.
 // A ray with an axis whose constants would leave the fp16 range (|o / d|
 // >~ 6e4) takes the fp32 test (traverse_spec); dropping the axis (I = 0,
 // C = -inf / +inf) would be conservative too, but such rays then visit most
@@ -533,8 +534,12 @@ struct HalfSlabs {
     __half2 c[3];  // (C_near, C_far)
 };
 
+// relative slack s of the reciprocals: the final rn rounding of an HFMA2 is
+// within 2^-11 of its result, so (1 - s)(1 + 2^-11) <= 1 <= (1 + s)(1 - 2^-11)
+// needs s >= 2^-11 / (1 - 2^-11); 2^-11 (1 + 2^-8) also covers the fp32
+// rounding of 1/d and of |1/d| (1 -+ s) (2^-24 each)
 #ifndef PS_HALF_SLACK
-#define PS_HALF_SLACK (1.0f / 1024.0f)
+#define PS_HALF_SLACK (1.00390625f / 2048.0f)
 #endif
 __device__ __forceinline__ bool half_axis(float o, float s, __half2 &I, __half2 &C) {
     const float mag = fabsf(1.0f / s);
