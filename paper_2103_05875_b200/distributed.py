@@ -536,12 +536,15 @@ class DistributedFrame:
         self._pending = []
         ppr = self.updater.color.probes_per_row
         # encoder ranks per kind: colour and visibility are separate encoder
-        # streams, so by default they are packed on different ranks (colour on
+        # streams, so at N = 2 they are packed on different ranks (colour on
         # rank 0, visibility on rank 1): the encoder-serial pack of the whole
-        # update atlas, which the other ranks never do, is split over two ranks.
-        # encoder=r puts both on rank r; PS_SPLIT_ENCODERS=0 the same for r = 0.
+        # update atlas, which the other ranks never do, is split over two ranks
+        # (C4: 2.614 vs 2.632 ms).  From N = 4 the peer export traffic into
+        # two encoder ranks costs more than it saves and both kinds stay on
+        # rank 0 (1.488 vs 1.515 ms; profiles/dist_r2/head3).  encoder=r puts
+        # both on rank r; PS_SPLIT_ENCODERS=0 / 1 forces one / two ranks.
         if encoder is None:
-            split = _env_flag("PS_SPLIT_ENCODERS", True) and world > 1
+            split = _env_flag("PS_SPLIT_ENCODERS", world == 2) and world > 1
             encoder = (0, 1 if split else 0)
         elif isinstance(encoder, int):
             encoder = (encoder, encoder)
