@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define PS_ABI_VERSION 9
+#define PS_ABI_VERSION 10
 
 /* status codes */
 #define PS_OK 0
@@ -165,7 +165,8 @@ int ps_bits_to_ids(const uint32_t *bits, int64_t probe_count, int64_t *out_ids,
  * ray_dirs (ray_count, 3) float64 from pvs_rays (frustum grid + fibonacci
  * sphere), camera = pose.position, volume_origin / volume_spacing: HOST
  * pointers to 3 doubles each; vertices (T, 3, 3) float64 on the device
- * (the BVH's source triangles), BVH as built by ps_bvh_build_wide.  Writes
+ * (the BVH's source triangles, world frame), BVH as built by
+ * ps_bvh_build_wide with its frame header before node 0 (see there).  Writes
  * the active-masked cage bitmap and (optionally) ascending ids + count. */
 size_t ps_pvs_workspace_bytes(int64_t probe_count);
 int ps_pvs(const float *nodes, int32_t bvh_width, const float *tris, const double *vertices,
@@ -347,7 +348,15 @@ int ps_bvh_build(const double *vertices, int64_t tri_count, int leaf_size,
  *      references (64-byte nodes; measured slower, kept for comparison);
  *   8  BVH8 with 8-bit quantised boxes (24-float / 96-byte nodes; measured
  *      slower, kept for comparison).
- * Layouts 3 and 8 are documented in csrc/ps_bvh.cpp (emit_bvh4r / emit_bvh8). */
+ * Layouts 3 and 8 are documented in csrc/ps_bvh.cpp (emit_bvh4r / emit_bvh8).
+ *
+ * BVH frame (ABI 10): the builder uses the vertices as given.  The traversal
+ * entry points (ps_trace_blend's `nodes`, ps_pvs) read a 64-byte header
+ * placed immediately BEFORE node 0: its first three floats are the origin
+ * of the frame the BVH was built in (the builder was given vertices minus
+ * that origin; zeros for a world-frame BVH).  Rays are moved into that frame
+ * for the traversal only.  scene.py builds around the scene's centre, which
+ * halves the fp16 boxes' outward rounding. */
 int ps_bvh_build_wide(const double *vertices, int64_t tri_count, int leaf_size, int width,
                       ps_bvh_sizes *sizes, float *nodes_out, float *tris_out);
 
@@ -364,7 +373,8 @@ typedef struct ps_trace_params {
     const float *ray_dirs;
     int32_t rays_per_probe;
     /* scene */
-    const float *nodes;      /* BVH nodes (ps_bvh_build_wide layout) */
+    const float *nodes;      /* BVH node 0 (ps_bvh_build_wide layout), preceded
+                              * by the 64-byte frame header (origin x, y, z) */
     int32_t bvh_width;       /* 2 or 4 */
     const float *tris;       /* triangle records */
     const float *materials;  /* per original triangle, 12 floats: albedo rgb _, emission

@@ -16,7 +16,7 @@ from pathlib import Path
 from .errors import LayoutMismatchError, NativeLibraryError, SlotOverflowError
 
 LIB_PATH = Path(os.environ.get("PROBESTREAM_LIB", Path(__file__).resolve().parent / "libprobestream.so"))
-ABI_VERSION = 9
+ABI_VERSION = 10
 
 PS_OK = 0
 PS_ERR_VALUE = -1
