@@ -96,6 +96,10 @@ __device__ __forceinline__ void cswap(float &da, int &ca, float &db, int &cb) {
 // them instead of seven 16-byte loads; with coherent warps (one ray direction
 // over a probe tile) the lanes share node lines, so fewer load instructions
 // per node are fewer L1 wavefronts
+// PS_TRACE_PREFETCH (tuning): prefetch a parked leaf's triangles into L1
+#ifndef PS_TRACE_PREFETCH
+#define PS_TRACE_PREFETCH 0
+#endif
 // PS_TRACE_L1_HINT (tuning): 1 = node loads L1::evict_last and triangle loads
 // L1::evict_first, 2 = node loads evict_last only
 #ifndef PS_TRACE_L1_HINT
@@ -677,6 +681,13 @@ __device__ int traverse_spec(const float4 *__restrict__ nodes, const float4 *__r
             }
             if (node < TRAV_DONE && leaf == 0) {  // park the leaf, keep walking
                 leaf = node;
+#if PS_TRACE_PREFETCH
+                {  // its triangle records (48 B each) are fetched into L1 meanwhile
+                    const float4 *tp = tris + 3 * ((~leaf) >> 3);
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(tp));
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(tp + 5));
+                }
+#endif
                 node = pop();
             }
             if (VOTE == 0) {
